@@ -1,0 +1,232 @@
+"""Oracle for the MoE-layer arithmetic: float64 restatement on the CPU.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).  PARITY UNPINNED by the
+reference: the reference charges a constant T_l per layer
+(/root/reference/pkg/src/moesim/engine.py:263, :606) and contains no router
+GEMV, softmax weights, SwiGLU experts, permute or combine.
+This module fixes the canonical semantics the product implements (DESIGN.md
+§3) and evaluates them in float64:
+
+  x      = rmsnorm(h)                         (weight 1, eps 1e-6)
+  logits = x . W_r^T                          (fp32 on device)
+  sel    = top-k of (logits + bias * resident) keyed (value desc, index asc)
+  w      = "mixtral": softmax over the k selected raw logits
+           "softmax_topk": softmax over all M raw logits, gathered (no renorm)
+  xe     = T(x); a = T(silu(xe.W1^T) * (xe.W3^T)); y = a.W2^T
+  moe    = sum_r w[t,r] * y[t,r]   (rank order)  [+ gate_t * shared(xe)]
+  h'     = h + moe
+
+Weights come from a counter-based generator (splitmix64 finaliser) that the
+CUDA kernel ``ef_fill_uniform`` reproduces bit for bit, so the oracle can
+regenerate any expert without copying it off the device.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+C1 = np.uint64(0xBF58476D1CE4E5B9)
+C2 = np.uint64(0x94D049BB133111EB)
+MAT_W1, MAT_W3, MAT_W2, MAT_ROUTER, MAT_SHARED_W1, MAT_SHARED_W3, MAT_SHARED_W2, MAT_SHARED_GATE, MAT_INPUT = range(9)
+
+
+def _mix(z: np.ndarray) -> np.ndarray:
+    z = z ^ (z >> np.uint64(30))
+    z = z * C1
+    z = z ^ (z >> np.uint64(27))
+    z = z * C2
+    return z ^ (z >> np.uint64(31))
+
+
+def stream_key(seed: int, layer: int, expert: int, mat: int) -> int:
+    """Key of one weight tensor; mirrored by ef_stream_key() in csrc."""
+    with np.errstate(over="ignore"):
+        tag = np.array([(layer << 32) | (expert << 8) | mat], dtype=np.uint64)
+        s = np.array([seed & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64)
+        return int(_mix(s ^ _mix(tag + GOLDEN))[0])
+
+
+def uniform_scale(var: float) -> np.float32:
+    """fp32 step so that values span U[-a, a) with a^2/3 = var."""
+    return np.float32(math.sqrt(3.0 * var) / 8388608.0)
+
+
+def fill_uniform(key: int, n: int, scale: np.float32, offset: int = 0) -> np.ndarray:
+    """Element i = float32(int24(mix(key + (offset+i+1)*GOLDEN)) - 2^23) * scale."""
+    with np.errstate(over="ignore"):
+        i = np.arange(offset + 1, offset + n + 1, dtype=np.uint64)
+        h = _mix(np.uint64(key) + i * GOLDEN)
+    u = (h >> np.uint64(40)).astype(np.int64) - 8388608
+    return u.astype(np.float32) * np.float32(scale)
+
+
+def to_bf16(a: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16, returned as float32 values."""
+    b = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)
+    return r.astype(np.uint32).view(np.float32)
+
+
+def cast(a: np.ndarray, dtype: str) -> np.ndarray:
+    return to_bf16(a) if dtype == "bf16" else np.asarray(a, dtype=np.float32)
+
+
+class ModelWeights:
+    """Lazily regenerates the synthetic weights of a model shape."""
+
+    def __init__(self, *, L, M, d, ff, dtype, seed, shared_ff=0, shared_gate=False):
+        self.L, self.M, self.d, self.ff, self.dtype, self.seed = L, M, d, ff, dtype, seed
+        self.shared_ff, self.shared_gate = shared_ff, shared_gate
+
+    def _mat(self, layer, expert, mat, rows, cols, fan_in):
+        key = stream_key(self.seed, layer, expert, mat)
+        v = fill_uniform(key, rows * cols, uniform_scale(1.0 / fan_in))
+        return cast(v, self.dtype).reshape(rows, cols)
+
+    def expert(self, layer, e):
+        d, ff = self.d, self.ff
+        return (self._mat(layer, e, MAT_W1, ff, d, d), self._mat(layer, e, MAT_W3, ff, d, d),
+                self._mat(layer, e, MAT_W2, d, ff, ff))
+
+    def router(self, layer):
+        return self._mat(layer, 0, MAT_ROUTER, self.M, self.d, self.d)
+
+    def shared(self, layer):
+        if not self.shared_ff:
+            return None
+        d, ff = self.d, self.shared_ff
+        w1 = self._mat(layer, 0, MAT_SHARED_W1, ff, d, d)
+        w3 = self._mat(layer, 0, MAT_SHARED_W3, ff, d, d)
+        w2 = self._mat(layer, 0, MAT_SHARED_W2, d, ff, ff)
+        g = self._mat(layer, 0, MAT_SHARED_GATE, 1, d, d)[0] if self.shared_gate else None
+        return w1, w3, w2, g
+
+
+def input_hidden(seed: int, step: int, B: int, d: int) -> np.ndarray:
+    """Synthetic decode input h_0 for step ``step``: U with variance 1, fp32."""
+    key = stream_key(seed, step, 0, MAT_INPUT)
+    return fill_uniform(key, B * d, uniform_scale(1.0)).reshape(B, d)
+
+
+def rmsnorm(h: np.ndarray, eps: float = 1e-6) -> np.ndarray:
+    h = np.asarray(h, dtype=np.float64)
+    return h / np.sqrt((h * h).mean(axis=1, keepdims=True) + eps)
+
+
+def router_logits(x: np.ndarray, wr: np.ndarray) -> np.ndarray:
+    return np.asarray(x, np.float64) @ np.asarray(wr, np.float64).T
+
+
+def topk_select(logits: np.ndarray, k: int, bias: float = 0.0,
+                resident: Optional[np.ndarray] = None) -> np.ndarray:
+    """Rank-ordered top-k keyed on fp32 (logit + bias*resident); ties -> low
+    index (selection keys on logits, same order as
+    scheduler.py:56-60 applied to softmax)."""
+    logits = np.asarray(logits, dtype=np.float32)
+    B, M = logits.shape
+    key = logits.copy()
+    if resident is not None and bias != 0.0:
+        key = (key + np.float32(bias) * resident.astype(np.float32)).astype(np.float32)
+    out = np.empty((B, k), dtype=np.int32)
+    for t in range(B):
+        out[t] = sorted(range(M), key=lambda e: (-float(key[t, e]), e))[:k]
+    return out
+
+
+def route_weights(logits: np.ndarray, sel: np.ndarray, mode: str) -> np.ndarray:
+    lg = np.asarray(logits, np.float64)
+    if mode == "mixtral":
+        picked = np.take_along_axis(lg, sel, axis=1)
+        z = np.exp(picked - picked.max(axis=1, keepdims=True))
+        return z / z.sum(axis=1, keepdims=True)
+    z = np.exp(lg - lg.max(axis=1, keepdims=True))
+    p = z / z.sum(axis=1, keepdims=True)
+    return np.take_along_axis(p, sel, axis=1)
+
+
+def permute(sel: np.ndarray, M: int):
+    """Stable permutation by (expert, token, rank): counts, offsets[M+1],
+    perm[B*k] (flat slot t*k+r), inv[B,k] (position of (t,r))."""
+    B, k = sel.shape
+    flat = sel.reshape(-1)
+    counts = np.bincount(flat, minlength=M).astype(np.int32)
+    offsets = np.zeros(M + 1, dtype=np.int32)
+    offsets[1:] = np.cumsum(counts)
+    perm = np.argsort(flat, kind="stable").astype(np.int32)
+    inv = np.empty(B * k, dtype=np.int32)
+    inv[perm] = np.arange(B * k, dtype=np.int32)
+    return counts, offsets, perm, inv.reshape(B, k)
+
+
+def swiglu(xe: np.ndarray, w1, w3, w2, dtype: str) -> np.ndarray:
+    xe = np.asarray(xe, np.float64)
+    g = xe @ np.asarray(w1, np.float64).T
+    u = xe @ np.asarray(w3, np.float64).T
+    a = cast((g / (1.0 + np.exp(-g))) * u, dtype).astype(np.float64)
+    return a @ np.asarray(w2, np.float64).T
+
+
+def moe_layer(h, weights: ModelWeights, layer, k, mode, bias=0.0, resident=None,
+              logits_override=None):
+    """One layer of the canonical MoE forward; returns dict of intermediates."""
+    x = rmsnorm(h)
+    wr = weights.router(layer)
+    logits = router_logits(x, wr)
+    lg32 = np.asarray(logits if logits_override is None else logits_override, np.float32)
+    sel = topk_select(lg32, k, bias, resident)
+    w = route_weights(lg32, sel, mode)
+    xe = cast(x.astype(np.float32), weights.dtype)
+    B = h.shape[0]
+    moe = np.zeros((B, weights.d), dtype=np.float64)
+    ys = {}
+    for e in sorted(set(sel.reshape(-1).tolist())):
+        rows = [t for t in range(B) if e in sel[t]]
+        w1, w3, w2 = weights.expert(layer, e)
+        y = swiglu(xe[rows], w1, w3, w2, weights.dtype)
+        for i, t in enumerate(rows):
+            ys[(t, e)] = y[i]
+    for t in range(B):
+        for r in range(k):
+            moe[t] += w[t, r] * ys[(t, int(sel[t, r]))]
+    sh = weights.shared(layer)
+    if sh is not None:
+        w1, w3, w2, g = sh
+        ysh = swiglu(xe, w1, w3, w2, weights.dtype)
+        if g is not None:
+            gate = 1.0 / (1.0 + np.exp(-(x @ np.asarray(g, np.float64))))
+            ysh = ysh * gate[:, None]
+        moe += ysh
+    return {"x": x, "logits": logits, "sel": sel, "w": w,
+            "h_next": np.asarray(h, np.float64) + moe}
+
+
+def softmax64(logits_row: Sequence[float]) -> List[float]:
+    """Canonical fp64 softmax of fp32 logits: glibc exp (math.exp), sequential
+    sum — the normalisation order SURVEY H6 pins for N_e."""
+    vals = [float(v) for v in logits_row]
+    m = max(vals)
+    ex = [math.exp(v - m) for v in vals]
+    s = 0.0
+    for v in ex:
+        s += v
+    return [v / s for v in ex]
+
+
+def batch_gate(logits: np.ndarray) -> np.ndarray:
+    """Token-weighted batch gate (workload.py:215-223 with per-token groups):
+    mean of per-token softmax64, renormalised by a sequential sum."""
+    B, M = logits.shape
+    w = 1.0 / B
+    mixed = [0.0] * M
+    for t in range(B):
+        p = softmax64(logits[t])
+        for e in range(M):
+            mixed[e] += w * p[e]
+    s = 0.0
+    for v in mixed:
+        s += v
+    return np.array([v / s for v in mixed], dtype=np.float64)
