@@ -1,0 +1,295 @@
+/*
+ * expertflow.h — C ABI of the B200-native ExpertFlow hot path
+ * (libexpertflow.so, built from paper_2510_26730_b200/csrc).
+ *
+ * Plain pointers, sizes and opaque handles only; no torch types.  Device
+ * pointers are CUDA device addresses (e.g. torch.Tensor.data_ptr()), streams
+ * are cudaStream_t passed as void*.  Every entry point returns an int status:
+ *   EF_OK (0), EF_EINVAL (-22, maps to ValueError), EF_ERUNTIME (-1, maps to
+ *   RuntimeError, e.g. the reference's no-forward-progress guard),
+ *   EF_ECUDA (-5, CUDA failure, RuntimeError), EF_ENOMEM (-12).
+ * ef_last_error() returns a thread-local message for the last failure.
+ *
+ * Each function names the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/moesim).  The reference is pure Python; its
+ * "FFI" for this path is the Python call surface, so the binding a
+ * maintainer adds is a ctypes stub.
+ */
+#ifndef EXPERTFLOW_H
+#define EXPERTFLOW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EF_OK 0
+#define EF_ERUNTIME (-1)
+#define EF_ECUDA (-5)
+#define EF_ENOMEM (-12)
+#define EF_EINVAL (-22)
+
+#define EF_TIER_HIGH 1 /* memory.py:24 TIER_HIGH */
+#define EF_TIER_LOW 0  /* memory.py:25 TIER_LOW  */
+
+/* cache event kinds (memory.py:63-65, :83-85) */
+#define EF_EV_MISS 0
+#define EF_EV_HIT 1
+#define EF_EV_ADMIT 2
+#define EF_EV_EVICT 3
+
+const char* ef_last_error(void);
+int ef_abi_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Decision primitives                                                */
+/* ------------------------------------------------------------------ */
+
+/* scheduler.py:36-53 expected_expert_count */
+int ef_expected_expert_count(const double* probs, int m, double cum_threshold, int* out_count);
+/* scheduler.py:56-60 top_experts: ascending indices of the `count` best */
+int ef_top_experts(const double* probs, int m, int count, int* out_sel);
+/* scheduler.py:63-74 swap_in_latency */
+int ef_swap_in_latency(int64_t n, int64_t size, int64_t bw, int64_t* out_ns);
+/* scheduler.py:77-105 compute_step, exact-integer bandwidth path */
+int ef_compute_step_int(int64_t n_e, int64_t size, int64_t bw, int64_t layer_ns, int min_step,
+                        int max_step, int* out_step);
+/* scheduler.py:77-105 compute_step, float-bandwidth path (math.ceil of a double) */
+int ef_compute_step_float(int64_t n_e, int64_t size, double bw, int64_t layer_ns, int min_step,
+                          int max_step, int* out_step);
+
+/* scheduler.py:108-163 StepState / on_stall / on_overfetch */
+typedef struct ef_step_state {
+  int32_t current, max_step, min_step, stall_count, overfetch_count, stall_threshold,
+      overfetch_threshold;
+} ef_step_state;
+int ef_step_validate(const ef_step_state* s);
+int ef_step_on_stall(ef_step_state* s);
+int ef_step_on_overfetch(ef_step_state* s);
+
+/* ------------------------------------------------------------------ */
+/* ExpertCache — memory.py:28-156 (two-tier LRU) + slot table          */
+/* ------------------------------------------------------------------ */
+typedef struct ef_cache ef_cache;
+int ef_cache_create(int64_t capacity_bytes, int64_t expert_size_bytes, int record_events,
+                    ef_cache** out);
+void ef_cache_destroy(ef_cache* c);
+int ef_cache_access(ef_cache* c, int32_t layer, int32_t expert, int64_t now, int* out_hit);
+/* victims written as (layer, expert) pairs; *n_victims may exceed max_victims (then truncated) */
+int ef_cache_admit(ef_cache* c, int32_t layer, int32_t expert, int tier, int64_t now,
+                   int32_t* victims, int max_victims, int* n_victims);
+/* pred: n_pred (layer, expert) pairs */
+int ef_cache_reassign_tiers(ef_cache* c, const int32_t* pred, int n_pred, int64_t recent_window,
+                            int64_t now);
+/* tier: EF_TIER_* or -1 when absent */
+int ef_cache_query(ef_cache* c, int32_t layer, int32_t expert, int* tier, int64_t* last_access);
+/* out: capacity_experts, size, hits, misses, admissions, evictions */
+int ef_cache_counters(ef_cache* c, int64_t out[6]);
+/* resident pairs in (layer, expert) order */
+int ef_cache_resident(ef_cache* c, int32_t* pairs, int max_pairs, int* n);
+/* events as rows (now, kind, layer, expert); returns -1 count when recording is off */
+int ef_cache_events(ef_cache* c, int64_t* rows, int64_t max_rows, int64_t* n);
+
+/* ------------------------------------------------------------------ */
+/* TransferQueue — memory.py:183-202; BandwidthEstimator — :205-236    */
+/* ------------------------------------------------------------------ */
+typedef struct ef_tqueue ef_tqueue;
+int ef_tqueue_create(ef_tqueue** out);
+void ef_tqueue_destroy(ef_tqueue* q);
+int ef_tqueue_enqueue(ef_tqueue* q, int32_t layer, int32_t expert, int priority, int64_t* out_seq);
+/* *found = 0 when empty */
+int ef_tqueue_next(ef_tqueue* q, int32_t* layer, int32_t* expert, int* priority, int64_t* seq,
+                   int* found);
+int ef_tqueue_len(ef_tqueue* q, int64_t* n);
+
+typedef struct ef_bw ef_bw;
+int ef_bw_create(int has_initial, double initial, double alpha, ef_bw** out);
+void ef_bw_destroy(ef_bw* b);
+int ef_bw_observe(ef_bw* b, int64_t bytes, int64_t elapsed_ns, double* out_estimate);
+int ef_bw_estimate(ef_bw* b, double* out);
+
+/* ------------------------------------------------------------------ */
+/* PredictionCache (scheduler.py:194-221) with encoded int64 values    */
+/* ------------------------------------------------------------------ */
+typedef struct ef_pcache ef_pcache;
+int ef_pcache_create(int capacity, ef_pcache** out);
+void ef_pcache_destroy(ef_pcache* p);
+/* key = (tokens[n_tokens], layer, step); value = int64 blob (encoding owned by caller) */
+int ef_pcache_get(ef_pcache* p, const int64_t* tokens, int n_tokens, int64_t layer, int64_t step,
+                  int64_t* val, int64_t max_val, int64_t* n_val, int* found);
+int ef_pcache_put(ef_pcache* p, const int64_t* tokens, int n_tokens, int64_t layer, int64_t step,
+                  const int64_t* val, int64_t n_val);
+int ef_pcache_stats(ef_pcache* p, int64_t out[3]); /* hits, misses, len */
+
+/* ------------------------------------------------------------------ */
+/* Forest inference — predictor.py:195-232, :312-359, :608-632         */
+/* ------------------------------------------------------------------ */
+typedef struct ef_forest ef_forest;
+/* flat node arrays for all trees concatenated; tree_off[n_trees+1] node offsets;
+   value[n_nodes*num_outputs] (leaf rows; ignored for interior nodes) */
+int ef_forest_create(int n_trees, const int64_t* tree_off, const int32_t* feature,
+                     const double* threshold, const int32_t* left, const int32_t* right,
+                     const double* value, int32_t feature_len, int32_t num_outputs, int residual,
+                     ef_forest** out);
+void ef_forest_destroy(ef_forest* f);
+int ef_forest_predict(ef_forest* f, const double* features, const double* baseline /*nullable*/,
+                      double* out_scores);
+/* predictor.py:113-128 inference_features; table row-major [vocab][embed_dim];
+   history given as (layer, n, experts...) records */
+int ef_inference_features(const double* table, int64_t vocab, int32_t embed_dim, int32_t L,
+                          int32_t M, const int64_t* tokens, int n_tokens, int32_t step,
+                          int32_t target, const int32_t* hist, int64_t hist_len, double* out);
+
+/* Prediction ladder — scheduler.py:247-309.  Callbacks stand in for the
+   reference's duck-typed plug points (PredictionQuery.pregate, forest). */
+typedef int (*ef_pregate_cb)(void* user, int32_t layer, int32_t horizon, double* probs_out);
+typedef int (*ef_forest_cb)(void* user, const double* features, int32_t n_features,
+                            const double* baseline /*nullable*/, double* scores_out);
+typedef struct ef_ladder_cfg {
+  int32_t L, M, top_k;
+  double cum_threshold;
+  /* forest: exactly one of native / callback, or neither */
+  ef_forest* forest;
+  ef_forest_cb forest_cb;
+  void* forest_user;
+  int32_t forest_feature_len;
+  const double* table; /* embedding table for features (required with a forest) */
+  int64_t vocab;
+  int32_t embed_dim;
+  ef_pregate_cb pregate_cb; /* nullable */
+  void* pregate_user;
+} ef_ladder_cfg;
+/* out: (target, n, experts...) records, *n_out int64 written */
+int ef_predict_experts(const ef_ladder_cfg* cfg, ef_pcache* cache, const int64_t* tokens,
+                       int n_tokens, int32_t layer, int32_t step, const double* router_probs,
+                       const int32_t* known, int64_t known_len, int64_t* out, int64_t max_out,
+                       int64_t* n_out);
+
+/* engine.py:192-209 route_batch.  groups: (gid, n, experts...) records over one layer;
+   resident: M-bit mask as bytes.  order/deferred receive group ids. */
+int ef_route_batch(const int32_t* groups, int64_t groups_len, const uint8_t* resident_mask,
+                   int32_t M, int32_t* order, int32_t* deferred, int32_t* n_groups,
+                   int32_t* n_deferred);
+
+/* ------------------------------------------------------------------ */
+/* Scheduler stepper — engine.py:240-716 (_Sim / simulate), steppable  */
+/* ------------------------------------------------------------------ */
+typedef struct ef_sim ef_sim;
+typedef struct ef_sim_cfg {
+  int32_t L, M, top_k;
+  int64_t expert_size_bytes, link_bw, device_memory_bytes, layer_ns;
+  /* PolicyConfig, engine.py:95-142 */
+  int32_t strategy;  /* 0 static 1 reactive 2 fixed_interval 3 adaptive */
+  int32_t predictor; /* 0 none 1 pregate 2 forest 3 oracle */
+  int32_t interval, cache_aware_routing, cold_start_preload;
+  double cum_threshold;
+  int32_t stall_threshold, overfetch_threshold, min_step, max_step /* -1 = L-1 */,
+      recent_window /* -1 = S */;
+  int32_t prediction_cache_capacity;
+  int32_t emit_events;
+  uint64_t seed;
+} ef_sim_cfg;
+int ef_sim_create(const ef_sim_cfg* cfg, const ef_ladder_cfg* ladder, ef_sim** out);
+void ef_sim_destroy(ef_sim* s);
+/* One token (= one trace, ActivationTrace workload.py:161-179):
+   gates[L*M] fp64, actual: (n, experts...) per layer, groups: per layer
+   (n_groups, [n, experts...]*), group_sizes[n_groups]. */
+int ef_sim_run_token(ef_sim* s, const int64_t* tokens, int n_tokens, const double* gates,
+                     const int32_t* actual, int64_t actual_len, const int32_t* groups,
+                     int64_t groups_len, const int64_t* group_sizes, int32_t n_groups);
+/* SimMetrics scalars (engine.py:157-189), fixed order documented in simcore.h */
+int ef_sim_metrics(ef_sim* s, int64_t* ints, int32_t n_ints, double* bw_estimate);
+/* variable-length outputs; kind: 0 step_history(2/row) 1 per_layer 2 samples 3 events 4 cache events */
+int ef_sim_output(ef_sim* s, int32_t kind, int64_t* buf, int64_t max_len, int64_t* n);
+/* event detail strings, '\n' separated, in sorted event order */
+int ef_sim_event_details(ef_sim* s, char* buf, int64_t max_len, int64_t* n);
+
+/* ------------------------------------------------------------------ */
+/* Device kernels (sm_100a).  Graph-capturable: no allocation, no sync */
+/* ------------------------------------------------------------------ */
+/* dtype codes */
+#define EF_F32 0
+#define EF_BF16 1
+/* routing conventions */
+#define EF_ROUTE_MIXTRAL 0 /* softmax over the k selected logits */
+#define EF_ROUTE_SOFTMAX_TOPK 1 /* softmax over all M, gathered, no renorm */
+
+/* counter-based synthetic weights (oracle/numerics.py fill_uniform) */
+int ef_fill_uniform(void* stream, void* dst, int dtype, int64_t n, uint64_t key, float scale,
+                    int64_t offset);
+uint64_t ef_stream_key(uint64_t seed, int32_t layer, int32_t expert, int32_t mat);
+
+/* x[B,d] = rmsnorm(h[B,d]) (fp32) */
+int ef_rmsnorm(void* stream, const float* h, float* x, int B, int d, float eps);
+/* (a)+(b): logits[R, B, M] fp32 = x[B,d] . W[rows]^T for R router matrices
+   starting at w (stacked [R, M, d] of dtype) */
+int ef_router_logits(void* stream, const float* x, const void* w, int dtype, int R, int B, int d,
+                     int M, float* logits);
+/* (a) epilogue + (c): top-k keyed on logits (+bias*resident), routing weights,
+   stable permutation.  sel[B,k], wts[B,k], counts[M], offsets[M+1], perm[B*k], inv[B*k] */
+int ef_route_permute(void* stream, const float* logits, int B, int M, int k, int mode,
+                     float bias, uint64_t resident_mask_lo, uint64_t resident_mask_hi,
+                     int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
+                     int32_t* perm, int32_t* inv);
+/* (d) decode expert FFN over a slot-indirected slab.
+   Active list: n_active entries of (slot, row_offset, n_rows) into perm.
+   Slot s holds [W1 ff*d | W3 ff*d | W2 d*ff] at slab + s*slot_stride_bytes.
+   Row p of the permuted batch reads x[perm[p]/k]; output y[p, d] fp32.
+   act is scratch [rows_total, ff] of dtype. */
+int ef_expert_ffn_decode(void* stream, const float* x, const int32_t* perm, int k,
+                         const void* slab, int64_t slot_stride_bytes, const int32_t* act_slot,
+                         const int32_t* act_off, const int32_t* act_rows, int n_active, int d,
+                         int ff, int dtype, void* act, float* y);
+/* (c) unpermute + weighted combine (rank order) + optional shared expert +
+   residual + next rmsnorm:  h[t] += sum_r wts[t,r]*y[inv[t,r]] + g_t*ys[t];
+   x = rmsnorm(h).  ys/shared_gate nullable. */
+int ef_combine(void* stream, float* h, float* x, const float* y, const int32_t* inv,
+               const float* wts, const float* ys, const float* shared_gate_logit, int B, int d,
+               int k, float eps);
+
+/* ------------------------------------------------------------------ */
+/* MoE decode engine: slab + pinned host store + copy streams + stepper */
+/* ------------------------------------------------------------------ */
+typedef struct ef_engine ef_engine;
+typedef struct ef_engine_cfg {
+  int32_t L, M, top_k, d, ff, dtype, route_mode, max_batch;
+  int32_t shared_ff, shared_gate; /* 0 = no shared expert */
+  int64_t budget_slots;           /* logical cache capacity in experts */
+  int32_t staging_slots;          /* extra physical slots (landing + pinned), >= 1 */
+  float routing_bias;             /* cache-aware logit bias (0 = off) */
+  uint64_t seed;
+  int32_t device;
+  int32_t timing; /* record per-layer stall events (physical stall %) */
+  int32_t record_routing; /* keep every layer's logits / selection for parity checks */
+} ef_engine_cfg;
+int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim, const ef_ladder_cfg* ladder,
+                     ef_engine** out);
+void ef_engine_destroy(ef_engine* e);
+/* one decode step: h[B,d] fp32 device in/out, on `stream` */
+int ef_engine_step(ef_engine* e, void* stream, float* h, int B, const int64_t* tokens,
+                   int n_tokens);
+/* scheduler outputs of the engine's stepper: same layouts as ef_sim_* */
+int ef_engine_metrics(ef_engine* e, int64_t* ints, int32_t n_ints, double* bw_estimate);
+int ef_engine_output(ef_engine* e, int32_t kind, int64_t* buf, int64_t max_len, int64_t* n);
+int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len, int64_t* n);
+/* physical counters, in order: steps, copies, copy_bytes, stall_ms, phys_slots,
+   logical_capacity, staging_slots, kernel_launches, host_decision_ms, ffn_ms, step_ms,
+   preload_copies, d2h_bytes */
+int ef_engine_stats(ef_engine* e, double* out, int n);
+/* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
+   6 perm, 7 inv, 8 y, 9 x */
+int ef_engine_ptr(ef_engine* e, int which, void** out);
+/* routing log entry `index` (one per executed layer, in order): R scored router
+   matrices of logits [R][B][M] fp32, sel [B][k], cache-aware bias mask.  Pass
+   null buffers to query sizes; *n_entries = log length. */
+int ef_engine_routing_log(ef_engine* e, int64_t index, float* logits, int64_t max_logits,
+                          int32_t* sel, int64_t max_sel, int32_t* R, int32_t* B,
+                          uint64_t* mask_lo, uint64_t* mask_hi, int64_t* n_entries);
+/* physical slot of (layer, expert) or -1 */
+int ef_engine_slot_of(ef_engine* e, int32_t layer, int32_t expert, int32_t* slot);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXPERTFLOW_H */

@@ -55,6 +55,11 @@ def uniform_scale(var: float) -> np.float32:
     return np.float32(math.sqrt(3.0 * var) / 8388608.0)
 
 
+def fan_scale(fan_in: int) -> np.float32:
+    """Weight step for variance 1/fan_in; same double expression as engine.cu."""
+    return np.float32(math.sqrt(3.0 / fan_in) / 8388608.0)
+
+
 def fill_uniform(key: int, n: int, scale: np.float32, offset: int = 0) -> np.ndarray:
     """Element i = float32(int24(mix(key + (offset+i+1)*GOLDEN)) - 2^23) * scale."""
     with np.errstate(over="ignore"):
@@ -84,7 +89,7 @@ class ModelWeights:
 
     def _mat(self, layer, expert, mat, rows, cols, fan_in):
         key = stream_key(self.seed, layer, expert, mat)
-        v = fill_uniform(key, rows * cols, uniform_scale(1.0 / fan_in))
+        v = fill_uniform(key, rows * cols, fan_scale(fan_in))
         return cast(v, self.dtype).reshape(rows, cols)
 
     def expert(self, layer, e):

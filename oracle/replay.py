@@ -1,0 +1,130 @@
+"""Replay a B200 engine run through the oracle — TEST INFRASTRUCTURE.
+
+Given the routing the GPU produced (the engine's routing log: per executed
+layer the scored fp32 router logits [R, B, M] and the selection [B, k]),
+rebuild the scheduler inputs with the canonical adapter of
+oracle/numerics.py (fp64 softmax, sequential sums, one group per token) and
+run the OracleStepper, which restates /root/reference/pkg/src/moesim/
+engine.py:_Sim.  The result must equal the engine's decisions bit for bit:
+that is the "given identical fp32 gate logits" parity of the north star.
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import numerics as N
+from .sim import OracleStepper, Policy, TokenTrace
+
+
+def token_traces(log, L: int, tokens_per_step: Sequence[Sequence[int]]) -> List[TokenTrace]:
+    out = []
+    for t, toks in enumerate(tokens_per_step):
+        gates, actual, grouped = [], [], []
+        for l in range(L):
+            logits, sel, _mask = log[t * L + l]
+            gates.append(N.batch_gate(logits[0]))
+            g = tuple(tuple(sorted(int(e) for e in row)) for row in sel)
+            grouped.append(g)
+            actual.append(tuple(sorted(set().union(*g))))
+        out.append(TokenTrace(tuple(toks), gates, actual, grouped, tuple([1] * sel.shape[0])))
+    return out
+
+
+def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, policy: Policy,
+           tokens_per_step, bias: float = 0.0, emit_events=True):
+    """Returns (stepper, mask_mismatches, selection_mismatches)."""
+    traces = token_traces(log, L, tokens_per_step)
+    cur = {"t": 0}
+
+    def pregate_fn(tt, layer, h):
+        logits = log[cur["t"] * L + layer][0]
+        return N.batch_gate(logits[h])
+
+    st = OracleStepper(num_layers=L, experts_per_layer=M, top_k=k, expert_size_bytes=expert_bytes,
+                       link_bw=link_bw, device_memory_bytes=budget_experts * expert_bytes,
+                       layer_compute_ns=layer_ns, policy=policy, emit_events=emit_events,
+                       pregate_fn=pregate_fn)
+    mask_bad, sel_bad = [], []
+
+    def hook(layer, resident):
+        logits, sel, mask = log[cur["t"] * L + layer]
+        want = sum(1 << e for e in range(M) if (layer, e) in resident) if bias else 0
+        if mask != want:
+            mask_bad.append((cur["t"], layer, mask, want))
+        res = np.array([(layer, e) in resident for e in range(M)])
+        ref = N.topk_select(logits[0], k, bias, res if bias else None)
+        if not np.array_equal(ref, sel):
+            sel_bad.append((cur["t"], layer))
+
+    st.pre_layer_hook = hook
+    for t, tt in enumerate(traces):
+        cur["t"] = t
+        st.run_token(tt)
+    return st, mask_bad, sel_bad
+
+
+def forward_step(h0: np.ndarray, log, step: int, weights: N.ModelWeights, L: int, k: int,
+                 mode: str) -> np.ndarray:
+    """fp64 oracle of one decode step using the GPU's logits for selection."""
+    h = np.asarray(h0, dtype=np.float64)
+    for l in range(L):
+        logits = log[step * L + l][0][0]
+        h = N.moe_layer(h, weights, l, k, mode, logits_override=logits)["h_next"]
+    return h
+
+
+def rel_err(got, want) -> float:
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
+
+
+def oracle_metrics_dict(st: OracleStepper) -> dict:
+    m = st.metrics
+    return {
+        "total_time_ns": m.total_time_ns, "compute_ns": m.compute_ns, "waiting_ns": m.waiting_ns,
+        "cache_miss_ns": m.cache_miss_ns, "prefetch_ns": m.prefetch_ns,
+        "cold_start_ns": m.cold_start_ns, "hits": m.hits, "misses": m.misses,
+        "admissions": m.admissions, "evictions": m.evictions, "stall_events": m.stall_events,
+        "overfetch_events": m.overfetch_events, "prediction_cache_hits": m.prediction_cache_hits,
+        "prediction_cache_misses": m.prediction_cache_misses,
+        "bandwidth_estimate": m.bandwidth_estimate, "final_step": m.final_step,
+        "n_selected": m.n_selected, "n_total": m.n_total,
+        "step_history": [tuple(x) for x in m.step_history],
+        "per_layer": [(r[0], r[1], r[2], r[3], r[4], tuple(r[5]), tuple(r[6]), r[7])
+                      for r in m.per_layer],
+        "samples": [(tuple(s[0]), s[1], tuple(s[2]), tuple(s[3]), s[4]) for s in m.samples],
+        "events": None if m.events is None else [tuple(e) for e in m.events],
+        "cache_events": None if st.cache.events is None else
+        [(n, k, e[0], e[1]) for n, k, e in st.cache.events],
+    }
+
+
+def product_metrics_dict(m, cache_events=None) -> dict:
+    """Same layout for a product SimMetrics (paper_2510_26730_b200.engine)."""
+    return {
+        "total_time_ns": m.total_time_ns, "compute_ns": m.compute_ns, "waiting_ns": m.waiting_ns,
+        "cache_miss_ns": m.cache_miss_ns, "prefetch_ns": m.prefetch_ns,
+        "cold_start_ns": m.cold_start_ns, "hits": m.hits, "misses": m.misses,
+        "admissions": m.admissions, "evictions": m.evictions, "stall_events": m.stall_events,
+        "overfetch_events": m.overfetch_events, "prediction_cache_hits": m.prediction_cache_hits,
+        "prediction_cache_misses": m.prediction_cache_misses,
+        "bandwidth_estimate": m.bandwidth_estimate, "final_step": m.final_step,
+        "n_selected": m.miss_stats.n_selected, "n_total": m.miss_stats.n_total,
+        "step_history": [tuple(x) for x in m.step_history],
+        "per_layer": [(r.layer, r.start_ns, r.end_ns, r.stall_ns, r.step, tuple(r.predicted),
+                       tuple(r.actual), r.demand_misses) for r in m.per_layer],
+        "samples": [(tuple(s.token_ids), s.layer_idx, tuple(s.predicted_experts),
+                     tuple(s.actual_experts), s.step_size) for s in m.samples],
+        "events": None if m.events is None else
+        [(e.time_ns, e.kind, e.seq, e.detail) for e in m.events],
+        "cache_events": None if cache_events is None else
+        [(n, k, e.layer, e.expert) for n, k, e in cache_events],
+    }
+
+
+def diff_dicts(got: dict, want: dict) -> List[str]:
+    return [k for k in want if got.get(k) != want[k]]

@@ -335,7 +335,11 @@ class OracleStepper:
                 self.cache.admit((0, x), D.HIGH, 0)
             self.metrics.cold_start_ns = D.swap_in_latency(len(tt.actual[0]), self.E_s, self.bw)
 
+    pre_layer_hook = None  # callable(layer, resident_set) before each layer's step
+
     def run_token(self, tt: TokenTrace) -> None:
+        if self.pre_layer_hook is not None:
+            self.pre_layer_hook(0, set(self.cache.tier))
         if self.tokens_run == 0:
             self._start(tt)
         self.predicted: Dict[int, tuple] = {}
@@ -344,6 +348,8 @@ class OracleStepper:
         self.next_boundary = 0
         pol, m = self.policy, self.metrics
         for layer in range(self.L):                               # :566-659
+            if layer and self.pre_layer_hook is not None:
+                self.pre_layer_hook(layer, set(self.cache.tier))
             self.now = self.tokens_run * self.L + layer
             t0 = self.clock
             self._advance_to(t0)

@@ -1,0 +1,528 @@
+// kernels.cu — sm_100a kernels of the ExpertFlow MoE decode path and their
+// C-ABI launchers (include/expertflow.h).
+//
+//   (a) ef_router_logits + ef_route_permute : router GEMV, top-k keyed on fp32
+//       logits (+ cache-aware bias), routing weights, stable permutation
+//   (b) ef_router_logits with R > 1          : future-layer pre-gate rows
+//   (c) ef_route_permute / ef_combine        : permute, unpermute + combine
+//   (d) ef_expert_ffn_decode                 : slot-indirected weight-streaming
+//       GEMV (gate+up+SiLU fused, then down), 16-byte L1-bypassing loads,
+//       warp-shuffle reductions
+// Decode GEMVs are HBM-bound (arithmetic intensity ~ n_rows FLOP/B); they keep
+// many independent 16 B loads in flight per lane instead of using tensor cores.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+
+#include "../../include/expertflow.h"
+#include "kernels.cuh"
+
+namespace ef {
+extern thread_local std::string g_last_error;
+}
+
+using namespace efk;
+
+#define EF_CUDA_RET(expr)                                                         \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      ef::g_last_error = std::string(#expr) + ": " + cudaGetErrorString(_e);     \
+      return EF_ECUDA;                                                            \
+    }                                                                             \
+  } while (0)
+
+#define EF_CHECK_ARG(cond, msg)     \
+  do {                                \
+    if (!(cond)) {                    \
+      ef::g_last_error = msg;         \
+      return EF_EINVAL;               \
+    }                                 \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ============================================================ synthetic weights
+template <typename T>
+__global__ void fill_uniform_kernel(T* dst, int64_t n, uint64_t key, float scale, int64_t offset) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    uint64_t h = mix64(key + (uint64_t)(offset + i + 1) * kGolden);
+    int32_t u = (int32_t)(h >> 40) - 8388608;
+    float v = __fmul_rn((float)u, scale);
+    WTraits<T>::store(dst + i, v);
+  }
+}
+
+extern "C" uint64_t ef_stream_key(uint64_t seed, int32_t layer, int32_t expert, int32_t mat) {
+  uint64_t tag = ((uint64_t)(uint32_t)layer << 32) | ((uint64_t)(uint32_t)expert << 8) |
+                 (uint64_t)(uint32_t)mat;
+  return mix64(seed ^ mix64(tag + kGolden));
+}
+
+extern "C" int ef_fill_uniform(void* stream, void* dst, int dtype, int64_t n, uint64_t key,
+                               float scale, int64_t offset) {
+  EF_CHECK_ARG(dst && n >= 0, "bad fill arguments");
+  if (n == 0) return EF_OK;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dtype == EF_BF16)
+    fill_uniform_kernel<__nv_bfloat16><<<blocks, 256, 0, S(stream)>>>(
+        (__nv_bfloat16*)dst, n, key, scale, offset);
+  else
+    fill_uniform_kernel<float><<<blocks, 256, 0, S(stream)>>>((float*)dst, n, key, scale, offset);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// ============================================================ rmsnorm
+__device__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  int nw = (blockDim.x + 31) >> 5;
+  float t = (threadIdx.x < nw) ? red[threadIdx.x] : 0.f;
+  if (w == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) red[0] = t;
+  __syncthreads();
+  float r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void rmsnorm_kernel(const float* __restrict__ h, float* __restrict__ x, int d,
+                               float eps) {
+  __shared__ float red[32];
+  const float* hr = h + (int64_t)blockIdx.x * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += hr[i] * hr[i];
+  ss = block_sum(ss, red);
+  float inv = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)blockIdx.x * d + i] = hr[i] * inv;
+}
+
+extern "C" int ef_rmsnorm(void* stream, const float* h, float* x, int B, int d, float eps) {
+  EF_CHECK_ARG(B >= 0 && d > 0, "bad rmsnorm shape");
+  if (B == 0) return EF_OK;
+  rmsnorm_kernel<<<B, 256, 0, S(stream)>>>(h, x, d, eps);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// ============================================================ (a)(b) router GEMV
+// One warp per router row (r, m); all B tokens accumulate in registers while
+// the row streams through once.  x is tiny and stays in L1/L2.
+template <typename WT, int MAXB>
+__global__ void router_kernel(const float* __restrict__ x, const WT* __restrict__ w, int rows,
+                              int B, int t0, int nb, int d, int M, float* __restrict__ logits) {
+  constexpr int V = WTraits<WT>::kPer16;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const WT* wr = w + (int64_t)warp * d;
+  float acc[MAXB];
+#pragma unroll
+  for (int t = 0; t < MAXB; ++t) acc[t] = 0.f;
+  for (int c = lane * V; c < d; c += 32 * V) {
+    float f[V];
+    WTraits<WT>::unpack(ld_stream16(wr + c), f);
+#pragma unroll
+    for (int t = 0; t < MAXB; ++t) {
+      if (t < nb) {
+        const float4* xp = reinterpret_cast<const float4*>(x + (int64_t)(t0 + t) * d + c);
+#pragma unroll
+        for (int q = 0; q < V / 4; ++q) {
+          float4 xv = __ldg(xp + q);
+          acc[t] = fmaf(f[4 * q + 0], xv.x, acc[t]);
+          acc[t] = fmaf(f[4 * q + 1], xv.y, acc[t]);
+          acc[t] = fmaf(f[4 * q + 2], xv.z, acc[t]);
+          acc[t] = fmaf(f[4 * q + 3], xv.w, acc[t]);
+        }
+      }
+    }
+  }
+  int r = warp / M, m = warp % M;
+#pragma unroll
+  for (int t = 0; t < MAXB; ++t) {
+    if (t < nb) {
+      float s = warp_sum(acc[t]);
+      if (lane == 0) logits[((int64_t)r * B + t0 + t) * M + m] = s;
+    }
+  }
+}
+
+template <typename WT>
+static void launch_router(cudaStream_t st, const float* x, const void* w, int R, int B, int d,
+                          int M, float* logits) {
+  const int rows = R * M, threads = 256;
+  const int blocks = (rows * 32 + threads - 1) / threads;
+  for (int t0 = 0; t0 < B; t0 += 8) {  // 8 tokens per pass bounds the accumulators
+    int nb = std::min(8, B - t0);
+    if (nb == 1)
+      router_kernel<WT, 1><<<blocks, threads, 0, st>>>(x, (const WT*)w, rows, B, t0, nb, d, M, logits);
+    else
+      router_kernel<WT, 8><<<blocks, threads, 0, st>>>(x, (const WT*)w, rows, B, t0, nb, d, M, logits);
+  }
+}
+
+extern "C" int ef_router_logits(void* stream, const float* x, const void* w, int dtype, int R,
+                                int B, int d, int M, float* logits) {
+  EF_CHECK_ARG(R >= 1 && B >= 0 && M >= 1, "bad router shape");
+  EF_CHECK_ARG(d % (dtype == EF_BF16 ? 8 : 4) == 0, "router d must be a multiple of 8 (bf16) / 4");
+  if (B == 0) return EF_OK;
+  if (dtype == EF_BF16)
+    launch_router<__nv_bfloat16>(S(stream), x, w, R, B, d, M, logits);
+  else
+    launch_router<float>(S(stream), x, w, R, B, d, M, logits);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// ============================================================ (a)+(c) route + permute
+// One CTA of 1024 threads.  Top-k per token (value desc, index asc), routing
+// weights, then a stable counting sort of the B*k (token, rank) slots by
+// expert using warp match/ballot ranks — deterministic, O(B*k).
+constexpr int kRouteThreads = 1024;
+constexpr int kMaxExperts = 256;
+
+__global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
+    const float* __restrict__ logits, int B, int M, int k, int mode, float bias, uint64_t mlo,
+    uint64_t mhi, int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts,
+    int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+  __shared__ int32_t warp_cnt[32][kMaxExperts];
+  __shared__ int32_t base[kMaxExperts];
+  __shared__ int32_t total[kMaxExperts];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  // ---- top-k and weights: one thread per token
+  for (int t = tid; t < B; t += blockDim.x) {
+    const float* lg = logits + (int64_t)t * M;
+    int chosen[16];
+    float mx_all = -INFINITY;
+    for (int e = 0; e < M; ++e) mx_all = fmaxf(mx_all, lg[e]);
+    for (int r = 0; r < k; ++r) {
+      float best = -INFINITY;
+      int be = -1;
+      for (int e = 0; e < M; ++e) {
+        bool used = false;
+        for (int q = 0; q < r; ++q) used |= (chosen[q] == e);
+        if (used) continue;
+        bool res = e < 64 ? ((mlo >> e) & 1ull) : ((mhi >> (e - 64)) & 1ull);
+        float key = (res && bias != 0.f) ? __fadd_rn(lg[e], bias) : lg[e];
+        if (be < 0 || key > best) {
+          best = key;
+          be = e;
+        }
+      }
+      chosen[r] = be;
+      sel[t * k + r] = be;
+    }
+    if (mode == EF_ROUTE_MIXTRAL) {
+      float mx = -INFINITY;
+      for (int r = 0; r < k; ++r) mx = fmaxf(mx, lg[chosen[r]]);
+      float ev[16], s = 0.f;
+      for (int r = 0; r < k; ++r) {
+        ev[r] = expf(lg[chosen[r]] - mx);
+        s += ev[r];
+      }
+      for (int r = 0; r < k; ++r) wts[t * k + r] = ev[r] / s;
+    } else {
+      float s = 0.f;
+      for (int e = 0; e < M; ++e) s += expf(lg[e] - mx_all);
+      for (int r = 0; r < k; ++r) wts[t * k + r] = expf(lg[chosen[r]] - mx_all) / s;
+    }
+  }
+  __syncthreads();
+
+  // ---- stable counting sort by expert over flat slots f = t*k + r
+  const int N = B * k;
+  for (int e = tid; e < M; e += blockDim.x) {
+    base[e] = 0;
+    total[e] = 0;
+  }
+  __syncthreads();
+  for (int c0 = 0; c0 < N; c0 += blockDim.x) {
+    for (int i = tid; i < 32 * M; i += blockDim.x) warp_cnt[i / M][i % M] = 0;
+    __syncthreads();
+    int f = c0 + tid;
+    int e = (f < N) ? sel[f] : -1;
+    unsigned same = __match_any_sync(0xffffffffu, e);
+    int rank_in_warp = __popc(same & ((1u << lane) - 1u));
+    if (e >= 0 && rank_in_warp == 0) warp_cnt[wid][e] = __popc(same);
+    __syncthreads();
+    // exclusive prefix over warps, per expert
+    for (int x = tid; x < M; x += blockDim.x) {
+      int run = base[x];
+      for (int w = 0; w < 32; ++w) {
+        int c = warp_cnt[w][x];
+        warp_cnt[w][x] = run;
+        run += c;
+      }
+      base[x] = run;
+    }
+    __syncthreads();
+    if (e >= 0) perm[f] = warp_cnt[wid][e] + rank_in_warp;  // rank within expert (temp)
+    __syncthreads();
+  }
+  // counts and offsets
+  if (tid == 0) {
+    int run = 0;
+    for (int x = 0; x < M; ++x) {
+      counts[x] = base[x];
+      offsets[x] = run;
+      total[x] = run;
+      run += base[x];
+    }
+    offsets[M] = run;
+  }
+  __syncthreads();
+  for (int f = tid; f < N; f += blockDim.x) {
+    int pos = total[sel[f]] + perm[f];
+    inv[f] = pos;
+  }
+  __syncthreads();
+  for (int f = tid; f < N; f += blockDim.x) perm[inv[f]] = f;
+}
+
+extern "C" int ef_route_permute(void* stream, const float* logits, int B, int M, int k, int mode,
+                                float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
+                                int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv) {
+  EF_CHECK_ARG(M >= 1 && M <= 128 && k >= 1 && k <= 16 && k <= M && B >= 0, "bad route shape");
+  EF_CHECK_ARG(mode == EF_ROUTE_MIXTRAL || mode == EF_ROUTE_SOFTMAX_TOPK, "bad routing mode");
+  route_permute_kernel<<<1, kRouteThreads, 0, S(stream)>>>(logits, B, M, k, mode, bias, mlo, mhi,
+                                                           sel, wts, counts, offsets, perm, inv);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// ============================================================ (d) decode expert FFN
+constexpr int kMaxActive = 80;
+struct ActiveList {
+  const char* w[kMaxActive];  // expert weight base ([W1|W3|W2])
+  int32_t p0[kMaxActive];     // first permuted row (also output row)
+  int32_t n[kMaxActive];      // rows
+};
+
+// Input-vector loaders (one 16-byte weight chunk = V columns).
+template <typename WT>
+struct XGather {  // T(x[perm[p]/k]) — expert input, cast to the weight dtype
+  const float* x;
+  const int32_t* perm;
+  int k, d;
+  bool identity;  // shared expert: row p reads token p - id_base
+  int id_base;
+  __device__ inline const float* row(int p) const {
+    int t = identity ? p - id_base : perm[p] / k;
+    return x + (int64_t)t * d;
+  }
+  __device__ inline void load(const float* r, int c, float* out) const {
+    constexpr int V = WTraits<WT>::kPer16;
+    const float4* p = reinterpret_cast<const float4*>(r + c);
+#pragma unroll
+    for (int q = 0; q < V / 4; ++q) {
+      float4 v = __ldg(p + q);
+      out[4 * q + 0] = WTraits<WT>::cast(v.x);
+      out[4 * q + 1] = WTraits<WT>::cast(v.y);
+      out[4 * q + 2] = WTraits<WT>::cast(v.z);
+      out[4 * q + 3] = WTraits<WT>::cast(v.w);
+    }
+  }
+};
+
+template <typename WT>
+struct XAct {  // act[p] (already in the weight dtype)
+  const WT* act;
+  int ff;
+  __device__ inline const WT* row(int p) const { return act + (int64_t)p * ff; }
+  __device__ inline void load(const WT* r, int c, float* out) const {
+    WTraits<WT>::unpack(*reinterpret_cast<const uint4*>(r + c), out);
+  }
+};
+
+// rows x cols matrix A (and B when DUAL) streamed once per token chunk; each
+// warp owns R consecutive output rows; lanes stride the columns in 16 B.
+template <typename WT, int NT, int R, bool DUAL, typename XL>
+__global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, int64_t offA, int64_t offB,
+                                                       int rows, int cols, XL xl, WT* act_out,
+                                                       float* y_out, int out_ld) {
+  constexpr int V = WTraits<WT>::kPer16;
+  constexpr int WARPS = 4;
+  const int a = blockIdx.y;
+  const int n_all = al.n[a];
+  if (n_all == 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int j0 = (blockIdx.x * WARPS + wid) * R;
+  if (j0 >= rows) return;
+  const WT* A = reinterpret_cast<const WT*>(al.w[a] + offA);
+  const WT* Bm = reinterpret_cast<const WT*>(al.w[a] + offB);
+  const int p0 = al.p0[a];
+
+  for (int tc = 0; tc < n_all; tc += NT) {
+    const int nt = min(NT, n_all - tc);
+    float accA[R][NT], accB[R][NT];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int t = 0; t < NT; ++t) accA[r][t] = accB[r][t] = 0.f;
+
+    decltype(xl.row(0)) xr[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) xr[t] = xl.row(p0 + tc + (t < nt ? t : 0));
+
+    for (int c = lane * V; c < cols; c += 32 * V) {
+      uint4 wa[R], wb[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        int j = min(j0 + r, rows - 1);
+        wa[r] = ld_stream16(A + (int64_t)j * cols + c);
+        if (DUAL) wb[r] = ld_stream16(Bm + (int64_t)j * cols + c);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (t < nt) {
+          float xv[V];
+          xl.load(xr[t], c, xv);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            float f[V];
+            WTraits<WT>::unpack(wa[r], f);
+#pragma unroll
+            for (int q = 0; q < V; ++q) accA[r][t] = fmaf(f[q], xv[q], accA[r][t]);
+            if (DUAL) {
+              WTraits<WT>::unpack(wb[r], f);
+#pragma unroll
+              for (int q = 0; q < V; ++q) accB[r][t] = fmaf(f[q], xv[q], accB[r][t]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (t < nt) {
+          float g = warp_sum(accA[r][t]);
+          float u = DUAL ? warp_sum(accB[r][t]) : 0.f;
+          int j = j0 + r;
+          if (lane == 0 && j < rows) {
+            int64_t row = p0 + tc + t;
+            if (DUAL) {
+              float s = g / (1.0f + expf(-g));
+              WTraits<WT>::store(act_out + row * out_ld + j, s * u);
+            } else {
+              y_out[row * out_ld + j] = g;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <typename WT, int NT>
+static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, int n_active, int d, int ff,
+                          const XGather<WT>& xg, WT* act, float* y) {
+  constexpr int R = 4, WARPS = 4;
+  const int64_t es = sizeof(WT);
+  dim3 gu((ff + WARPS * R - 1) / (WARPS * R), n_active);
+  ffn_gemv_kernel<WT, NT, R, true, XGather<WT>>
+      <<<gu, 128, 0, st>>>(al, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
+  dim3 gd((d + WARPS * R - 1) / (WARPS * R), n_active);
+  XAct<WT> xa{act, ff};
+  ffn_gemv_kernel<WT, NT, R, false, XAct<WT>>
+      <<<gd, 128, 0, st>>>(al, 2 * (int64_t)ff * d * es, 0, d, ff, xa, nullptr, y, d);
+}
+
+template <typename WT>
+static void launch_ffn(cudaStream_t st, const ActiveList& al, int n_active, int max_rows, int d,
+                       int ff, const XGather<WT>& xg, WT* act, float* y) {
+  if (max_rows <= 1)
+    launch_ffn_nt<WT, 1>(st, al, n_active, d, ff, xg, act, y);
+  else if (max_rows <= 2)
+    launch_ffn_nt<WT, 2>(st, al, n_active, d, ff, xg, act, y);
+  else if (max_rows <= 4)
+    launch_ffn_nt<WT, 4>(st, al, n_active, d, ff, xg, act, y);
+  else
+    launch_ffn_nt<WT, 8>(st, al, n_active, d, ff, xg, act, y);
+}
+
+namespace ef {
+// Internal entry used by the engine: weight bases are explicit pointers.
+int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k, bool identity,
+                    const char* const* wbase, const int32_t* p0, const int32_t* nrows,
+                    int n_active, int d, int ff, int dtype, void* act, float* y) {
+  EF_CHECK_ARG(n_active >= 0 && n_active <= kMaxActive, "too many active experts");
+  EF_CHECK_ARG(d % 8 == 0 && ff % 8 == 0, "d and ff must be multiples of 8");
+  if (n_active == 0) return EF_OK;
+  ActiveList al;
+  int max_rows = 0;
+  for (int i = 0; i < n_active; ++i) {
+    al.w[i] = wbase[i];
+    al.p0[i] = p0[i];
+    al.n[i] = nrows[i];
+    max_rows = std::max(max_rows, nrows[i]);
+  }
+  if (max_rows == 0) return EF_OK;
+  if (dtype == EF_BF16) {
+    XGather<__nv_bfloat16> xg{x, perm, k, d, identity, identity ? p0[0] : 0};
+    launch_ffn<__nv_bfloat16>(st, al, n_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y);
+  } else {
+    XGather<float> xg{x, perm, k, d, identity, identity ? p0[0] : 0};
+    launch_ffn<float>(st, al, n_active, max_rows, d, ff, xg, (float*)act, y);
+  }
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+}  // namespace ef
+
+extern "C" int ef_expert_ffn_decode(void* stream, const float* x, const int32_t* perm, int k,
+                                    const void* slab, int64_t stride, const int32_t* act_slot,
+                                    const int32_t* act_off, const int32_t* act_rows,
+                                    int n_active, int d, int ff, int dtype, void* act, float* y) {
+  EF_CHECK_ARG(n_active <= kMaxActive, "too many active experts");
+  const char* w[kMaxActive];
+  for (int i = 0; i < n_active; ++i)
+    w[i] = reinterpret_cast<const char*>(slab) + (int64_t)act_slot[i] * stride;
+  return ef::expert_ffn_ptrs(S(stream), x, perm, k, false, w, act_off, act_rows, n_active, d, ff,
+                             dtype, act, y);
+}
+
+// ============================================================ (c) combine + norm
+__global__ void combine_kernel(float* __restrict__ h, float* __restrict__ x,
+                               const float* __restrict__ y, const int32_t* __restrict__ inv,
+                               const float* __restrict__ wts, const float* __restrict__ ys,
+                               const float* __restrict__ gate_logit, int d, int k, float eps) {
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  float g = 1.f;
+  if (gate_logit) g = 1.0f / (1.0f + expf(-gate_logit[t]));
+  float* hr = h + (int64_t)t * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float acc = 0.f;
+    for (int r = 0; r < k; ++r)
+      acc = fmaf(wts[t * k + r], y[(int64_t)inv[t * k + r] * d + i], acc);
+    if (ys) acc = fmaf(g, ys[(int64_t)t * d + i], acc);
+    float v = hr[i] + acc;
+    hr[i] = v;
+    ss += v * v;
+  }
+  ss = block_sum(ss, red);
+  float invn = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)t * d + i] = hr[i] * invn;
+}
+
+extern "C" int ef_combine(void* stream, float* h, float* x, const float* y, const int32_t* inv,
+                          const float* wts, const float* ys, const float* gate_logit, int B,
+                          int d, int k, float eps) {
+  EF_CHECK_ARG(B >= 0 && d > 0 && k >= 1, "bad combine shape");
+  if (B == 0) return EF_OK;
+  combine_kernel<<<B, 256, 0, S(stream)>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}

@@ -1,0 +1,215 @@
+"""MoEEngine — the B200 decode engine behind ``step()``.
+
+PyTorch supplies device memory for activations and the CUDA stream; all
+decisions and data movement happen in libexpertflow.so (engine.cu): the
+Stepper decides hits / misses / prefetches exactly as the reference
+scheduler would on a logical clock, the slab + copy stream make those
+decisions physical, and the sm_100a kernels compute the MoE layers.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, replace
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .core import HardwareSpec, ModelSpec, Seed, seconds_to_ns
+from .engine import PolicyConfig, SimMetrics, collect_metrics
+from .predictor import ForestModel
+from .scheduler import _Ladder
+from .workload import EmbeddingTable
+
+DTYPES = {"f32": 0, "bf16": 1}
+ROUTE_MODES = {"mixtral": 0, "softmax_topk": 1}
+
+
+@dataclass(frozen=True)
+class MoEConfig:
+    """MoE layer-stack shape (public HF configs)."""
+    name: str
+    num_layers: int
+    num_experts: int
+    top_k: int
+    d_model: int
+    d_ff: int
+    dtype: str = "bf16"
+    route_mode: str = "mixtral"
+    shared_ff: int = 0
+    shared_gate: bool = False
+    embed_dim: int = 8
+    vocab_size: int = 32000
+
+    @property
+    def elem_bytes(self) -> int:
+        return 2 if self.dtype == "bf16" else 4
+
+    @property
+    def expert_bytes(self) -> int:
+        return 3 * self.d_model * self.d_ff * self.elem_bytes
+
+    @property
+    def total_experts(self) -> int:
+        return self.num_layers * self.num_experts
+
+    def model_spec(self) -> ModelSpec:
+        return ModelSpec(self.num_layers, self.num_experts, self.top_k, self.expert_bytes,
+                         self.embed_dim, self.vocab_size)
+
+
+PRESETS = {
+    "tiny": MoEConfig("tiny", 4, 8, 2, 256, 1024, dtype="f32"),
+    "tiny-bf16": MoEConfig("tiny-bf16", 4, 8, 2, 256, 1024, dtype="bf16"),
+    "mixtral-8x7b": MoEConfig("mixtral-8x7b", 32, 8, 2, 4096, 14336),
+    "qwen1.5-moe-a2.7b": MoEConfig("qwen1.5-moe-a2.7b", 24, 60, 4, 2048, 1408,
+                                   route_mode="softmax_topk", shared_ff=5632, shared_gate=True),
+    "deepseek-v2-lite": MoEConfig("deepseek-v2-lite", 26, 64, 6, 2048, 1408,
+                                  route_mode="softmax_topk", shared_ff=2816),
+    "mixtral-8x22b": MoEConfig("mixtral-8x22b", 56, 8, 2, 6144, 16384),
+}
+
+
+class MoEEngine:
+    """One decode engine on one GPU.
+
+    ``budget_experts``: HBM expert-cache capacity in experts (the logical
+    cache of the reference, ``ExpertCache`` slots).  ``link_bw`` (bytes/s)
+    and ``layer_time_s`` parameterise the scheduler's logical clock exactly
+    like ``HardwareSpec`` does in the reference; the bench measures them.
+    """
+
+    def __init__(self, cfg: MoEConfig, *, budget_experts: int, policy: PolicyConfig,
+                 link_bw: int, layer_time_s: float, max_batch: int = 1, seed: int = 0,
+                 routing_bias: float = 0.0, staging_slots: Optional[int] = None,
+                 forest: Optional[ForestModel] = None, table: Optional[EmbeddingTable] = None,
+                 emit_events: bool = False, timing: bool = False, record_routing: bool = False,
+                 device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
+        self.cfg, self.policy = cfg, policy
+        self.max_batch = max_batch
+        self.emit_events = emit_events
+        self.device = torch.device("cuda", device)
+        model = cfg.model_spec()
+        hw = HardwareSpec(int(link_bw), int(budget_experts) * cfg.expert_bytes, float(layer_time_s))
+        policy.check(model)
+        if policy.predictor == "oracle":
+            raise ValueError("the oracle predictor needs future routing; use simulate()")
+        if policy.predictor == "forest" and (forest is None or table is None):
+            raise ValueError("forest predictor needs a trained model and table")
+        self.hw = hw
+        self._ladder = _Ladder(L_=cfg.num_layers, M=cfg.num_experts, top_k=cfg.top_k,
+                               cum_threshold=policy.cum_threshold,
+                               forest=forest if policy.predictor == "forest" else None,
+                               table=table if policy.predictor == "forest" else None)
+        sim = policy.to_c(model, hw, Seed(seed), emit_events)
+        ec = L.EngineCfg()
+        ec.L, ec.M, ec.top_k = cfg.num_layers, cfg.num_experts, cfg.top_k
+        ec.d, ec.ff, ec.dtype = cfg.d_model, cfg.d_ff, DTYPES[cfg.dtype]
+        ec.route_mode = ROUTE_MODES[cfg.route_mode]
+        ec.max_batch = max_batch
+        ec.shared_ff, ec.shared_gate = cfg.shared_ff, int(cfg.shared_gate)
+        ec.budget_slots = budget_experts
+        # landing slot for the one in-flight transfer + slots pinned by the
+        # current layer after an in-layer eviction
+        ec.staging_slots = staging_slots or (2 + min(max_batch * cfg.top_k, cfg.num_experts))
+        ec.routing_bias = routing_bias
+        ec.seed = seed
+        ec.device = device
+        ec.timing = int(timing)
+        ec.record_routing = int(record_routing)
+        torch.cuda.set_device(device)
+        torch.cuda.init()
+        h = L.vp()
+        L._pending_exc.clear()
+        L.check(L.lib.ef_engine_create(C.byref(ec), C.byref(sim), C.byref(self._ladder.cfg),
+                                       C.byref(h)))
+        self._h = L.Handle(h.value, L.lib.ef_engine_destroy)
+        self._ec = ec
+
+    # ------------------------------------------------------------------ API
+    def step(self, h: torch.Tensor, token_ids: Optional[Sequence[int]] = None) -> torch.Tensor:
+        """One decode step: h[B, d] (fp32, on this device) <- MoE stack(h),
+        in place on the current stream; returns h."""
+        if h.device != self.device or h.dtype != torch.float32 or not h.is_contiguous():
+            raise ValueError("h must be a contiguous fp32 tensor on the engine's device")
+        B, d = h.shape
+        if d != self.cfg.d_model:
+            raise ValueError(f"hidden width {d} != d_model {self.cfg.d_model}")
+        toks = L.i64arr(list(token_ids) if token_ids else [0])
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        L._pending_exc.clear()
+        L.check(L.lib.ef_engine_step(self._h.ptr, C.c_void_p(stream), C.c_void_p(h.data_ptr()),
+                                     B, L.as_ptr(toks, C.c_int64),
+                                     len(token_ids) if token_ids else 0))
+        return h
+
+    def metrics(self) -> SimMetrics:
+        return collect_metrics(self.policy.name, self._h.ptr, L.lib.ef_engine_metrics,
+                               L.lib.ef_engine_output, L.lib.ef_engine_event_details,
+                               self.emit_events)
+
+    def cache_events(self):
+        from .engine import _read_output
+        from .core import ExpertId
+        rows = _read_output(L.lib.ef_engine_output, self._h.ptr, 4)
+        names = {0: "miss", 1: "hit", 2: "admit", 3: "evict"}
+        return [(rows[i], names[rows[i + 1]], ExpertId(rows[i + 2], rows[i + 3]))
+                for i in range(0, len(rows), 4)]
+
+    def stats(self) -> dict:
+        keys = ["steps", "copies", "copy_bytes", "stall_ms", "phys_slots", "logical_capacity",
+                "staging_slots", "kernel_launches", "host_decision_ms", "ffn_ms", "step_ms",
+                "preload_copies", "d2h_bytes"]
+        out = (C.c_double * len(keys))()
+        L.check(L.lib.ef_engine_stats(self._h.ptr, out, len(keys)))
+        return dict(zip(keys, list(out)))
+
+    def routing_log(self):
+        """[(logits[R,B,M] fp32, sel[B,k] int32, resident_mask int)] per executed layer."""
+        n = C.c_int64()
+        R, B, lo, hi = C.c_int32(), C.c_int32(), C.c_uint64(), C.c_uint64()
+        L.check(L.lib.ef_engine_routing_log(self._h.ptr, -1, None, 0, None, 0, C.byref(R),
+                                            C.byref(B), C.byref(lo), C.byref(hi), C.byref(n)))
+        out = []
+        M, k = self.cfg.num_experts, self.cfg.top_k
+        Rmax = self.cfg.num_layers
+        for i in range(n.value):
+            lg = np.empty(Rmax * self.max_batch * M, dtype=np.float32)
+            sel = np.empty(self.max_batch * k, dtype=np.int32)
+            L.check(L.lib.ef_engine_routing_log(self._h.ptr, i, L.as_ptr(lg, C.c_float), lg.size,
+                                                L.as_ptr(sel, C.c_int32), sel.size, C.byref(R),
+                                                C.byref(B), C.byref(lo), C.byref(hi),
+                                                C.byref(n)))
+            r, b = R.value, B.value
+            out.append((lg[:r * b * M].reshape(r, b, M).copy(), sel[:b * k].reshape(b, k).copy(),
+                        lo.value | (hi.value << 64)))
+        return out
+
+    def device_ptr(self, which: int) -> int:
+        p = L.vp()
+        L.check(L.lib.ef_engine_ptr(self._h.ptr, which, C.byref(p)))
+        return p.value or 0
+
+    def slot_of(self, layer: int, expert: int) -> int:
+        s = C.c_int32()
+        L.check(L.lib.ef_engine_slot_of(self._h.ptr, layer, expert, C.byref(s)))
+        return s.value
+
+    def close(self) -> None:
+        self._h = None
+
+
+def synthetic_hidden(cfg: MoEConfig, seed: int, step: int, B: int, device) -> torch.Tensor:
+    """Deterministic decode input h_0 (oracle/numerics.py input_hidden)."""
+    h = torch.empty(B, cfg.d_model, dtype=torch.float32, device=device)
+    key = L.lib.ef_stream_key(seed, step, 0, 8)
+    scale = np.float32(math.sqrt(3.0) / 8388608.0)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    L.check(L.lib.ef_fill_uniform(C.c_void_p(stream), C.c_void_p(h.data_ptr()), 0, h.numel(),
+                                  key, float(scale), 0))
+    return h
