@@ -1,0 +1,418 @@
+"""Benchmark: decode tokens/s and expert-stall % of step at a fixed HBM
+expert-cache budget (BASELINE.json metric) on the Mixtral-8x7B shape,
+batch-1 decode, cache budget 40 % of experts (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0.  `value` is device-timed throughput with each
+step's input already in HBM; `e2e` is the same through MoEEngine.step()
+with the input copied from pinned host memory and the result read back
+inside the timed region.  `roofline` is the expert FFN (the dominant
+kernel pair) against the measured HBM copy peak; `cpu_baseline` is the CPU
+oracle port on the host cores over a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s and expert-stall % of step at fixed HBM expert-cache budget"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral-8x7b")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--budget-frac", type=float, default=0.4)
+    ap.add_argument("--strategy", default="adaptive")
+    ap.add_argument("--predictor", default="pregate")
+    ap.add_argument("--bias", type=float, default=None,
+                    help="cache-aware routing logit bias (default: the config's headline)")
+    ap.add_argument("--rho", type=float, default=0.8,
+                    help="temporal correlation of successive decode inputs (AR(1))")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-baseline", action="store_true", help="skip the reactive baseline run")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.rows, self.proc, self.index = [], None, index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) >= 7
+                          for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------- CPU arm
+def cpu_port(cfg, B, seed=0, n_layers=1):
+    from oracle import numerics as N
+    w = N.ModelWeights(L=cfg.num_layers, M=cfg.num_experts, d=cfg.d_model, ff=cfg.d_ff,
+                       dtype=cfg.dtype, seed=seed, shared_ff=cfg.shared_ff,
+                       shared_gate=cfg.shared_gate)
+    return N.CpuPortLayerSample(w, range(n_layers), B, cfg.top_k, cfg.route_mode, seed)
+
+
+def time_cpu_port(port, cfg, B, seconds):
+    """Run the CPU port's layer sample repeatedly for ~seconds; tokens/s
+    extrapolated from per-layer time to the full L-layer stack."""
+    reps, t0 = 0, time.perf_counter()
+    while reps < 1 or time.perf_counter() - t0 < seconds:
+        port.run()
+        reps += 1
+    per_layer = (time.perf_counter() - t0) / (reps * len(port.layers))
+    desc = (f"{len(port.layers)} of {cfg.num_layers} layers of a B={B} {cfg.name} decode step "
+            f"(router, top-k, routing weights, SwiGLU experts, combine, shared expert) in "
+            f"float32 numpy/BLAS, {reps} reps, extrapolated to {cfg.num_layers} layers; "
+            f"routed expert weights pre-materialised in host RAM")
+    return B / (per_layer * cfg.num_layers), desc
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    try:
+        import torch
+        torch.set_num_threads(os.cpu_count())
+    except Exception:
+        pass
+    port = cpu_port(cfg, args.batch, args.seed)
+    per_step = min(5.0, max(0.5, 120.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        v, desc = time_cpu_port(port, cfg, args.batch, per_step)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * args.batch / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+            "config": {"workload": f"{cfg.name} decode B={args.batch}, CPU oracle port"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(),
+                             "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU arm
+def measure_h2d(torch, nbytes):
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        d.copy_(h, non_blocking=True)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(3):
+        d.copy_(h, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    bw = 3 * nbytes / (s.elapsed_time(e) / 1e3)
+    del h, d
+    return int(bw)
+
+
+def measure_layer_time(torch, cfg, B):
+    """Device time of one layer's routed expert FFN at the roofline-bound
+    kernel speed (top_k experts, B rows) + router/combine, on a scratch slab."""
+    import ctypes as C
+    from paper_2510_26730_b200 import _lib as L
+    k = cfg.top_k
+    n_act = min(cfg.num_experts, B * k)
+    slab = torch.empty(n_act, cfg.expert_bytes, dtype=torch.uint8, device="cuda")
+    x = torch.randn(B, cfg.d_model, device="cuda")
+    perm = torch.arange(B * k, dtype=torch.int32, device="cuda")
+    act = torch.empty(B * k, cfg.d_ff * cfg.elem_bytes, dtype=torch.uint8, device="cuda")
+    y = torch.empty(B * k, cfg.d_model, device="cuda")
+    slab.view(torch.bfloat16 if cfg.dtype == "bf16" else torch.float32).normal_(0, 0.01)
+    rows = [B * k // n_act] * n_act
+    rows[0] += B * k - sum(rows)
+    offs = [sum(rows[:i]) for i in range(n_act)]
+    a_slot, a_off, a_rows = L.i32arr(range(n_act)), L.i32arr(offs), L.i32arr(rows)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def go():
+        L.check(L.lib.ef_expert_ffn_decode(
+            st, C.c_void_p(x.data_ptr()), C.c_void_p(perm.data_ptr()), k,
+            C.c_void_p(slab.data_ptr()), cfg.expert_bytes, L.as_ptr(a_slot, C.c_int32),
+            L.as_ptr(a_off, C.c_int32), L.as_ptr(a_rows, C.c_int32), n_act, cfg.d_model,
+            cfg.d_ff, 1 if cfg.dtype == "bf16" else 0, C.c_void_p(act.data_ptr()),
+            C.c_void_p(y.data_ptr())))
+    for _ in range(3):
+        go()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(10):
+        go()
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / 10 / 1e3
+    del slab
+    return t + 15e-6  # + router, route/permute, combine launches
+
+
+def run_ours(args, cfg, bias):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2510_26730_b200 as ef
+    from paper_2510_26730_b200.runtime import MoEEngine, synthetic_hidden
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    B = args.batch
+    budget = max(cfg.top_k, int(round(args.budget_frac * cfg.total_experts)))
+    link_bw = measure_h2d(torch, cfg.expert_bytes)
+    layer_s = measure_layer_time(torch, cfg, B)
+    policy = ef.PolicyConfig(f"{args.strategy}_{args.predictor}", args.strategy,
+                             predictor=args.predictor if args.strategy != "static" else "none",
+                             cache_aware_routing=True)
+    t_init = time.perf_counter()
+    eng = MoEEngine(cfg, budget_experts=budget, policy=policy, link_bw=link_bw,
+                    layer_time_s=layer_s, max_batch=B, seed=args.seed, routing_bias=bias,
+                    timing=True, device=local)
+    init_s = time.perf_counter() - t_init
+
+    # decode inputs: AR(1) in time with correlation rho, unit variance, in HBM
+    K, W = args.steps, args.warmup
+    n_in = W + 2 * K  # timed pass W..W+K, end-to-end pass on fresh inputs after it
+    xs = [synthetic_hidden(cfg, args.seed + 1000 * rank, 0, B, dev)]
+    for t in range(1, n_in):
+        eps = synthetic_hidden(cfg, args.seed + 1000 * rank, t, B, dev)
+        xs.append(args.rho * xs[-1] + math.sqrt(1 - args.rho ** 2) * eps)
+    inputs = [x.clone() for x in xs]
+    stream = torch.cuda.current_stream(dev)
+
+    for t in range(W):
+        eng.step(inputs[t])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    st0 = eng.stats()
+    m0 = eng.metrics()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        time.sleep(0.5)  # let the sampler take its first readings
+        s.record(stream)
+        for t in range(W, W + K):
+            eng.step(inputs[t])
+        e.record(stream)
+        torch.cuda.synchronize()
+    dev_ms = s.elapsed_time(e)
+    st1 = eng.stats()
+    m1 = eng.metrics()
+    if world > 1:
+        tt = torch.tensor([dev_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms = float(tt.item())
+    value = world * B * K / (dev_ms / 1e3)
+
+    # expert-stall % of step: physical (device wait on copy events) and logical
+    stall_ms = st1["stall_ms"] - st0["stall_ms"]
+    stall_pct = 100.0 * stall_ms / dev_ms
+    log_wait = m1.waiting_ns - m0.waiting_ns
+    log_total = m1.total_time_ns - m0.total_time_ns
+    ffn_ms = st1["ffn_ms"] - st0["ffn_ms"]
+    ffn_bytes = st1["ffn_bytes"] - st0["ffn_bytes"]
+    ffn_pairs = (st1["ffn_launches"] - st0["ffn_launches"]) / 2
+    launches = int(st1["kernel_launches"] - st0["kernel_launches"])
+    hbm_peak, peak_kind = peaks()
+    achieved = ffn_bytes / (ffn_ms / 1e3) / 1e9 if ffn_ms > 0 else 0.0
+
+    # ---- end to end through the public API with host buffers
+    host_in = [x.cpu().pin_memory() for x in xs]
+    host_out = torch.empty(B, cfg.d_model, dtype=torch.float32).pin_memory()
+    buf = torch.empty(B, cfg.d_model, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    se, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    se.record(stream)
+    for t in range(K):
+        buf.copy_(host_in[W + K + t], non_blocking=True)
+        eng.step(buf)
+        host_out.copy_(buf, non_blocking=True)
+    ee.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = se.elapsed_time(ee)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e = world * B * K / (e2e_ms / 1e3)
+    finite = bool(torch.isfinite(host_out).all())
+
+    phys_slots = int(st1["phys_slots"])
+    eng.close()
+    del eng
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    baseline = None
+    if not args.no_baseline and rank == 0 and world == 1:
+        baseline = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K)
+
+    if rank == 0:
+        cpu_v, cpu_desc = (None, "skipped (--no-cpu)") if args.no_cpu else \
+            time_cpu_port(cpu_port(cfg, B, args.seed), cfg, B, args.cpu_seconds)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (random-init weights, AR(1) hidden inputs)",
+            "config": {"workload": f"{cfg.name} shape, bf16 random-init, batch-{B} decode, "
+                                   f"cache budget {budget}/{cfg.total_experts} experts "
+                                   f"({100 * budget / cfg.total_experts:.0f}%) on 1xB200",
+                       "model": cfg.name, "global_batch": B * world, "seq_len": 1,
+                       "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+                       "policy": policy.name, "routing_bias": bias, "rho": args.rho,
+                       "budget_experts": budget, "physical_slots": phys_slots,
+                       "link_bw_measured_GBps": link_bw / 1e9,
+                       "layer_time_calibrated_us": layer_s * 1e6,
+                       "l2": "expert weights streamed per step (>= 22 GB) exceed the 126 MB L2",
+                       "engine_init_s": round(init_s, 1)},
+            "expert_stall_pct": stall_pct,
+            "logical_stall_pct": 100.0 * log_wait / log_total if log_total else 0.0,
+            "hit_rate": _rate(m1.hits - m0.hits, m1.misses - m0.misses),
+            "copies_per_step": (st1["copies"] - st0["copies"]) / K,
+            "h2d_GBps": (st1["copy_bytes"] - st0["copy_bytes"]) / (dev_ms / 1e3) / 1e9,
+            "host_decision_us_per_layer": 1e3 * (st1["host_decision_ms"] - st0["host_decision_ms"])
+            / (K * cfg.num_layers),
+            "gate_wait_us_per_layer": 1e3 * (st1["gate_wait_ms"] - st0["gate_wait_ms"])
+            / (K * cfg.num_layers),
+            "ffn_us_per_layer": 1e3 * ffn_ms / (K * cfg.num_layers),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None,
+                         "kernel": "ef_expert_ffn_decode (gate/up+SiLU GEMV, down GEMV)",
+                         "bytes_per_launch": ffn_bytes / max(ffn_pairs, 1),
+                         "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * cfg.d_model * 4,
+                    "d2h_bytes_per_step": B * cfg.d_model * 4, "output_finite": finite},
+            "gpu_launches": launches,
+            "cpu_baseline": {"value": cpu_v, "unit": UNIT, "cores": os.cpu_count(),
+                             "kind": "port", "sample": cpu_desc},
+            "clocks": clocks.summary(),
+        }
+        if baseline:
+            line["reactive_baseline"] = baseline
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _rate(h, m):
+    return h / (h + m) if h + m else 0.0
+
+
+def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K):
+    """The reactive per-layer baseline (engine.py:488-489) on the same
+    engine type, budget and inputs; no routing bias."""
+    import torch
+    import paper_2510_26730_b200 as ef
+    from paper_2510_26730_b200.runtime import MoEEngine
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    eng = MoEEngine(cfg, budget_experts=budget,
+                    policy=ef.PolicyConfig("reactive", "reactive", predictor="pregate"),
+                    link_bw=link_bw, layer_time_s=layer_s, max_batch=args.batch, seed=args.seed,
+                    routing_bias=0.0, timing=True)
+    n = min(K, 6)
+    for t in range(min(W, 2)):
+        eng.step(inputs[t].clone())
+    torch.cuda.synchronize()
+    st0 = eng.stats()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for t in range(W, W + n):
+        eng.step(inputs[t].clone())
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    st1 = eng.stats()
+    return {"tokens_per_s": args.batch * n / (ms / 1e3), "steps": n,
+            "expert_stall_pct": 100.0 * (st1["stall_ms"] - st0["stall_ms"]) / ms,
+            "policy": "reactive/pregate, routing_bias 0"}
+
+
+def main():
+    args = parse()
+    from paper_2510_26730_b200.runtime import PRESETS
+    cfg = PRESETS[args.config]
+    # headline: cache-aware routing bias on (the north star's kernel (a))
+    bias = args.bias if args.bias is not None else 2.0
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg, bias)
+
+
+if __name__ == "__main__":
+    main()

@@ -176,13 +176,16 @@ def swiglu(xe: np.ndarray, w1, w3, w2, dtype: str) -> np.ndarray:
 
 
 def moe_layer(h, weights: ModelWeights, layer, k, mode, bias=0.0, resident=None,
-              logits_override=None):
-    """One layer of the canonical MoE forward; returns dict of intermediates."""
+              logits_override=None, sel_override=None):
+    """One layer of the canonical MoE forward; returns dict of intermediates.
+    ``logits_override``/``sel_override`` replay the device's fp32 logits and
+    selection (the "given identical fp32 gate logits" condition)."""
     x = rmsnorm(h)
     wr = weights.router(layer)
     logits = router_logits(x, wr)
     lg32 = np.asarray(logits if logits_override is None else logits_override, np.float32)
-    sel = topk_select(lg32, k, bias, resident)
+    sel = topk_select(lg32, k, bias, resident) if sel_override is None else \
+        np.asarray(sel_override, dtype=np.int32)
     w = route_weights(lg32, sel, mode)
     xe = cast(x.astype(np.float32), weights.dtype)
     B = h.shape[0]
@@ -221,9 +224,21 @@ def softmax64(logits_row: Sequence[float]) -> List[float]:
     return [v / s for v in ex]
 
 
-def batch_gate(logits: np.ndarray) -> np.ndarray:
+def biased_keys(logits: np.ndarray, bias: float = 0.0, mask: int = 0) -> np.ndarray:
+    """fp32 router keys: logit + bias for experts in the residency bit mask
+    (the key the route kernel selects on)."""
+    key = np.asarray(logits, dtype=np.float32).copy()
+    if bias != 0.0:
+        cols = [e for e in range(key.shape[-1]) if (mask >> e) & 1]
+        key[..., cols] = key[..., cols] + np.float32(bias)
+    return key
+
+
+def batch_gate(logits: np.ndarray, bias: float = 0.0, mask: int = 0) -> np.ndarray:
     """Token-weighted batch gate (workload.py:215-223 with per-token groups):
-    mean of per-token softmax64, renormalised by a sequential sum."""
+    mean of per-token softmax64 of the (biased) fp32 keys, renormalised by a
+    sequential sum."""
+    logits = biased_keys(logits, bias, mask)
     B, M = logits.shape
     w = 1.0 / B
     mixed = [0.0] * M
@@ -235,3 +250,59 @@ def batch_gate(logits: np.ndarray) -> np.ndarray:
     for v in mixed:
         s += v
     return np.array([v / s for v in mixed], dtype=np.float64)
+
+
+class CpuPortLayerSample:
+    """Timed CPU port of the decode layer (the bench's cpu_baseline and
+    ``--impl reference`` arm): the same canonical semantics as moe_layer in
+    float32 numpy/BLAS on all host threads, over a bounded sample of layers
+    whose routed experts are generated once and then kept in host memory."""
+
+    def __init__(self, weights: ModelWeights, layers, B: int, k: int, mode: str, seed: int = 0):
+        self.w, self.layers, self.k, self.mode = weights, list(layers), k, mode
+        self.h0 = input_hidden(seed, 0, B, weights.d).astype(np.float32)
+        self.router = {l: weights.router(l).astype(np.float32) for l in self.layers}
+        self.experts = {}
+        self.shared = {l: weights.shared(l) for l in self.layers}
+        h = self.h0
+        for l in self.layers:  # first pass: find and materialise the routed experts
+            x = rmsnorm(h).astype(np.float32)
+            sel = topk_select(x @ self.router[l].T, k)
+            for e in sorted(set(sel.reshape(-1).tolist())):
+                self.experts[(l, e)] = tuple(np.ascontiguousarray(m, np.float32)
+                                             for m in weights.expert(l, e))
+            h = self._layer(h, l)
+
+    def _swiglu(self, xe, w1, w3, w2):
+        g = xe @ w1.T
+        u = xe @ w3.T
+        a = cast((g / (np.float32(1) + np.exp(-g))) * u, self.w.dtype)
+        return a @ w2.T
+
+    def _layer(self, h, l):
+        x = (h / np.sqrt((h * h).mean(axis=1, keepdims=True) + np.float32(1e-6))).astype(np.float32)
+        lg = x @ self.router[l].T
+        sel = topk_select(lg, self.k)
+        wts = route_weights(lg, sel, self.mode).astype(np.float32)
+        xe = cast(x, self.w.dtype)
+        out = h.copy()
+        for t in range(h.shape[0]):
+            for r in range(self.k):
+                w1, w3, w2 = self.experts.get((l, int(sel[t, r]))) or tuple(
+                    np.asarray(m, np.float32) for m in self.w.expert(l, int(sel[t, r])))
+                out[t] += wts[t, r] * self._swiglu(xe[t:t + 1], w1, w3, w2)[0]
+        sh = self.shared[l]
+        if sh is not None:
+            w1, w3, w2, g = sh
+            ys = self._swiglu(xe, np.asarray(w1, np.float32), np.asarray(w3, np.float32),
+                              np.asarray(w2, np.float32))
+            if g is not None:
+                ys = ys * (1.0 / (1.0 + np.exp(-(x @ np.asarray(g, np.float32)))))[:, None]
+            out += ys
+        return out
+
+    def run(self):
+        h = self.h0
+        for l in self.layers:
+            h = self._layer(h, l)
+        return h

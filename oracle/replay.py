@@ -19,13 +19,14 @@ from . import numerics as N
 from .sim import OracleStepper, Policy, TokenTrace
 
 
-def token_traces(log, L: int, tokens_per_step: Sequence[Sequence[int]]) -> List[TokenTrace]:
+def token_traces(log, L: int, tokens_per_step: Sequence[Sequence[int]],
+                 bias: float = 0.0) -> List[TokenTrace]:
     out = []
     for t, toks in enumerate(tokens_per_step):
         gates, actual, grouped = [], [], []
         for l in range(L):
-            logits, sel, _mask = log[t * L + l]
-            gates.append(N.batch_gate(logits[0]))
+            logits, sel, mask = log[t * L + l]
+            gates.append(N.batch_gate(logits[0], bias, mask))
             g = tuple(tuple(sorted(int(e) for e in row)) for row in sel)
             grouped.append(g)
             actual.append(tuple(sorted(set().union(*g))))
@@ -36,17 +37,21 @@ def token_traces(log, L: int, tokens_per_step: Sequence[Sequence[int]]) -> List[
 def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, policy: Policy,
            tokens_per_step, bias: float = 0.0, emit_events=True):
     """Returns (stepper, mask_mismatches, selection_mismatches)."""
-    traces = token_traces(log, L, tokens_per_step)
+    traces = token_traces(log, L, tokens_per_step, bias)
     cur = {"t": 0}
+    holder = {}
 
     def pregate_fn(tt, layer, h):
         logits = log[cur["t"] * L + layer][0]
-        return N.batch_gate(logits[h])
+        cache = holder["st"].cache
+        mask = sum(1 << e for e in range(M) if (layer + h, e) in cache) if bias else 0
+        return N.batch_gate(logits[h], bias, mask)
 
     st = OracleStepper(num_layers=L, experts_per_layer=M, top_k=k, expert_size_bytes=expert_bytes,
                        link_bw=link_bw, device_memory_bytes=budget_experts * expert_bytes,
                        layer_compute_ns=layer_ns, policy=policy, emit_events=emit_events,
                        pregate_fn=pregate_fn)
+    holder["st"] = st
     mask_bad, sel_bad = [], []
 
     def hook(layer, resident):
@@ -71,8 +76,9 @@ def forward_step(h0: np.ndarray, log, step: int, weights: N.ModelWeights, L: int
     """fp64 oracle of one decode step using the GPU's logits for selection."""
     h = np.asarray(h0, dtype=np.float64)
     for l in range(L):
-        logits = log[step * L + l][0][0]
-        h = N.moe_layer(h, weights, l, k, mode, logits_override=logits)["h_next"]
+        logits, sel, _mask = log[step * L + l]
+        h = N.moe_layer(h, weights, l, k, mode, logits_override=logits[0],
+                        sel_override=sel)["h_next"]
     return h
 
 

@@ -1,24 +1,35 @@
 // engine.cu — the MoE decode engine: HBM expert-cache slab with a physical
-// slot table, pinned host store, dedicated copy stream with events, and the
-// scheduler Stepper (simcore.h) driving it.
+// slot table, pinned host store, dedicated copy stream, and the scheduler
+// Stepper (simcore.h) driving it through a flag-gated GPU pipeline.
 //
 // Decision parity: the Stepper runs the reference's per-layer loop
 // (engine.py:566-659) on a LOGICAL integer-ns clock, so the hit / miss /
 // admit / evict trace, predictions and step sizes are exactly the oracle's
 // for the routing the GPU produced.  Data movement is PHYSICAL: every
-// logical transfer start issues one cudaMemcpyAsync of the expert blob into a
-// free HBM slot on the copy stream; the expert FFN of a layer waits (stream
-// wait on the copy's event) only for the slots it reads, so swap-ins overlap
-// compute and the measured wait is the physical expert stall.
+// logical transfer start issues one cudaMemcpyAsync of the expert blob into
+// a free HBM slot on the copy stream, followed by a 1-thread kernel that
+// publishes the slot's fill sequence number; the routed FFN of a layer spins
+// on those numbers for the slots it reads, so swap-ins overlap compute and
+// the measured spin is the physical expert stall.
 //
-// Slot safety: a slot freed by an eviction is reused by a later copy only
-// after the last kernel that read it (per-layer reader event), and slots read
-// by the current layer stay pinned until that layer's kernels are enqueued.
-// The slab therefore holds capacity + staging slots.
+// Pipeline (per layer l, kernels enqueued one layer ahead; no per-layer host
+// synchronisation or launch on the critical path):
+//   router(l) -> route(l) [publishes sel + row-0 logits + done flag to mapped
+//   host memory] -> shared expert(l) -> gate(l) [waits for the host's go
+//   flag, copies the decision to device memory] -> routed FFN(l) -> combine(l)
+// Host: spin on done(l) -> Stepper begin_layer/run_layer (issues copies) ->
+// write slots + next layer's bias mask -> go(l).
+//
+// Slot safety: when the host decides layer l, route(l) has completed, so
+// every kernel of layers < l has completed (stream order); the only pending
+// reader is FFN(l), whose slots stay pinned until the decision of layer l+1.
+// Copies therefore never wait on compute, and compute only on its own copies.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -30,13 +41,8 @@
 
 #include "../../include/expertflow.h"
 #include "capi_util.h"
+#include "pipeline.h"
 #include "simcore.h"
-
-namespace ef {
-int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k, bool identity,
-                    const char* const* wbase, const int32_t* p0, const int32_t* nrows,
-                    int n_active, int d, int ff, int dtype, void* act, float* y);
-}
 
 using namespace ef;
 
@@ -45,25 +51,32 @@ using namespace ef;
     cudaError_t _e = (expr);                                                              \
     if (_e != cudaSuccess) throw CudaErr(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
-#define CKS(expr)                                                          \
-  do {                                                                     \
-    int _s = (expr);                                                       \
+#define CKS(expr)                                                             \
+  do {                                                                        \
+    int _s = (expr);                                                          \
     if (_s != EF_OK) throw CudaErr(std::string(#expr) + ": " + g_last_error); \
   } while (0)
 
-// fp64 softmax of fp32 logits: glibc exp, sequential sum (
-// oracle/numerics.py softmax64) and the token-weighted batch gate
-// (workload.py:215-223 with one group per token).
-static void batch_gate(const float* logits, int B, int M, double* out) {
-  std::vector<double> mixed(M, 0.0), ex(M);
+// fp64 batch gate of fp32 router keys (oracle/numerics.py
+// batch_gate): key = fp32(logit + bias) for experts in `mask` (the same key
+// the route kernel selects on), softmax with glibc exp and sequential sums,
+// token-weighted mean renormalised (workload.py:215-223, one group per token).
+static void batch_gate(const float* logits, int B, int M, float bias, const uint64_t* mask,
+                       double* out) {
+  std::vector<double> mixed(M, 0.0), ex(M), key(M);
   const double w = 1.0 / (double)B;
   for (int t = 0; t < B; ++t) {
     const float* lg = logits + (int64_t)t * M;
-    double mx = (double)lg[0];
-    for (int e = 1; e < M; ++e) mx = std::max(mx, (double)lg[e]);
+    for (int e = 0; e < M; ++e) {
+      float kf = lg[e];
+      if (bias != 0.f && ((mask[e >> 6] >> (e & 63)) & 1ull)) kf = lg[e] + bias;
+      key[e] = (double)kf;
+    }
+    double mx = key[0];
+    for (int e = 1; e < M; ++e) mx = std::max(mx, key[e]);
     double s = 0.0;
     for (int e = 0; e < M; ++e) {
-      ex[e] = std::exp((double)lg[e] - mx);
+      ex[e] = std::exp(key[e] - mx);
       s += ex[e];
     }
     for (int e = 0; e < M; ++e) {
@@ -96,24 +109,29 @@ struct ef_engine {
   int32_t *sel_d = nullptr, *counts_d = nullptr, *offsets_d = nullptr, *perm_d = nullptr,
           *inv_d = nullptr;
   void *act_d = nullptr, *acts_d = nullptr;
-  // host pinned
-  float* logits_h = nullptr;
-  int32_t* sel_h = nullptr;
+  DevCtrl* dctrl = nullptr;               // [L]
+  uint32_t* ready = nullptr;              // [P] fill sequence published by the copy stream
+  unsigned long long* stats_d = nullptr;  // [L][8]
+  // host pinned / mapped
+  HostCtrl* hctrl = nullptr;  // [L] mapped
+  HostCtrl* hctrl_dev = nullptr;
+  char* hout = nullptr;  // [L] x out_stride, mapped
+  char* hout_dev = nullptr;
+  int64_t out_stride = 0;
+  float* logits_h = nullptr;  // pre-gate rows fetched on demand
+  std::vector<unsigned long long> stats_h;
   std::vector<char*> store;  // per layer: M * stride bytes
-  cudaStream_t copy_stream = nullptr;
-  std::vector<cudaEvent_t> fill_ev;     // per physical slot: last copy into it
-  std::vector<int> fill_recorded;
-  std::vector<cudaEvent_t> reader_ring;  // per-layer "kernels done" events
-  std::vector<int> reader_of;            // per slot: ring index of last reader (-1)
-  int ring_next = 0;
-  std::vector<cudaEvent_t> stall_a, stall_b;  // per layer (timing)
+  cudaStream_t copy_stream = nullptr, side_stream = nullptr;
   // slot table
-  std::vector<int32_t> phys_of;  // [L*M] -> slot or -1
+  std::vector<int32_t> phys_of;    // [L*M] -> slot or -1
+  std::vector<uint32_t> slot_seq;  // fill sequence of each slot's current content
+  uint32_t copy_seq = 0;
   std::deque<int> free_slots;
   std::vector<char> pinned;
   std::vector<int> pinned_list, deferred_free;
   int inflight_slot = -1;
   std::vector<int> layer_use;  // [M] -> slot used by the current layer (-1)
+  uint64_t cur_mask[2] = {0, 0};
   struct RoutingRec {
     std::vector<float> logits;
     std::vector<int32_t> sel;
@@ -123,12 +141,12 @@ struct ef_engine {
   std::vector<RoutingRec> rlog;
   // stats
   int64_t steps = 0, copies = 0, copy_bytes = 0, launches = 0, preload_copies = 0,
-          d2h_bytes = 0;
-  double stall_ms = 0, host_ms = 0, ffn_ms = 0, step_ms = 0;
+          d2h_bytes = 0, ffn_bytes = 0, ffn_launches = 0;
+  double stall_ms = 0, host_ms = 0, ffn_ms = 0, step_ms = 0, bubble_ms = 0;
 
   struct Mirror : Observer {
     ef_engine* e;
-    void on_transfer_start(uint64_t key, int prio) override { e->issue_copy(key, false); }
+    void on_transfer_start(uint64_t key, int) override { e->issue_copy(key, false); }
     void on_admit(uint64_t key) override {
       if (e->inflight_slot < 0) throw RuntimeErr("admit without a landed transfer");
       e->phys_of[e->idx(key)] = e->inflight_slot;
@@ -144,7 +162,7 @@ struct ef_engine {
         e->free_slots.push_back(s);
     }
     void on_preload(uint64_t key) override { e->issue_copy(key, true); }
-    void on_group_run(int layer, const std::vector<uint64_t>& demand) override {
+    void on_group_run(int, const std::vector<uint64_t>& demand) override {
       for (uint64_t k : demand) {
         int s = e->phys_of[e->idx(k)];
         if (s < 0) throw RuntimeErr("group runs with a non-resident expert");
@@ -157,22 +175,34 @@ struct ef_engine {
     }
   } mirror;
 
-  int64_t idx(uint64_t key) const {
-    return (int64_t)eid_layer(key) * cfg.M + eid_expert(key);
+  int64_t idx(uint64_t key) const { return (int64_t)eid_layer(key) * cfg.M + eid_expert(key); }
+  HostOut* out(int l) { return reinterpret_cast<HostOut*>(hout + (int64_t)l * out_stride); }
+  int32_t* out_sel(int l) {
+    return reinterpret_cast<int32_t*>(hout + (int64_t)l * out_stride + sizeof(HostOut));
+  }
+  float* out_logits(int l) {
+    return reinterpret_cast<float*>(hout + (int64_t)l * out_stride + sizeof(HostOut) +
+                                    (int64_t)cfg.max_batch * cfg.top_k * 4);
+  }
+  template <typename T>
+  T* dev_of(T* host_mapped) {
+    return reinterpret_cast<T*>(hout_dev + (reinterpret_cast<char*>(host_mapped) - hout));
   }
 
   void issue_copy(uint64_t key, bool preload) {
+    // A free slot's previous readers have all completed (see the header).
     if (free_slots.empty())
       throw RuntimeErr("no free physical expert slot (raise staging_slots)");
     int s = free_slots.front();
     free_slots.pop_front();
-    if (reader_of[s] >= 0) CK(cudaStreamWaitEvent(copy_stream, reader_ring[reader_of[s]], 0));
     const char* src = store[eid_layer(key)] + (int64_t)eid_expert(key) * stride;
     CK(cudaMemcpyAsync(slab + (int64_t)s * stride, src, stride, cudaMemcpyHostToDevice,
                        copy_stream));
-    CK(cudaEventRecord(fill_ev[s], copy_stream));
-    fill_recorded[s] = 1;
+    uint32_t seq = ++copy_seq;
+    CKS(launch_set_ready(copy_stream, ready, s, seq));
+    slot_seq[s] = seq;
     ++copies;
+    ++launches;
     copy_bytes += stride;
     if (preload) {
       ++preload_copies;
@@ -182,6 +212,15 @@ struct ef_engine {
     }
   }
 
+  void residency_mask(int layer, uint64_t* m) const {
+    m[0] = m[1] = 0;
+    if (cfg.routing_bias == 0.f || layer >= cfg.L) return;
+    for (int e = 0; e < cfg.M; ++e)
+      if (st->resident(layer, e)) m[e >> 6] |= 1ull << (e & 63);
+  }
+
+  void enqueue_layer(cudaStream_t stream, int l, int B, float* h);
+  void abort_pipeline(cudaStream_t stream, int from, int enq);
   void init_weights();
   void step(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
   ~ef_engine();
@@ -221,15 +260,15 @@ void ef_engine::init_weights() {
   int it = 0;
   for (int l = 0; l < L; ++l) {
     for (int e = 0; e < M; ++e, ++it) {
-      char* st = stage[it & 1];
+      char* sb = stage[it & 1];
       if (it >= 2) CK(cudaEventSynchronize(done[it & 1]));
-      CKS(ef_fill_uniform(s, st, dt, nff, ef_stream_key(cfg.seed, l, e, 0), scale_for(d), 0));
-      CKS(ef_fill_uniform(s, st + nff * esz, dt, nff, ef_stream_key(cfg.seed, l, e, 1),
+      CKS(ef_fill_uniform(s, sb, dt, nff, ef_stream_key(cfg.seed, l, e, 0), scale_for(d), 0));
+      CKS(ef_fill_uniform(s, sb + nff * esz, dt, nff, ef_stream_key(cfg.seed, l, e, 1),
                           scale_for(d), 0));
-      CKS(ef_fill_uniform(s, st + 2 * nff * esz, dt, nff, ef_stream_key(cfg.seed, l, e, 2),
+      CKS(ef_fill_uniform(s, sb + 2 * nff * esz, dt, nff, ef_stream_key(cfg.seed, l, e, 2),
                           scale_for(ff), 0));
-      CK(cudaMemcpyAsync(store[l] + (int64_t)e * stride, st, 3 * nff * esz, cudaMemcpyDeviceToHost,
-                         s));
+      CK(cudaMemcpyAsync(store[l] + (int64_t)e * stride, sb, 3 * nff * esz,
+                         cudaMemcpyDeviceToHost, s));
       CK(cudaEventRecord(done[it & 1], s));
     }
   }
@@ -244,157 +283,227 @@ void ef_engine::init_weights() {
 ef_engine::~ef_engine() {
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   cudaDeviceSynchronize();
-  for (auto ev : fill_ev) cudaEventDestroy(ev);
-  for (auto ev : reader_ring) cudaEventDestroy(ev);
-  for (auto ev : stall_a) cudaEventDestroy(ev);
-  for (auto ev : stall_b) cudaEventDestroy(ev);
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
-                  (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d})
+                  (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
+                  (void*)dctrl, (void*)ready, (void*)stats_d})
     if (p) cudaFree(p);
-  if (logits_h) cudaFreeHost(logits_h);
-  if (sel_h) cudaFreeHost(sel_h);
+  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h})
+    if (p) cudaFreeHost(p);
   for (char* p : store)
     if (p) cudaFreeHost(p);
   if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (side_stream) cudaStreamDestroy(side_stream);
+}
+
+// Enqueue every kernel of layer l: router (+ pre-gate rows), route (publishes
+// to the host), shared expert, gate, routed FFN, combine + next rmsnorm.
+void ef_engine::enqueue_layer(cudaStream_t stream, int l, int B, float* h) {
+  const int M = cfg.M, k = cfg.top_k, d = cfg.d;
+  const int R = std::min(Rmax, cfg.L - l);  // (a)+(b): layer l and pre-gate rows l+1..l+R-1
+  CKS(ef_router_logits(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R, B,
+                       d, M, logits_d));
+  ++launches;
+  const bool sgate = cfg.shared_ff && cfg.shared_gate;
+  if (sgate) {
+    CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
+                         1, sgl_d));
+    ++launches;
+  }
+  CKS(launch_route_publish(stream, logits_d, B, M, k, cfg.route_mode, cfg.routing_bias, sel_d,
+                           wts_d, counts_d, offsets_d, perm_d, inv_d, &hctrl_dev[l].mask,
+                           dev_of(out_sel(l)), dev_of(out_logits(l)),
+                           const_cast<uint32_t*>(&dev_of(out(l))->done)));
+  ++launches;
+  if (cfg.shared_ff) {  // always resident: runs while the host decides the layer
+    const char* sw = shared_w + (int64_t)l * sstride;
+    int32_t z = 0, nb = B;
+    CKS(expert_ffn_ptrs(stream, x_d, perm_d, k, true, &sw, &z, &nb, 1, d, cfg.shared_ff,
+                        cfg.dtype, acts_d, ys_d));
+    launches += 2;
+  }
+  CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + 8 * l));
+  ++launches;
+  CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + 8 * l,
+                      std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
+  launches += 2;
+  CKS(ef_combine(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
+                 sgate ? sgl_d : nullptr, B, d, k, 1e-6f));
+  ++launches;
+}
+
+void ef_engine::abort_pipeline(cudaStream_t stream, int from, int enq) {
+  // Release every enqueued gate with an empty decision so the GPU drains,
+  // then reset the flags for the next step.
+  for (int j = from; j < enq; ++j) {
+    hctrl[j].n_active = 0;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    hctrl[j].go = 1u;
+  }
+  cudaStreamSynchronize(stream);
+  cudaStreamSynchronize(copy_stream);
+  for (int j = 0; j < cfg.L; ++j) {
+    hctrl[j].go = 0u;
+    out(j)->done = 0u;
+  }
+  std::fill(pinned.begin(), pinned.end(), 0);
+  pinned_list.clear();
+  for (int s : deferred_free) free_slots.push_back(s);
+  deferred_free.clear();
 }
 
 void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens_in) {
   using clk = std::chrono::steady_clock;
-  const int L = cfg.L, M = cfg.M, k = cfg.top_k, d = cfg.d;
+  const int L = cfg.L, M = cfg.M, k = cfg.top_k;
   if (B < 1 || B > cfg.max_batch) throw ValueError("batch size outside [1, max_batch]");
   std::vector<int64_t> tokens = tokens_in;
   if (tokens.empty()) tokens.push_back(-(int64_t)(steps + 1));  // unique prediction-cache key
-  cudaEvent_t t_begin, t_end;
-  CK(cudaEventCreate(&t_begin));
-  CK(cudaEventCreate(&t_end));
-  CK(cudaEventRecord(t_begin, stream));
-  CKS(ef_rmsnorm(stream, h, x_d, B, d, 1e-6f));
-  ++launches;
-  std::vector<double> gate(M);
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  if (cfg.timing) {
+    CK(cudaEventCreate(&t_begin));
+    CK(cudaEventCreate(&t_end));
+    CK(cudaEventRecord(t_begin, stream));
+  }
+  CKS(launch_init_stats(stream, stats_d, L));
+  CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
+  launches += 2;
+  residency_mask(0, cur_mask);
+  hctrl[0].mask[0] = cur_mask[0];
+  hctrl[0].mask[1] = cur_mask[1];
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+
   std::vector<int64_t> gsizes(B, 1);
   double host_acc = 0;
-  for (int l = 0; l < L; ++l) {
-    // (b) how many future router matrices to score at this layer
-    int R = 1;
-    if (l == 0)  // the boundary state of a new token is set after its layer-0 routing
-      R = Rmax;
-    else
-      R = 1 + std::min(st->planned_horizon(l), Rmax - 1);
-    R = std::min(R, L - l);
-    // cache-aware bias mask: residency before this layer's step
-    uint64_t mlo = 0, mhi = 0;
-    if (cfg.routing_bias != 0.f)
-      for (int e = 0; e < M; ++e)
-        if (st->resident(l, e)) (e < 64 ? mlo : mhi) |= 1ull << (e & 63);
-    CKS(ef_router_logits(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R, B,
-                         d, M, logits_d));
-    ++launches;
-    if (cfg.shared_ff && cfg.shared_gate) {
-      CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
-                           1, sgl_d));
-      ++launches;
-    }
-    CKS(ef_route_permute(stream, logits_d, B, M, k, cfg.route_mode, cfg.routing_bias, mlo, mhi,
-                         sel_d, wts_d, counts_d, offsets_d, perm_d, inv_d));
-    ++launches;
-    CK(cudaMemcpyAsync(logits_h, logits_d, (size_t)R * B * M * sizeof(float),
-                       cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(sel_h, sel_d, (size_t)B * k * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                       stream));
-    d2h_bytes += (int64_t)R * B * M * 4 + (int64_t)B * k * 4;
-    CK(cudaStreamSynchronize(stream));
-    auto h0 = clk::now();
-    // ---- scheduler view of this layer's routing (workload.py:161-179 contract)
-    LayerRouting r;
-    r.gate.resize(M);
-    batch_gate(logits_h, B, M, r.gate.data());
-    std::set<int> uni;
-    r.group_actual.resize(B);
-    for (int t = 0; t < B; ++t) {
-      std::vector<int> g(sel_h + t * k, sel_h + (t + 1) * k);
-      std::sort(g.begin(), g.end());
-      for (int e : g) uni.insert(e);
-      r.group_actual[t] = g;
-    }
-    r.actual.assign(uni.begin(), uni.end());
-    if (cfg.record_routing)
-      rlog.push_back(RoutingRec{std::vector<float>(logits_h, logits_h + (int64_t)R * B * M),
-                                std::vector<int32_t>(sel_h, sel_h + B * k), R, B, mlo, mhi});
-    const int Rl = R;
-    hooks->pregate_fn = [this, Rl, B, M](int layer, int hz, double* out) {
-      if (hz >= Rl) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
-      batch_gate(logits_h + (int64_t)hz * B * M, B, M, out);
-    };
-    if (l == 0) st->begin_token(tokens, gsizes, r);
-    std::fill(layer_use.begin(), layer_use.end(), -1);
-    st->begin_layer(l);
-    st->run_layer(l, r);
-    host_acc += std::chrono::duration<double, std::milli>(clk::now() - h0).count();
-
-    // ---- (d) expert FFN over the slots the scheduler resolved
-    std::vector<int> cnt(M, 0);
-    for (int i = 0; i < B * k; ++i) cnt[sel_h[i]]++;
-    std::vector<const char*> wb;
-    std::vector<int32_t> p0, nr;
-    int run = 0;
-    if (cfg.timing) CK(cudaEventRecord(stall_a[l], stream));
-    for (int e = 0; e < M; ++e) {
-      if (cnt[e]) {
-        int s = layer_use[e];
-        if (s < 0) throw RuntimeErr("routed expert has no resolved slot");
-        if (fill_recorded[s]) CK(cudaStreamWaitEvent(stream, fill_ev[s], 0));
-        wb.push_back(slab + (int64_t)s * stride);
-        p0.push_back(run);
-        nr.push_back(cnt[e]);
+  int enq = 0;
+  int l = 0;
+  try {
+    enqueue_layer(stream, 0, B, h);
+    enq = 1;
+    for (l = 0; l < L; ++l) {
+      if (enq < L) {  // keep the GPU one layer ahead of the host
+        enqueue_layer(stream, enq, B, h);
+        ++enq;
       }
-      run += cnt[e];
+      // ---- wait for route(l) to publish its selection
+      HostOut* ho = out(l);
+      auto w0 = clk::now();
+      unsigned spins = 0;
+      while (ho->done == 0u) {
+        _mm_pause();
+        if ((++spins & 0xffff) == 0 &&
+            std::chrono::duration<double>(clk::now() - w0).count() > 60.0)
+          throw RuntimeErr("route kernel did not publish within 60 s");
+      }
+      std::atomic_thread_fence(std::memory_order_acquire);
+      ho->done = 0u;
+      auto h0 = clk::now();
+      const int32_t* sel = out_sel(l);
+      const float* lg0 = out_logits(l);
+      const int R = std::min(Rmax, L - l);
+      // ---- scheduler view of this layer's routing (workload.py:161-179 contract)
+      LayerRouting r;
+      r.gate.resize(M);
+      batch_gate(lg0, B, M, cfg.routing_bias, cur_mask, r.gate.data());
+      std::vector<int> cnt(M, 0);
+      r.group_actual.resize(B);
+      for (int t = 0; t < B; ++t) {
+        std::vector<int> g(sel + t * k, sel + (t + 1) * k);
+        for (int e : g) {
+          if (e < 0 || e >= M) throw RuntimeErr("route kernel produced an invalid expert id");
+          cnt[e]++;
+        }
+        std::sort(g.begin(), g.end());
+        r.group_actual[t] = std::move(g);
+      }
+      for (int e = 0; e < M; ++e)
+        if (cnt[e]) r.actual.push_back(e);
+      bool fetched = false;
+      auto fetch_rows = [&]() {
+        if (fetched || R <= 1) return;
+        CK(cudaMemcpyAsync(logits_h + (int64_t)B * M, logits_d + (int64_t)B * M,
+                           (size_t)(R - 1) * B * M * sizeof(float), cudaMemcpyDeviceToHost,
+                           side_stream));
+        CK(cudaStreamSynchronize(side_stream));
+        d2h_bytes += (int64_t)(R - 1) * B * M * 4;
+        fetched = true;
+      };
+      hooks->pregate_fn = [&, R](int layer, int hz, double* o) {
+        if (hz >= R) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
+        fetch_rows();
+        uint64_t m[2];
+        residency_mask(layer + hz, m);
+        batch_gate(logits_h + (int64_t)hz * B * M, B, M, cfg.routing_bias, m, o);
+      };
+      if (cfg.record_routing) {
+        fetch_rows();
+        std::vector<float> lg((int64_t)R * B * M);
+        std::memcpy(lg.data(), lg0, sizeof(float) * B * M);
+        if (R > 1)
+          std::memcpy(lg.data() + (int64_t)B * M, logits_h + (int64_t)B * M,
+                      sizeof(float) * (R - 1) * B * M);
+        rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(sel, sel + B * k), R, B,
+                                  cur_mask[0], cur_mask[1]});
+      }
+      if (l == 0) st->begin_token(tokens, gsizes, r);
+      std::fill(layer_use.begin(), layer_use.end(), -1);
+      st->begin_layer(l);
+      st->run_layer(l, r);
+      // ---- publish the decision: slots, rows, copy sequence numbers
+      HostCtrl& hc = hctrl[l];
+      int n = 0, run = 0;
+      for (int e = 0; e < M; ++e) {
+        if (cnt[e]) {
+          int s = layer_use[e];
+          if (s < 0) throw RuntimeErr("routed expert has no resolved slot");
+          hc.ent[n] = make_int4(s, run, cnt[e], (int)slot_seq[s]);
+          ++n;
+        }
+        run += cnt[e];
+      }
+      hc.n_active = n;
+      ffn_bytes += (int64_t)n * stride;
+      ffn_launches += 2;
+      if (l + 1 < L) {
+        residency_mask(l + 1, cur_mask);
+        hctrl[l + 1].mask[0] = cur_mask[0];
+        hctrl[l + 1].mask[1] = cur_mask[1];
+      }
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      _mm_sfence();
+      hc.go = 1u;
+      host_acc += std::chrono::duration<double, std::milli>(clk::now() - h0).count();
+      // slots read by FFN(l) become reusable at the decision of layer l+1
+      for (int s : pinned_list) pinned[s] = 0;
+      pinned_list.clear();
+      for (int s : deferred_free) free_slots.push_back(s);
+      deferred_free.clear();
     }
-    if (cfg.timing) CK(cudaEventRecord(stall_b[l], stream));
-    CKS(expert_ffn_ptrs(stream, x_d, perm_d, k, false, wb.data(), p0.data(), nr.data(),
-                        (int)wb.size(), d, cfg.ff, cfg.dtype, act_d, y_d));
-    launches += 2;
-    const float* ys = nullptr;
-    if (cfg.shared_ff) {
-      const char* sw = shared_w + (int64_t)l * sstride;
-      int32_t z = 0, nb = B;
-      CKS(expert_ffn_ptrs(stream, x_d, perm_d, k, true, &sw, &z, &nb, 1, d, cfg.shared_ff,
-                          cfg.dtype, acts_d, ys_d));
-      launches += 2;
-      ys = ys_d;
-    }
-    CKS(ef_combine(stream, h, x_d, y_d, inv_d, wts_d, ys,
-                   (cfg.shared_ff && cfg.shared_gate) ? sgl_d : nullptr, B, d, k, 1e-6f));
-    ++launches;
-    // release the layer's slots behind a reader event
-    int ri = ring_next;
-    ring_next = (ring_next + 1) % (int)reader_ring.size();
-    CK(cudaEventRecord(reader_ring[ri], stream));
-    for (int s : pinned_list) {
-      reader_of[s] = ri;
-      pinned[s] = 0;
-    }
-    pinned_list.clear();
-    for (int s : deferred_free) free_slots.push_back(s);
-    deferred_free.clear();
+    st->end_token();
+  } catch (...) {
+    abort_pipeline(stream, l, enq);
+    if (t_begin) cudaEventDestroy(t_begin);
+    if (t_end) cudaEventDestroy(t_end);
+    throw;
   }
-  st->end_token();
-  CK(cudaEventRecord(t_end, stream));
-  CK(cudaEventSynchronize(t_end));
-  float ms = 0;
-  CK(cudaEventElapsedTime(&ms, t_begin, t_end));
-  step_ms += ms;
-  if (cfg.timing) {
-    for (int l = 0; l < L; ++l) {
-      float a = 0;
-      CK(cudaEventElapsedTime(&a, stall_a[l], stall_b[l]));
-      stall_ms += a;
-    }
-  }
-  cudaEventDestroy(t_begin);
-  cudaEventDestroy(t_end);
   host_ms += host_acc;
   ++steps;
+  if (cfg.timing) {
+    CK(cudaEventRecord(t_end, stream));
+    CK(cudaEventSynchronize(t_end));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, t_begin, t_end));
+    step_ms += ms;
+    CK(cudaMemcpy(stats_h.data(), stats_d, sizeof(unsigned long long) * 8 * L,
+                  cudaMemcpyDeviceToHost));
+    for (int j = 0; j < L; ++j) {
+      const unsigned long long* sj = &stats_h[8 * j];
+      stall_ms += sj[2] * 1e-6;
+      if (sj[1] >= sj[0]) bubble_ms += (sj[1] - sj[0]) * 1e-6;
+      if (sj[3] != ~0ull && sj[4] > sj[3]) ffn_ms += (sj[4] - sj[3]) * 1e-6;
+    }
+    cudaEventDestroy(t_begin);
+    cudaEventDestroy(t_end);
+  }
 }
 
 extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
@@ -409,6 +518,8 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       throw ValueError("d must be a multiple of 256 and ff of 8");
     if (c.dtype != EF_BF16 && c.dtype != EF_F32) throw ValueError("dtype must be bf16 or f32");
     if (c.max_batch < 1 || c.max_batch * c.top_k > 1024) throw ValueError("bad max_batch");
+    if (std::min(c.max_batch * c.top_k, c.M) > kMaxActive)
+      throw ValueError("more routed experts per layer than the control block holds");
     if (c.staging_slots < 1) throw ValueError("staging_slots must be >= 1");
     e->esz = c.dtype == EF_BF16 ? 2 : 4;
     e->stride = 3LL * c.d * c.ff * e->esz;
@@ -426,19 +537,20 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->st->set_observer(&e->mirror);
     int64_t cap = e->st->cache().capacity();
     e->P = (int)(cap + c.staging_slots);
-    int pol_max = e->simcfg.policy.max_step >= 0 ? e->simcfg.policy.max_step : std::max(1, c.L - 1);
+    int pol_max =
+        e->simcfg.policy.max_step >= 0 ? e->simcfg.policy.max_step : std::max(1, c.L - 1);
     e->Rmax = 1 + std::min(pol_max, c.L - 1);
     if (e->simcfg.policy.strategy == 2) e->Rmax = 1 + std::min(e->simcfg.policy.interval, c.L - 1);
     if (e->simcfg.policy.strategy == 1) e->Rmax = std::min(2, c.L);
     if (e->simcfg.policy.strategy == 0) e->Rmax = 1;
 
     CK(cudaSetDevice(c.device));
-    const int B = c.max_batch, M = c.M, k = c.top_k, d = c.d;
+    const int B = c.max_batch, M = c.M, k = c.top_k, d = c.d, L = c.L;
     CK(cudaMalloc(&e->slab, (size_t)e->P * e->stride));
-    CK(cudaMalloc(&e->router_w, (size_t)c.L * M * d * e->esz));
+    CK(cudaMalloc(&e->router_w, (size_t)L * M * d * e->esz));
     if (c.shared_ff) {
-      CK(cudaMalloc(&e->shared_w, (size_t)c.L * e->sstride));
-      CK(cudaMalloc(&e->sgate_w, (size_t)c.L * d * e->esz));
+      CK(cudaMalloc(&e->shared_w, (size_t)L * e->sstride));
+      CK(cudaMalloc(&e->sgate_w, (size_t)L * d * e->esz));
       CK(cudaMalloc(&e->acts_d, (size_t)B * c.shared_ff * e->esz));
       CK(cudaMalloc(&e->ys_d, (size_t)B * d * 4));
     }
@@ -453,28 +565,31 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     CK(cudaMalloc(&e->inv_d, (size_t)B * k * 4));
     CK(cudaMalloc(&e->act_d, (size_t)B * k * c.ff * e->esz));
     CK(cudaMalloc(&e->y_d, (size_t)B * k * d * 4));
+    CK(cudaMalloc(&e->dctrl, sizeof(DevCtrl) * L));
+    CK(cudaMalloc(&e->ready, sizeof(uint32_t) * e->P));
+    CK(cudaMemset(e->ready, 0, sizeof(uint32_t) * e->P));
+    CK(cudaMalloc(&e->stats_d, sizeof(unsigned long long) * 8 * L));
+    e->stats_h.assign(8 * L, 0);
+    // mapped control blocks
+    CK(cudaHostAlloc(&e->hctrl, sizeof(HostCtrl) * L, cudaHostAllocMapped));
+    std::memset((void*)e->hctrl, 0, sizeof(HostCtrl) * L);
+    CK(cudaHostGetDevicePointer((void**)&e->hctrl_dev, e->hctrl, 0));
+    e->out_stride =
+        ((int64_t)sizeof(HostOut) + (int64_t)B * k * 4 + (int64_t)B * M * 4 + 127) / 128 * 128;
+    CK(cudaHostAlloc(&e->hout, e->out_stride * L, cudaHostAllocMapped));
+    std::memset(e->hout, 0, e->out_stride * L);
+    CK(cudaHostGetDevicePointer((void**)&e->hout_dev, e->hout, 0));
     CK(cudaHostAlloc(&e->logits_h, (size_t)e->Rmax * B * M * 4, cudaHostAllocDefault));
-    CK(cudaHostAlloc(&e->sel_h, (size_t)B * k * 4, cudaHostAllocDefault));
-    e->store.assign(c.L, nullptr);
-    for (int l = 0; l < c.L; ++l)
+    e->store.assign(L, nullptr);
+    for (int l = 0; l < L; ++l)
       CK(cudaHostAlloc(&e->store[l], (size_t)M * e->stride, cudaHostAllocDefault));
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     CK(cudaStreamCreateWithPriority(&e->copy_stream, cudaStreamNonBlocking, prio_hi));
-    e->fill_ev.resize(e->P);
-    e->fill_recorded.assign(e->P, 0);
-    e->reader_of.assign(e->P, -1);
+    CK(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking));
+    e->slot_seq.assign(e->P, 0);
     e->pinned.assign(e->P, 0);
-    for (auto& ev : e->fill_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    e->reader_ring.resize(std::max(64, 2 * c.L));
-    for (auto& ev : e->reader_ring) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    if (c.timing) {
-      e->stall_a.resize(c.L);
-      e->stall_b.resize(c.L);
-      for (auto& ev : e->stall_a) CK(cudaEventCreate(&ev));
-      for (auto& ev : e->stall_b) CK(cudaEventCreate(&ev));
-    }
-    e->phys_of.assign((size_t)c.L * M, -1);
+    e->phys_of.assign((size_t)L * M, -1);
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
     e->init_weights();
@@ -514,21 +629,22 @@ extern "C" int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len,
 
 extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   EF_TRY({
-    double v[13] = {(double)e->steps,         (double)e->copies,
+    double v[16] = {(double)e->steps,         (double)e->copies,
                     (double)e->copy_bytes,    e->stall_ms,
                     (double)e->P,             (double)e->st->cache().capacity(),
                     (double)e->cfg.staging_slots, (double)e->launches,
                     e->host_ms,               e->ffn_ms,
                     e->step_ms,               (double)e->preload_copies,
-                    (double)e->d2h_bytes};
-    for (int i = 0; i < n && i < 13; ++i) out[i] = v[i];
+                    (double)e->d2h_bytes,     (double)e->ffn_bytes,
+                    (double)e->ffn_launches,  e->bubble_ms};
+    for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
   });
 }
 
 extern "C" int ef_engine_ptr(ef_engine* e, int which, void** out) {
   EF_TRY({
-    void* p[10] = {e->slab,   e->router_w, e->shared_w, e->logits_d, e->sel_d,
-                   e->wts_d,  e->perm_d,   e->inv_d,    e->y_d,      e->x_d};
+    void* p[10] = {e->slab,  e->router_w, e->shared_w, e->logits_d, e->sel_d,
+                   e->wts_d, e->perm_d,   e->inv_d,    e->y_d,      e->x_d};
     if (which < 0 || which >= 10) throw ValueError("unknown pointer id");
     *out = p[which];
   });

@@ -14,11 +14,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <string>
 
 #include "../../include/expertflow.h"
 #include "kernels.cuh"
+#include "pipeline.h"
 
 namespace ef {
 extern thread_local std::string g_last_error;
@@ -192,11 +194,17 @@ constexpr int kMaxExperts = 256;
 __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
     const float* __restrict__ logits, int B, int M, int k, int mode, float bias, uint64_t mlo,
     uint64_t mhi, int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts,
-    int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+    int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv,
+    const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
+    volatile uint32_t* host_done) {
   __shared__ int32_t warp_cnt[32][kMaxExperts];
   __shared__ int32_t base[kMaxExperts];
   __shared__ int32_t total[kMaxExperts];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (mask_src) {  // engine pipeline: the host publishes the residency mask before go(l-1)
+    mlo = mask_src[0];
+    mhi = mask_src[1];
+  }
 
   // ---- top-k and weights: one thread per token
   for (int t = tid; t < B; t += blockDim.x) {
@@ -286,6 +294,16 @@ __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
   }
   __syncthreads();
   for (int f = tid; f < N; f += blockDim.x) perm[inv[f]] = f;
+  if (host_done) {  // publish the selection and row-0 logits to mapped host memory
+    for (int f = tid; f < N; f += blockDim.x) host_sel[f] = sel[f];
+    for (int i = tid; i < B * M; i += blockDim.x) host_logits[i] = logits[i];
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      *host_done = 1u;
+    }
+  }
 }
 
 extern "C" int ef_route_permute(void* stream, const float* logits, int B, int M, int k, int mode,
@@ -294,13 +312,16 @@ extern "C" int ef_route_permute(void* stream, const float* logits, int B, int M,
   EF_CHECK_ARG(M >= 1 && M <= 128 && k >= 1 && k <= 16 && k <= M && B >= 0, "bad route shape");
   EF_CHECK_ARG(mode == EF_ROUTE_MIXTRAL || mode == EF_ROUTE_SOFTMAX_TOPK, "bad routing mode");
   route_permute_kernel<<<1, kRouteThreads, 0, S(stream)>>>(logits, B, M, k, mode, bias, mlo, mhi,
-                                                           sel, wts, counts, offsets, perm, inv);
+                                                           sel, wts, counts, offsets, perm, inv,
+                                                           nullptr, nullptr, nullptr, nullptr);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
 
 // ============================================================ (d) decode expert FFN
-constexpr int kMaxActive = 80;
+using ef::kMaxActive;
+using ef::DevCtrl;
+using ef::HostCtrl;
 struct ActiveList {
   const char* w[kMaxActive];  // expert weight base ([W1|W3|W2])
   int32_t p0[kMaxActive];     // first permuted row (also output row)
@@ -345,21 +366,69 @@ struct XAct {  // act[p] (already in the weight dtype)
 
 // rows x cols matrix A (and B when DUAL) streamed once per token chunk; each
 // warp owns R consecutive output rows; lanes stride the columns in 16 B.
+// Engine pipeline control (pipeline.h): the gate kernel copies the host's
+// per-layer decision into DevCtrl; entries are {slot, p0, rows, need_seq}; a
+// slot is usable once ready[slot] >= need_seq (set by the copy stream after
+// the swap-in lands).
+struct CtrlSrc {
+  const DevCtrl* ctrl;
+  const char* slab;
+  int64_t stride;
+  const volatile uint32_t* ready;
+  unsigned long long* stats;  // per layer: [0] gate enter [1] go [2] max wait [3] ffn start [4] ffn end
+  bool wait_ready;            // first kernel of the pair waits for the copies
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <typename WT, int NT, int R, bool DUAL, typename XL>
-__global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, int64_t offA, int64_t offB,
-                                                       int rows, int cols, XL xl, WT* act_out,
-                                                       float* y_out, int out_ld) {
+__global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs, int64_t offA,
+                                                       int64_t offB, int rows, int cols, XL xl,
+                                                       WT* act_out, float* y_out, int out_ld) {
   constexpr int V = WTraits<WT>::kPer16;
   constexpr int WARPS = 4;
   const int a = blockIdx.y;
-  const int n_all = al.n[a];
-  if (n_all == 0) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int n_all, p0;
+  const char* wbase;
+  if (cs.ctrl) {
+    __shared__ int4 e_sh;
+    if (threadIdx.x == 0) {
+      int4 e = make_int4(0, 0, 0, 0);
+      if (a < cs.ctrl->n_active) e = cs.ctrl->ent[a];
+      if (cs.wait_ready && e.z > 0) {
+        unsigned long long t0 = globaltimer();
+        unsigned need = (unsigned)e.w;
+        if (cs.ready[e.x] < need) {
+          while (cs.ready[e.x] < need) {
+            __nanosleep(256);
+            if (globaltimer() - t0 > 60000000000ull) asm volatile("trap;");
+          }
+          atomicMax(&cs.stats[2], globaltimer() - t0);
+        }
+        atomicMin(&cs.stats[3], globaltimer());
+      }
+      e_sh = e;
+    }
+    __syncthreads();
+    int4 e = e_sh;
+    n_all = e.z;
+    p0 = e.y;
+    wbase = cs.slab + (int64_t)e.x * cs.stride;
+  } else {
+    n_all = al.n[a];
+    p0 = al.p0[a];
+    wbase = al.w[a];
+  }
+  if (n_all == 0) return;
   const int j0 = (blockIdx.x * WARPS + wid) * R;
   if (j0 >= rows) return;
-  const WT* A = reinterpret_cast<const WT*>(al.w[a] + offA);
-  const WT* Bm = reinterpret_cast<const WT*>(al.w[a] + offB);
-  const int p0 = al.p0[a];
+  const WT* A = reinterpret_cast<const WT*>(wbase + offA);
+  const WT* Bm = reinterpret_cast<const WT*>(wbase + offB);
 
   for (int tc = 0; tc < n_all; tc += NT) {
     const int nt = min(NT, n_all - tc);
@@ -422,33 +491,36 @@ __global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, int64_t of
       }
     }
   }
+  if (cs.ctrl && !DUAL && cs.stats && lane == 0) atomicMax(&cs.stats[4], globaltimer());
 }
 
 template <typename WT, int NT>
-static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, int n_active, int d, int ff,
-                          const XGather<WT>& xg, WT* act, float* y) {
+static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& cs, int n_active,
+                          int d, int ff, const XGather<WT>& xg, WT* act, float* y) {
   constexpr int R = 4, WARPS = 4;
   const int64_t es = sizeof(WT);
   dim3 gu((ff + WARPS * R - 1) / (WARPS * R), n_active);
   ffn_gemv_kernel<WT, NT, R, true, XGather<WT>>
-      <<<gu, 128, 0, st>>>(al, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
+      <<<gu, 128, 0, st>>>(al, cs, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
   dim3 gd((d + WARPS * R - 1) / (WARPS * R), n_active);
   XAct<WT> xa{act, ff};
+  CtrlSrc cs2 = cs;
+  cs2.wait_ready = false;
   ffn_gemv_kernel<WT, NT, R, false, XAct<WT>>
-      <<<gd, 128, 0, st>>>(al, 2 * (int64_t)ff * d * es, 0, d, ff, xa, nullptr, y, d);
+      <<<gd, 128, 0, st>>>(al, cs2, 2 * (int64_t)ff * d * es, 0, d, ff, xa, nullptr, y, d);
 }
 
 template <typename WT>
-static void launch_ffn(cudaStream_t st, const ActiveList& al, int n_active, int max_rows, int d,
-                       int ff, const XGather<WT>& xg, WT* act, float* y) {
+static void launch_ffn(cudaStream_t st, const ActiveList& al, const CtrlSrc& cs, int n_active,
+                       int max_rows, int d, int ff, const XGather<WT>& xg, WT* act, float* y) {
   if (max_rows <= 1)
-    launch_ffn_nt<WT, 1>(st, al, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 1>(st, al, cs, n_active, d, ff, xg, act, y);
   else if (max_rows <= 2)
-    launch_ffn_nt<WT, 2>(st, al, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 2>(st, al, cs, n_active, d, ff, xg, act, y);
   else if (max_rows <= 4)
-    launch_ffn_nt<WT, 4>(st, al, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 4>(st, al, cs, n_active, d, ff, xg, act, y);
   else
-    launch_ffn_nt<WT, 8>(st, al, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 8>(st, al, cs, n_active, d, ff, xg, act, y);
 }
 
 namespace ef {
@@ -468,13 +540,98 @@ int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k,
     max_rows = std::max(max_rows, nrows[i]);
   }
   if (max_rows == 0) return EF_OK;
+  CtrlSrc cs{};
   if (dtype == EF_BF16) {
     XGather<__nv_bfloat16> xg{x, perm, k, d, identity, identity ? p0[0] : 0};
-    launch_ffn<__nv_bfloat16>(st, al, n_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y);
+    launch_ffn<__nv_bfloat16>(st, al, cs, n_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y);
   } else {
     XGather<float> xg{x, perm, k, d, identity, identity ? p0[0] : 0};
-    launch_ffn<float>(st, al, n_active, max_rows, d, ff, xg, (float*)act, y);
+    launch_ffn<float>(st, al, cs, n_active, max_rows, d, ff, xg, (float*)act, y);
   }
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// Engine pipeline: slots / rows come from the gate-copied DevCtrl at run time.
+int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
+                    int64_t stride, const void* dctrl, const uint32_t* ready,
+                    unsigned long long* stats, int max_active, int max_rows, int d, int ff,
+                    int dtype, void* act, float* y) {
+  EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
+  ActiveList al{};
+  CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
+  if (dtype == EF_BF16) {
+    XGather<__nv_bfloat16> xg{x, perm, k, d, false, 0};
+    launch_ffn<__nv_bfloat16>(st, al, cs, max_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y);
+  } else {
+    XGather<float> xg{x, perm, k, d, false, 0};
+    launch_ffn<float>(st, al, cs, max_active, max_rows, d, ff, xg, (float*)act, y);
+  }
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// ------------------------------------------------------------ pipeline glue
+__global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats) {
+  __shared__ int n_sh;
+  if (threadIdx.x == 0) {
+    unsigned long long t0 = globaltimer();
+    stats[0] = t0;
+    while (hc->go == 0u) {
+      __nanosleep(128);
+      if (globaltimer() - t0 > 60000000000ull) asm volatile("trap;");  // host died: fail loudly
+    }
+    stats[1] = globaltimer();
+    __threadfence_system();
+    n_sh = hc->n_active;
+  }
+  __syncthreads();
+  int n = n_sh;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    volatile int* src = reinterpret_cast<volatile int*>(&hc->ent[i]);
+    dc->ent[i] = make_int4(src[0], src[1], src[2], src[3]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    dc->n_active = n;
+    hc->go = 0u;  // consumed; the host sets it again for the next token's layer
+  }
+}
+
+int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats) {
+  gate_kernel<<<1, 64, 0, st>>>(reinterpret_cast<HostCtrl*>(host_ctrl_dev),
+                                reinterpret_cast<DevCtrl*>(dctrl), stats);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+__global__ void set_ready_kernel(uint32_t* ready, int slot, uint32_t seq) {
+  *(volatile uint32_t*)(ready + slot) = seq;
+}
+
+int launch_set_ready(cudaStream_t st, uint32_t* ready, int slot, uint32_t seq) {
+  set_ready_kernel<<<1, 1, 0, st>>>(ready, slot, seq);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+__global__ void init_stats_kernel(unsigned long long* stats, int L) {
+  for (int i = threadIdx.x; i < L * 8; i += blockDim.x) stats[i] = (i % 8 == 3) ? ~0ull : 0ull;
+}
+
+int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L) {
+  init_stats_kernel<<<1, 256, 0, st>>>(stats, L);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
+                         float bias, int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
+                         int32_t* perm, int32_t* inv, const void* mask_src, int32_t* host_sel,
+                         float* host_logits, uint32_t* host_done) {
+  route_permute_kernel<<<1, kRouteThreads, 0, st>>>(
+      logits, B, M, k, mode, bias, 0ull, 0ull, sel, wts, counts, offsets, perm, inv,
+      reinterpret_cast<const volatile uint64_t*>(mask_src), host_sel, host_logits, host_done);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }

@@ -1,0 +1,47 @@
+// pipeline.h — host/device control blocks of the engine's flag-gated decode
+// pipeline (engine.cu) and the launchers in kernels.cu.
+//
+// Per layer: the route kernel publishes (sel, row-0 logits, done=1) into
+// mapped host memory; the host runs the scheduler step and writes a HostCtrl
+// (slots, rows, copy sequence numbers, next layer's bias mask) then go=1; the
+// gate kernel copies it to DevCtrl, resets go and lets the routed FFN run.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ef {
+constexpr int kMaxActive = 80;
+
+struct HostCtrl {
+  volatile uint32_t go;
+  int32_t n_active;
+  uint64_t mask[2];    // cache-aware bias mask for THIS layer's routing
+  int4 ent[kMaxActive];  // {slot, p0, rows, need_seq}
+};
+
+struct DevCtrl {
+  int32_t n_active, pad[3];
+  int4 ent[kMaxActive];
+};
+
+struct HostOut {  // followed by sel[B*k] int32 and logits[B*M] f32
+  volatile uint32_t done;
+  uint32_t pad[15];
+};
+
+int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k, bool identity,
+                    const char* const* wbase, const int32_t* p0, const int32_t* nrows,
+                    int n_active, int d, int ff, int dtype, void* act, float* y);
+int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
+                    int64_t stride, const void* dctrl, const uint32_t* ready,
+                    unsigned long long* stats, int max_active, int max_rows, int d, int ff,
+                    int dtype, void* act, float* y);
+int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats);
+int launch_set_ready(cudaStream_t st, uint32_t* ready, int slot, uint32_t seq);
+int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L);
+int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
+                         float bias, int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
+                         int32_t* perm, int32_t* inv, const void* mask_src, int32_t* host_sel,
+                         float* host_logits, uint32_t* host_done);
+}  // namespace ef

@@ -164,7 +164,7 @@ class MoEEngine:
     def stats(self) -> dict:
         keys = ["steps", "copies", "copy_bytes", "stall_ms", "phys_slots", "logical_capacity",
                 "staging_slots", "kernel_launches", "host_decision_ms", "ffn_ms", "step_ms",
-                "preload_copies", "d2h_bytes"]
+                "preload_copies", "d2h_bytes", "ffn_bytes", "ffn_launches", "gate_wait_ms"]
         out = (C.c_double * len(keys))()
         L.check(L.lib.ef_engine_stats(self._h.ptr, out, len(keys)))
         return dict(zip(keys, list(out)))
@@ -195,6 +195,11 @@ class MoEEngine:
         L.check(L.lib.ef_engine_ptr(self._h.ptr, which, C.byref(p)))
         return p.value or 0
 
+    def slab_view(self, slot: int) -> torch.Tensor:
+        """uint8 view of one physical slab slot (for checks; no copy)."""
+        base = self.device_ptr(0) + slot * self.cfg.expert_bytes
+        return _raw_device_view(base, self.cfg.expert_bytes, self.device)
+
     def slot_of(self, layer: int, expert: int) -> int:
         s = C.c_int32()
         L.check(L.lib.ef_engine_slot_of(self._h.ptr, layer, expert, C.byref(s)))
@@ -202,6 +207,16 @@ class MoEEngine:
 
     def close(self) -> None:
         self._h = None
+
+
+class _RawDevice:
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def _raw_device_view(ptr: int, nbytes: int, device) -> torch.Tensor:
+    return torch.as_tensor(_RawDevice(ptr, nbytes), device=device)
 
 
 def synthetic_hidden(cfg: MoEConfig, seed: int, step: int, B: int, device) -> torch.Tensor:
