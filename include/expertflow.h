@@ -248,6 +248,17 @@ int ef_combine(void* stream, float* h, float* x, const float* y, const int32_t* 
                const float* wts, const float* ys, const float* shared_gate_logit, int B, int d,
                int k, float eps);
 
+/* (d) prefill expert FFN: TMA + tcgen05 grouped GEMM (grouped_gemm.cu).
+   C[rows, N] = A[rows, K] . B_e^T per tile; A bf16 [a_rows, K] K-contiguous;
+   B bf16 view [b_rows, K] with row pitch b_pitch elements (the slab viewed as
+   one tensor).  tiles: DEVICE int4[n_tiles] = {a_row0, b_row0, m_valid, n0}
+   (128-row m-tiles, 128-column n-tiles, K % 64 == 0).  dual: B rows
+   b_row0+n0.. are W1 and b_row0+dual_off+n0.. are W3; out = bf16
+   silu(A.W1^T) * (A.W3^T).  Otherwise out = fp32 A.B^T.  out_ld in elements. */
+int ef_grouped_gemm_bf16(void* stream, const void* A, int64_t a_rows, int K, const void* B,
+                         int64_t b_rows, int64_t b_pitch, const void* tiles, int n_tiles, int dual,
+                         int dual_off, void* out, int out_ld);
+
 /* ------------------------------------------------------------------ */
 /* MoE decode engine: slab + pinned host store + copy streams + stepper */
 /* ------------------------------------------------------------------ */

@@ -120,6 +120,8 @@ _SIGS = {
     "ef_expert_ffn_decode": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
                                        C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]),
     "ef_combine": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, f32]),
+    "ef_grouped_gemm_bf16": (C.c_int, [vp, vp, i64, C.c_int, vp, i64, i64, vp, C.c_int, C.c_int,
+                                       C.c_int, vp, C.c_int]),
     "ef_engine_create": (C.c_int, [P(EngineCfg), P(SimCfg), P(LadderCfg), P(vp)]),
     "ef_engine_destroy": (None, [vp]),
     "ef_engine_step": (C.c_int, [vp, vp, vp, C.c_int, P(i64), C.c_int]),

@@ -32,6 +32,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -119,6 +120,8 @@ struct ef_engine {
   char* hout_dev = nullptr;
   int64_t out_stride = 0;
   float* logits_h = nullptr;  // pre-gate rows fetched on demand
+  static constexpr uint32_t kSeqRing = 1u << 16;  // pinned sources of the ready-flag copies
+  uint32_t* seq_ring = nullptr;
   std::vector<unsigned long long> stats_h;
   std::vector<char*> store;  // per layer: M * stride bytes
   cudaStream_t copy_stream = nullptr, side_stream = nullptr;
@@ -199,10 +202,15 @@ struct ef_engine {
     CK(cudaMemcpyAsync(slab + (int64_t)s * stride, src, stride, cudaMemcpyHostToDevice,
                        copy_stream));
     uint32_t seq = ++copy_seq;
-    CKS(launch_set_ready(copy_stream, ready, s, seq));
+    // Publish the fill sequence with the copy engine (a 4-byte H2D copy from a
+    // pinned ring right behind the blob on the same stream).  A kernel would
+    // need an SM, and the routed FFN waiting on this flag may hold all of them.
+    uint32_t* src_seq = &seq_ring[seq % kSeqRing];
+    *src_seq = seq;
+    CK(cudaMemcpyAsync(ready + s, src_seq, sizeof(uint32_t), cudaMemcpyHostToDevice,
+                       copy_stream));
     slot_seq[s] = seq;
     ++copies;
-    ++launches;
     copy_bytes += stride;
     if (preload) {
       ++preload_copies;
@@ -220,6 +228,11 @@ struct ef_engine {
   }
 
   void enqueue_layer(cudaStream_t stream, int l, int B, float* h);
+  void enqueue_front(cudaStream_t stream, int l, int B);
+  void enqueue_back(cudaStream_t stream, int l, int B, float* h);
+  bool debug = false;  // EF_PIPE_DEBUG=1: no run-ahead, sync + check after each half-layer
+  bool persistent = true;  // EF_FFN=split selects the two-launch GEMV pair
+  int* counters_d = nullptr;
   void abort_pipeline(cudaStream_t stream, int from, int enq);
   void init_weights();
   void step(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
@@ -286,9 +299,9 @@ ef_engine::~ef_engine() {
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
-                  (void*)dctrl, (void*)ready, (void*)stats_d})
+                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d})
     if (p) cudaFree(p);
-  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h})
+  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring})
     if (p) cudaFreeHost(p);
   for (char* p : store)
     if (p) cudaFreeHost(p);
@@ -299,6 +312,11 @@ ef_engine::~ef_engine() {
 // Enqueue every kernel of layer l: router (+ pre-gate rows), route (publishes
 // to the host), shared expert, gate, routed FFN, combine + next rmsnorm.
 void ef_engine::enqueue_layer(cudaStream_t stream, int l, int B, float* h) {
+  enqueue_front(stream, l, B);
+  enqueue_back(stream, l, B, h);
+}
+
+void ef_engine::enqueue_front(cudaStream_t stream, int l, int B) {
   const int M = cfg.M, k = cfg.top_k, d = cfg.d;
   const int R = std::min(Rmax, cfg.L - l);  // (a)+(b): layer l and pre-gate rows l+1..l+R-1
   CKS(ef_router_logits(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R, B,
@@ -322,11 +340,23 @@ void ef_engine::enqueue_layer(cudaStream_t stream, int l, int B, float* h) {
                         cfg.dtype, acts_d, ys_d));
     launches += 2;
   }
-  CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + 8 * l));
+}
+
+void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
+  const int M = cfg.M, k = cfg.top_k, d = cfg.d;
+  const bool sgate = cfg.shared_ff && cfg.shared_gate;
+  CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + 8 * l,
+                  persistent ? counters_d : nullptr));
   ++launches;
-  CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + 8 * l,
-                      std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
-  launches += 2;
+  if (persistent) {
+    CKS(expert_ffn_persistent(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready,
+                              stats_d + 8 * l, counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
+    launches += 1;
+  } else {
+    CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + 8 * l,
+                        std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
+    launches += 2;
+  }
   CKS(ef_combine(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
                  sgate ? sgl_d : nullptr, B, d, k, 1e-6f));
   ++launches;
@@ -376,11 +406,24 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
   double host_acc = 0;
   int enq = 0;
   int l = 0;
+  auto dbg_sync = [&](const char* what, int layer) {
+    cudaError_t e1 = cudaStreamSynchronize(stream);
+    cudaError_t e2 = cudaStreamSynchronize(copy_stream);
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+      throw CudaErr(std::string("debug sync after ") + what + " of layer " +
+                    std::to_string(layer) + ": " + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  };
   try {
-    enqueue_layer(stream, 0, B, h);
+    if (debug) {
+      dbg_sync("init/rmsnorm", 0);
+      enqueue_front(stream, 0, B);
+      dbg_sync("router/route/shared", 0);
+    } else {
+      enqueue_layer(stream, 0, B, h);
+    }
     enq = 1;
     for (l = 0; l < L; ++l) {
-      if (enq < L) {  // keep the GPU one layer ahead of the host
+      if (!debug && enq < L) {  // keep the GPU one layer ahead of the host
         enqueue_layer(stream, enq, B, h);
         ++enq;
       }
@@ -391,8 +434,8 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
       while (ho->done == 0u) {
         _mm_pause();
         if ((++spins & 0xffff) == 0 &&
-            std::chrono::duration<double>(clk::now() - w0).count() > 60.0)
-          throw RuntimeErr("route kernel did not publish within 60 s");
+            std::chrono::duration<double>(clk::now() - w0).count() > 20.0)
+          throw RuntimeErr("route kernel did not publish within 20 s");
       }
       std::atomic_thread_fence(std::memory_order_acquire);
       ho->done = 0u;
@@ -472,6 +515,16 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
       _mm_sfence();
       hc.go = 1u;
       host_acc += std::chrono::duration<double, std::milli>(clk::now() - h0).count();
+      if (debug) {
+        dbg_sync("copies", l);
+        enqueue_back(stream, l, B, h);
+        dbg_sync("gate/ffn/combine", l);
+        if (l + 1 < L) {
+          enqueue_front(stream, l + 1, B);
+          dbg_sync("router/route/shared", l + 1);
+          enq = l + 2;
+        }
+      }
       // slots read by FFN(l) become reusable at the decision of layer l+1
       for (int s : pinned_list) pinned[s] = 0;
       pinned_list.clear();
@@ -580,6 +633,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     std::memset(e->hout, 0, e->out_stride * L);
     CK(cudaHostGetDevicePointer((void**)&e->hout_dev, e->hout, 0));
     CK(cudaHostAlloc(&e->logits_h, (size_t)e->Rmax * B * M * 4, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&e->seq_ring, sizeof(uint32_t) * ef_engine::kSeqRing, cudaHostAllocDefault));
     e->store.assign(L, nullptr);
     for (int l = 0; l < L; ++l)
       CK(cudaHostAlloc(&e->store[l], (size_t)M * e->stride, cudaHostAllocDefault));
@@ -593,6 +647,11 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
     e->init_weights();
+    const char* dbg = getenv("EF_PIPE_DEBUG");
+    e->debug = dbg && dbg[0] == '1';
+    const char* ffn = getenv("EF_FFN");
+    e->persistent = !(ffn && std::string(ffn) == "split");
+    CK(cudaMalloc(&e->counters_d, sizeof(int) * (kMaxActive + 1)));
     *out = e.release();
   });
 }

@@ -379,6 +379,10 @@ struct CtrlSrc {
   bool wait_ready;            // first kernel of the pair waits for the copies
 };
 
+// ~10 s at 2 GHz: a spin this long means the host side died; fail loudly
+// instead of hanging the GPU.
+constexpr long long kSpinTimeoutCycles = 20000000000LL;
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -404,11 +408,13 @@ __global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs
         unsigned long long t0 = globaltimer();
         unsigned need = (unsigned)e.w;
         if (cs.ready[e.x] < need) {
+          const long long c0 = clock64();  // SM cycles: monotonic, used for the timeout
           while (cs.ready[e.x] < need) {
             __nanosleep(256);
-            if (globaltimer() - t0 > 60000000000ull) asm volatile("trap;");
+            if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
           }
-          atomicMax(&cs.stats[2], globaltimer() - t0);
+          unsigned long long t1 = globaltimer();
+          if (t1 > t0) atomicMax(&cs.stats[2], t1 - t0);
         }
         atomicMin(&cs.stats[3], globaltimer());
       }
@@ -571,15 +577,244 @@ int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k,
   return EF_OK;
 }
 
+// ------------------------------------------------------------ persistent FFN
+// One launch per layer for the routed experts (engine pipeline).  CTAs claim
+// tiles from an atomic counter: first every gate/up tile of every active
+// expert (8 rows of ff each, one row per warp: W1 and W3 rows streamed
+// together, fused SiLU*up), then every down tile (8 rows of d).  A down tile
+// waits only for the up tiles of its own expert (per-expert completion
+// counter) and prefetches its first W2 chunks before waiting.  Claiming is
+// dynamic, so a CTA only ever waits on tiles that running CTAs already
+// claimed: deadlock-free at any occupancy.  Up tiles of an expert whose
+// swap-in is still in flight spin on ready[slot]; tiles of resident experts
+// keep the GPU streaming meanwhile.
+struct PersistArgs {
+  const DevCtrl* ctrl;
+  const char* slab;
+  int64_t stride;
+  const volatile uint32_t* ready;
+  unsigned long long* stats;
+  int* counters;  // [0] tile counter, [1 + a] up tiles done for active expert a
+  const float* x;
+  const int32_t* perm;
+  int k, d, ff;
+  void* act;
+  float* y;
+};
+
+constexpr int kPWarps = 8;  // rows per tile
+constexpr int kPUnroll = 4; // 16-byte chunks in flight per matrix per lane
+
+template <typename WT, int NT>
+__global__ void __launch_bounds__(kPWarps * 32) ffn_persist_kernel(PersistArgs p) {
+  constexpr int V = WTraits<WT>::kPer16;
+  constexpr int CH = 32 * V;  // columns per warp-wide chunk
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ int tile_sh[2];
+  __shared__ int4 ent_sh;
+  const int n_active = p.ctrl->n_active;
+  const int n_up = (p.ff + kPWarps - 1) / kPWarps;
+  const int n_dn = (p.d + kPWarps - 1) / kPWarps;
+  const int total_up = n_active * n_up;
+  const int total = total_up + n_active * n_dn;
+  const int64_t es = sizeof(WT);
+  WT* act = reinterpret_cast<WT*>(p.act);
+  bool started = false;
+  if (threadIdx.x == 0) tile_sh[0] = atomicAdd(&p.counters[0], 1);
+  __syncthreads();
+  int buf = 0;
+  for (;;) {
+    const int t = tile_sh[buf];
+    if (t >= total) break;
+    // claim the next tile early so its atomic latency overlaps this tile
+    if (threadIdx.x == 0) tile_sh[buf ^ 1] = atomicAdd(&p.counters[0], 1);
+    const bool up = t < total_up;
+    const int a = up ? t / n_up : (t - total_up) / n_dn;
+    const int row = (up ? t % n_up : (t - total_up) % n_dn) * kPWarps + wid;
+    if (threadIdx.x == 0) {
+      int4 e = p.ctrl->ent[a];
+      if (up) {
+        unsigned need = (unsigned)e.w;
+        if (p.ready[e.x] < need) {
+          unsigned long long t0 = globaltimer();
+          const long long c0 = clock64();
+          while (p.ready[e.x] < need) {
+            __nanosleep(256);
+            if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+          }
+          unsigned long long t1 = globaltimer();
+          if (t1 > t0) atomicMax(&p.stats[2], t1 - t0);
+        }
+      }
+      ent_sh = e;
+      if (!started) atomicMin(&p.stats[3], globaltimer());
+    }
+    started = true;
+    __syncthreads();
+    const int4 e = ent_sh;
+    const char* w = p.slab + (int64_t)e.x * p.stride;
+    const int p0 = e.y, n_all = e.z;
+    if (up) {
+      const int rows = p.ff, cols = p.d;
+      const WT* A = reinterpret_cast<const WT*>(w) + (int64_t)min(row, rows - 1) * cols;
+      const WT* Bm = reinterpret_cast<const WT*>(w + (int64_t)rows * cols * es) +
+                     (int64_t)min(row, rows - 1) * cols;
+      for (int tc = 0; tc < n_all; tc += NT) {
+        const int nt = min(NT, n_all - tc);
+        const float* xr[NT];
+#pragma unroll
+        for (int q = 0; q < NT; ++q) xr[q] = p.x + (int64_t)(p.perm[p0 + tc + (q < nt ? q : 0)] / p.k) * cols;
+        float ga[NT], ua[NT];
+#pragma unroll
+        for (int q = 0; q < NT; ++q) ga[q] = ua[q] = 0.f;
+        for (int c0 = lane * V; c0 < cols; c0 += kPUnroll * CH) {
+          uint4 wa[kPUnroll], wb[kPUnroll];
+#pragma unroll
+          for (int u = 0; u < kPUnroll; ++u) {
+            int c = c0 + u * CH;
+            if (c < cols) {
+              wa[u] = ld_stream16(A + c);
+              wb[u] = ld_stream16(Bm + c);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kPUnroll; ++u) {
+            int c = c0 + u * CH;
+            if (c < cols) {
+              float fa[V], fb[V];
+              WTraits<WT>::unpack(wa[u], fa);
+              WTraits<WT>::unpack(wb[u], fb);
+#pragma unroll
+              for (int q = 0; q < NT; ++q) {
+                if (q < nt) {
+                  const float4* xp = reinterpret_cast<const float4*>(xr[q] + c);
+#pragma unroll
+                  for (int v4 = 0; v4 < V / 4; ++v4) {
+                    float4 xv = __ldg(xp + v4);
+                    float xs[4] = {WTraits<WT>::cast(xv.x), WTraits<WT>::cast(xv.y),
+                                   WTraits<WT>::cast(xv.z), WTraits<WT>::cast(xv.w)};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                      ga[q] = fmaf(fa[4 * v4 + i], xs[i], ga[q]);
+                      ua[q] = fmaf(fb[4 * v4 + i], xs[i], ua[q]);
+                    }
+                  }
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          if (q < nt) {
+            float g = warp_sum(ga[q]);
+            float u = warp_sum(ua[q]);
+            if (lane == 0 && row < rows)
+              WTraits<WT>::store(act + (int64_t)(p0 + tc + q) * rows + row, g / (1.0f + expf(-g)) * u);
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&p.counters[1 + a], 1);
+      }
+    } else {
+      const int rows = p.d, cols = p.ff;
+      const WT* A = reinterpret_cast<const WT*>(w + 2 * (int64_t)p.ff * p.d * es) +
+                    (int64_t)min(row, rows - 1) * cols;
+      // prefetch the first W2 chunks, then wait for this expert's up tiles
+      uint4 pre[kPUnroll];
+#pragma unroll
+      for (int u = 0; u < kPUnroll; ++u) {
+        int c = lane * V + u * CH;
+        if (c < cols) pre[u] = ld_stream16(A + c);
+      }
+      if (threadIdx.x == 0) {
+        volatile int* done = p.counters + 1 + a;
+        const long long c0 = clock64();
+        while (*done < n_up) {
+          __nanosleep(64);
+          if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      for (int tc = 0; tc < n_all; tc += NT) {
+        const int nt = min(NT, n_all - tc);
+        float acc[NT];
+#pragma unroll
+        for (int q = 0; q < NT; ++q) acc[q] = 0.f;
+        for (int c0 = lane * V; c0 < cols; c0 += kPUnroll * CH) {
+          uint4 wa[kPUnroll];
+#pragma unroll
+          for (int u = 0; u < kPUnroll; ++u) {
+            int c = c0 + u * CH;
+            if (c < cols) wa[u] = (tc == 0 && c0 == lane * V) ? pre[u] : ld_stream16(A + c);
+          }
+#pragma unroll
+          for (int u = 0; u < kPUnroll; ++u) {
+            int c = c0 + u * CH;
+            if (c < cols) {
+              float fa[V];
+              WTraits<WT>::unpack(wa[u], fa);
+#pragma unroll
+              for (int q = 0; q < NT; ++q) {
+                if (q < nt) {
+                  // act was written by other CTAs of this launch: bypass L1
+                  uint4 av = __ldcg(reinterpret_cast<const uint4*>(
+                      act + (int64_t)(p0 + tc + q) * cols + c));
+                  float fx[V];
+                  WTraits<WT>::unpack(av, fx);
+#pragma unroll
+                  for (int i = 0; i < V; ++i) acc[q] = fmaf(fa[i], fx[i], acc[q]);
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          if (q < nt) {
+            float g = warp_sum(acc[q]);
+            if (lane == 0 && row < rows) p.y[(int64_t)(p0 + tc + q) * rows + row] = g;
+          }
+        }
+      }
+    }
+    __syncthreads();  // tile_sh[buf] consumed; the claim for the next slot is visible
+    buf ^= 1;
+  }
+  if (started && threadIdx.x == 0) atomicMax(&p.stats[4], globaltimer());
+}
+
+template <typename WT, int NT>
+static int launch_persist_nt(cudaStream_t st, const PersistArgs& pa) {
+  static int grid = 0;
+  if (!grid) {
+    int occ = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffn_persist_kernel<WT, NT>,
+                                                  kPWarps * 32, 0);
+    grid = std::max(1, occ) * sms;
+  }
+  ffn_persist_kernel<WT, NT><<<grid, kPWarps * 32, 0, st>>>(pa);
+  return EF_OK;
+}
+
 // ------------------------------------------------------------ pipeline glue
-__global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats) {
+__global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats,
+                            int* counters) {
   __shared__ int n_sh;
+  if (counters)  // fresh tile / completion counters for this layer's persistent FFN
+    for (int i = threadIdx.x; i <= kMaxActive; i += blockDim.x) counters[i] = 0;
   if (threadIdx.x == 0) {
-    unsigned long long t0 = globaltimer();
-    stats[0] = t0;
+    stats[0] = globaltimer();
+    const long long c0 = clock64();
     while (hc->go == 0u) {
       __nanosleep(128);
-      if (globaltimer() - t0 > 60000000000ull) asm volatile("trap;");  // host died: fail loudly
+      if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");  // host died: fail loudly
     }
     stats[1] = globaltimer();
     __threadfence_system();
@@ -598,9 +833,32 @@ __global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long lo
   }
 }
 
-int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats) {
+int expert_ffn_persistent(cudaStream_t st, const float* x, const int32_t* perm, int k,
+                          const char* slab, int64_t stride, const void* dctrl,
+                          const uint32_t* ready, unsigned long long* stats, int* counters,
+                          int max_rows, int d, int ff, int dtype, void* act, float* y) {
+  PersistArgs pa{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, counters,
+                 x, perm, k, d, ff, act, y};
+  EF_CHECK_ARG(d % 256 == 0 && ff % 8 == 0, "d must be a multiple of 256 and ff of 8");
+  if (dtype == EF_BF16) {
+    if (max_rows <= 1) launch_persist_nt<__nv_bfloat16, 1>(st, pa);
+    else if (max_rows <= 2) launch_persist_nt<__nv_bfloat16, 2>(st, pa);
+    else if (max_rows <= 4) launch_persist_nt<__nv_bfloat16, 4>(st, pa);
+    else launch_persist_nt<__nv_bfloat16, 8>(st, pa);
+  } else {
+    if (max_rows <= 1) launch_persist_nt<float, 1>(st, pa);
+    else if (max_rows <= 2) launch_persist_nt<float, 2>(st, pa);
+    else if (max_rows <= 4) launch_persist_nt<float, 4>(st, pa);
+    else launch_persist_nt<float, 8>(st, pa);
+  }
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats,
+                int* counters) {
   gate_kernel<<<1, 64, 0, st>>>(reinterpret_cast<HostCtrl*>(host_ctrl_dev),
-                                reinterpret_cast<DevCtrl*>(dctrl), stats);
+                                reinterpret_cast<DevCtrl*>(dctrl), stats, counters);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }

@@ -127,6 +127,13 @@ def test_tiny_f32_engine_parity(policy):
                   layer_s=0.0002)
 
 
+def test_split_ffn_kernel_pair_parity(monkeypatch):
+    """The two-launch GEMV pair (EF_FFN=split) against the same oracle."""
+    monkeypatch.setenv("EF_FFN", "split")
+    run_and_check(PRESETS["tiny"], ef.PolicyConfig("a", "adaptive", predictor="pregate"), B=3,
+                  steps=2, budget=16, link_bw=4 * ef.GB, layer_s=0.0002)
+
+
 def test_tiny_bf16_batch32_engine_parity():
     run_and_check(PRESETS["tiny-bf16"], ef.PolicyConfig("a", "adaptive", predictor="pregate"),
                   B=32, steps=2, budget=12, link_bw=ef.GB, layer_s=0.0003)
