@@ -241,6 +241,14 @@ int ef_expert_ffn_decode(void* stream, const float* x, const int32_t* perm, int 
                          const void* slab, int64_t slot_stride_bytes, const int32_t* act_slot,
                          const int32_t* act_off, const int32_t* act_rows, int n_active, int d,
                          int ff, int dtype, void* act, float* y);
+/* (d) the engine's persistent decode FFN (one launch: gate/up tiles then down
+   tiles) on an explicit active list, for tests.  scratch: device buffer of at least
+   4096 + 4 * (max slot + 1) bytes. */
+int ef_expert_ffn_persistent_test(void* stream, const float* x, const int32_t* perm, int k,
+                                  const void* slab, int64_t slot_stride_bytes,
+                                  const int32_t* act_slot, const int32_t* act_off,
+                                  const int32_t* act_rows, int n_active, int max_rows, int d,
+                                  int ff, int dtype, void* act, float* y, void* scratch);
 /* (c) unpermute + weighted combine (rank order) + optional shared expert +
    residual + next rmsnorm:  h[t] += sum_r wts[t,r]*y[inv[t,r]] + g_t*ys[t];
    x = rmsnorm(h).  ys/shared_gate nullable. */
@@ -248,6 +256,9 @@ int ef_combine(void* stream, float* h, float* x, const float* y, const int32_t* 
                const float* wts, const float* ys, const float* shared_gate_logit, int B, int d,
                int k, float eps);
 
+/* (c) prefill permute gather: out[p] = bf16(x[perm[p] / k]) rows, x fp32 [*, d] */
+int ef_gather_rows_bf16(void* stream, const float* x, const int32_t* perm, int k, int d, int n,
+                        void* out);
 /* (d) prefill expert FFN: TMA + tcgen05 grouped GEMM (grouped_gemm.cu).
    C[rows, N] = A[rows, K] . B_e^T per tile; A bf16 [a_rows, K] K-contiguous;
    B bf16 view [b_rows, K] with row pitch b_pitch elements (the slab viewed as

@@ -16,6 +16,10 @@ LIB_PATH = os.path.join(HERE, "libexpertflow.so")
 
 EF_OK, EF_ERUNTIME, EF_ECUDA, EF_ENOMEM, EF_EINVAL = 0, -1, -5, -12, -22
 
+# The engine's pipeline keeps a kernel spinning on a host flag; kernels must
+# not be loaded lazily behind it (see preload_pipeline_kernels in kernels.cu).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} is missing: build it with `python paper_2510_26730_b200/build.py` "
@@ -119,7 +123,11 @@ _SIGS = {
                                    vp, vp, vp, vp, vp]),
     "ef_expert_ffn_decode": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
                                        C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]),
+    "ef_expert_ffn_persistent_test": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
+                                                C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
+                                                vp, vp]),
     "ef_combine": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, f32]),
+    "ef_gather_rows_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "ef_grouped_gemm_bf16": (C.c_int, [vp, vp, i64, C.c_int, vp, i64, i64, vp, C.c_int, C.c_int,
                                        C.c_int, vp, C.c_int]),
     "ef_engine_create": (C.c_int, [P(EngineCfg), P(SimCfg), P(LadderCfg), P(vp)]),

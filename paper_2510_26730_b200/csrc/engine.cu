@@ -647,6 +647,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
     e->init_weights();
+    if (preload_pipeline_kernels() < 30) throw CudaErr("could not load the pipeline kernels");
     const char* dbg = getenv("EF_PIPE_DEBUG");
     e->debug = dbg && dbg[0] == '1';
     const char* ffn = getenv("EF_FFN");

@@ -120,8 +120,10 @@ extern "C" int ef_rmsnorm(void* stream, const float* h, float* x, int B, int d, 
 // the row streams through once.  x is tiny and stays in L1/L2.
 template <typename WT, int MAXB>
 __global__ void router_kernel(const float* __restrict__ x, const WT* __restrict__ w, int rows,
-                              int B, int t0, int nb, int d, int M, float* __restrict__ logits) {
+                              int B, int d, int M, float* __restrict__ logits) {
   constexpr int V = WTraits<WT>::kPer16;
+  const int t0 = blockIdx.y * MAXB;  // token chunk of this CTA row
+  const int nb = min(MAXB, B - t0);
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -162,13 +164,12 @@ static void launch_router(cudaStream_t st, const float* x, const void* w, int R,
                           int M, float* logits) {
   const int rows = R * M, threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
-  for (int t0 = 0; t0 < B; t0 += 8) {  // 8 tokens per pass bounds the accumulators
-    int nb = std::min(8, B - t0);
-    if (nb == 1)
-      router_kernel<WT, 1><<<blocks, threads, 0, st>>>(x, (const WT*)w, rows, B, t0, nb, d, M, logits);
-    else
-      router_kernel<WT, 8><<<blocks, threads, 0, st>>>(x, (const WT*)w, rows, B, t0, nb, d, M, logits);
-  }
+  // one launch; grid.y walks token chunks of 8 (bounds the accumulators)
+  if (B == 1)
+    router_kernel<WT, 1><<<dim3(blocks, 1), threads, 0, st>>>(x, (const WT*)w, rows, B, d, M, logits);
+  else
+    router_kernel<WT, 8><<<dim3(blocks, (B + 7) / 8), threads, 0, st>>>(x, (const WT*)w, rows, B, d,
+                                                                          M, logits);
 }
 
 extern "C" int ef_router_logits(void* stream, const float* x, const void* w, int dtype, int R,
@@ -612,6 +613,7 @@ __global__ void __launch_bounds__(kPWarps * 32) ffn_persist_kernel(PersistArgs p
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __shared__ int tile_sh[2];
   __shared__ int4 ent_sh;
+  __shared__ int landed_sh;  // down tile: slot copy already landed -> W2 prefetch is safe
   const int n_active = p.ctrl->n_active;
   const int n_up = (p.ff + kPWarps - 1) / kPWarps;
   const int n_dn = (p.d + kPWarps - 1) / kPWarps;
@@ -645,6 +647,10 @@ __global__ void __launch_bounds__(kPWarps * 32) ffn_persist_kernel(PersistArgs p
           unsigned long long t1 = globaltimer();
           if (t1 > t0) atomicMax(&p.stats[2], t1 - t0);
         }
+      }
+      else {
+        landed_sh = p.ready[e.x] >= (unsigned)e.w;
+        __threadfence();
       }
       ent_sh = e;
       if (!started) atomicMin(&p.stats[3], globaltimer());
@@ -714,21 +720,21 @@ __global__ void __launch_bounds__(kPWarps * 32) ffn_persist_kernel(PersistArgs p
           }
         }
       }
+      __threadfence();  // every writer publishes its act rows before the count
       __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(&p.counters[1 + a], 1);
-      }
+      if (threadIdx.x == 0) atomicAdd(&p.counters[1 + a], 1);
     } else {
       const int rows = p.d, cols = p.ff;
       const WT* A = reinterpret_cast<const WT*>(w + 2 * (int64_t)p.ff * p.d * es) +
                     (int64_t)min(row, rows - 1) * cols;
-      // prefetch the first W2 chunks, then wait for this expert's up tiles
+      // prefetch the first W2 chunks (only if the slot's swap-in has landed),
+      // then wait for this expert's up tiles
+      const bool pref = landed_sh != 0;
       uint4 pre[kPUnroll];
 #pragma unroll
       for (int u = 0; u < kPUnroll; ++u) {
         int c = lane * V + u * CH;
-        if (c < cols) pre[u] = ld_stream16(A + c);
+        if (pref && c < cols) pre[u] = ld_stream16(A + c);
       }
       if (threadIdx.x == 0) {
         volatile int* done = p.counters + 1 + a;
@@ -750,7 +756,7 @@ __global__ void __launch_bounds__(kPWarps * 32) ffn_persist_kernel(PersistArgs p
 #pragma unroll
           for (int u = 0; u < kPUnroll; ++u) {
             int c = c0 + u * CH;
-            if (c < cols) wa[u] = (tc == 0 && c0 == lane * V) ? pre[u] : ld_stream16(A + c);
+            if (c < cols) wa[u] = (pref && tc == 0 && c0 == lane * V) ? pre[u] : ld_stream16(A + c);
           }
 #pragma unroll
           for (int u = 0; u < kPUnroll; ++u) {
@@ -855,6 +861,39 @@ int expert_ffn_persistent(cudaStream_t st, const float* x, const int32_t* perm, 
   return EF_OK;
 }
 
+// Test entry: run the persistent FFN on an explicit active list (slots are
+// treated as resident).  scratch: device buffer >= sizeof(DevCtrl) +
+// 4*(kMaxActive+1) + 8*8 + 4*max_slot+4 bytes.
+extern "C" int ef_expert_ffn_persistent_test(void* stream, const float* x, const int32_t* perm,
+                                             int k, const void* slab, int64_t stride,
+                                             const int32_t* act_slot, const int32_t* act_off,
+                                             const int32_t* act_rows, int n_active, int max_rows,
+                                             int d, int ff, int dtype, void* act, float* y,
+                                             void* scratch) {
+  EF_CHECK_ARG(n_active >= 0 && n_active <= kMaxActive, "too many active experts");
+  DevCtrl h{};
+  h.n_active = n_active;
+  int max_slot = 0;
+  for (int i = 0; i < n_active; ++i) {
+    h.ent[i] = make_int4(act_slot[i], act_off[i], act_rows[i], 0);
+    max_slot = std::max(max_slot, act_slot[i]);
+  }
+  char* base = reinterpret_cast<char*>(scratch);
+  DevCtrl* dc = reinterpret_cast<DevCtrl*>(base);
+  int* counters = reinterpret_cast<int*>(base + sizeof(DevCtrl));
+  unsigned long long* stats =
+      reinterpret_cast<unsigned long long*>(base + sizeof(DevCtrl) + 4 * (kMaxActive + 2));
+  uint32_t* ready = reinterpret_cast<uint32_t*>(base + sizeof(DevCtrl) + 4 * (kMaxActive + 2) + 64);
+  cudaStream_t st = S(stream);
+  EF_CUDA_RET(cudaMemcpyAsync(dc, &h, sizeof(DevCtrl), cudaMemcpyHostToDevice, st));
+  EF_CUDA_RET(cudaMemsetAsync(counters, 0, 4 * (kMaxActive + 1), st));
+  EF_CUDA_RET(cudaMemsetAsync(stats, 0, 64, st));
+  EF_CUDA_RET(cudaMemsetAsync(ready, 0, 4 * (max_slot + 1), st));
+  EF_CUDA_RET(cudaStreamSynchronize(st));  // h is on the host stack
+  return expert_ffn_persistent(st, x, perm, k, reinterpret_cast<const char*>(slab), stride, dc,
+                               ready, stats, counters, max_rows, d, ff, dtype, act, y);
+}
+
 int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats,
                 int* counters) {
   gate_kernel<<<1, 64, 0, st>>>(reinterpret_cast<HostCtrl*>(host_ctrl_dev),
@@ -893,6 +932,7 @@ int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
+
 }  // namespace ef
 
 extern "C" int ef_expert_ffn_decode(void* stream, const float* x, const int32_t* perm, int k,
@@ -905,6 +945,29 @@ extern "C" int ef_expert_ffn_decode(void* stream, const float* x, const int32_t*
     w[i] = reinterpret_cast<const char*>(slab) + (int64_t)act_slot[i] * stride;
   return ef::expert_ffn_ptrs(S(stream), x, perm, k, false, w, act_off, act_rows, n_active, d, ff,
                              dtype, act, y);
+}
+
+// ============================================================ (c) permute gather (prefill)
+// x_perm[p] = T(x[perm[p] / k]) as bf16 rows for the grouped GEMM's A operand.
+__global__ void gather_rows_bf16_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
+                                        int k, int d, int n, __nv_bfloat16* __restrict__ out) {
+  const int p = blockIdx.x;
+  if (p >= n) return;
+  const float* src = x + (int64_t)(perm[p] / k) * d;
+  __nv_bfloat16* dst = out + (int64_t)p * d;
+  for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
+    float2 v = *reinterpret_cast<const float2*>(src + i);
+    *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(v.x, v.y);
+  }
+}
+
+extern "C" int ef_gather_rows_bf16(void* stream, const float* x, const int32_t* perm, int k, int d,
+                                   int n, void* out) {
+  EF_CHECK_ARG(n >= 0 && d % 2 == 0 && k >= 1, "bad gather shape");
+  if (n == 0) return EF_OK;
+  gather_rows_bf16_kernel<<<n, 256, 0, S(stream)>>>(x, perm, k, d, n, (__nv_bfloat16*)out);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
 }
 
 // ============================================================ (c) combine + norm
@@ -941,3 +1004,46 @@ extern "C" int ef_combine(void* stream, float* h, float* x, const float* y, cons
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
+
+namespace ef {
+// Under CUDA lazy module loading the first launch of a kernel may wait for
+// the device to go idle; the pipeline's gate kernel spins until the host
+// publishes a decision, so every kernel the pipeline launches is loaded up
+// front, while the device is idle.
+template <typename T>
+static void preload(T* fn, int& n) {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(fn)) == cudaSuccess) ++n;
+}
+
+template <typename WT>
+static void preload_dtype(int& n) {
+  preload(router_kernel<WT, 1>, n);
+  preload(router_kernel<WT, 8>, n);
+  preload(ffn_persist_kernel<WT, 1>, n);
+  preload(ffn_persist_kernel<WT, 2>, n);
+  preload(ffn_persist_kernel<WT, 4>, n);
+  preload(ffn_persist_kernel<WT, 8>, n);
+  preload(ffn_gemv_kernel<WT, 1, 4, true, XGather<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 2, 4, true, XGather<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 4, 4, true, XGather<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 8, 4, true, XGather<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 1, 4, false, XAct<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 2, 4, false, XAct<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 4, 4, false, XAct<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 8, 4, false, XAct<WT>>, n);
+}
+
+int preload_pipeline_kernels() {
+  int n = 0;
+  preload_dtype<__nv_bfloat16>(n);
+  preload_dtype<float>(n);
+  preload(route_permute_kernel, n);
+  preload(gate_kernel, n);
+  preload(init_stats_kernel, n);
+  preload(rmsnorm_kernel, n);
+  preload(combine_kernel, n);
+  preload(set_ready_kernel, n);
+  return n;
+}
+}  // namespace ef

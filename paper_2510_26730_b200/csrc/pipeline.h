@@ -45,6 +45,7 @@ int expert_ffn_persistent(cudaStream_t st, const float* x, const int32_t* perm, 
                           int max_rows, int d, int ff, int dtype, void* act, float* y);
 int launch_set_ready(cudaStream_t st, uint32_t* ready, int slot, uint32_t seq);
 int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L);
+int preload_pipeline_kernels();
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
                          float bias, int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
                          int32_t* perm, int32_t* inv, const void* mask_src, int32_t* host_sel,
