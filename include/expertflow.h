@@ -249,6 +249,13 @@ int ef_expert_ffn_persistent_test(void* stream, const float* x, const int32_t* p
                                   const int32_t* act_slot, const int32_t* act_off,
                                   const int32_t* act_rows, int n_active, int max_rows, int d,
                                   int ff, int dtype, void* act, float* y, void* scratch);
+/* same, mode 0 = persistent register-streaming kernel, 1 = bulk-copy
+   (cp.async.bulk + mbarrier) streaming kernel (the engine default) */
+int ef_expert_ffn_ctrl_test(void* stream, const float* x, const int32_t* perm, int k,
+                            const void* slab, int64_t slot_stride_bytes, const int32_t* act_slot,
+                            const int32_t* act_off, const int32_t* act_rows, int n_active,
+                            int max_rows, int d, int ff, int dtype, void* act, float* y,
+                            void* scratch, int mode);
 /* (c) unpermute + weighted combine (rank order) + optional shared expert +
    residual + next rmsnorm:  h[t] += sum_r wts[t,r]*y[inv[t,r]] + g_t*ys[t];
    x = rmsnorm(h).  ys/shared_gate nullable. */

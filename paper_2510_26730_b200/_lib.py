@@ -126,6 +126,9 @@ _SIGS = {
     "ef_expert_ffn_persistent_test": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
                                                 C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
                                                 vp, vp]),
+    "ef_expert_ffn_ctrl_test": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
+                                          C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp,
+                                          C.c_int]),
     "ef_combine": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, f32]),
     "ef_gather_rows_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "ef_grouped_gemm_bf16": (C.c_int, [vp, vp, i64, C.c_int, vp, i64, i64, vp, C.c_int, C.c_int,

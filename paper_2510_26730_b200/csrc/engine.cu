@@ -32,6 +32,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -231,7 +232,7 @@ struct ef_engine {
   void enqueue_front(cudaStream_t stream, int l, int B);
   void enqueue_back(cudaStream_t stream, int l, int B, float* h);
   bool debug = false;  // EF_PIPE_DEBUG=1: no run-ahead, sync + check after each half-layer
-  bool persistent = true;  // EF_FFN=split selects the two-launch GEMV pair
+  int ffn_mode = 2;  // EF_FFN: split (GEMV pair, default) | stream (bulk-copy) | persistent
   int* counters_d = nullptr;
   void abort_pipeline(cudaStream_t stream, int from, int enq);
   void init_weights();
@@ -319,8 +320,8 @@ void ef_engine::enqueue_layer(cudaStream_t stream, int l, int B, float* h) {
 void ef_engine::enqueue_front(cudaStream_t stream, int l, int B) {
   const int M = cfg.M, k = cfg.top_k, d = cfg.d;
   const int R = std::min(Rmax, cfg.L - l);  // (a)+(b): layer l and pre-gate rows l+1..l+R-1
-  CKS(ef_router_logits(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R, B,
-                       d, M, logits_d));
+  CKS(router_logits_stamped(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
+                            B, d, M, logits_d, stats_d + 8 * l + 7));
   ++launches;
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
   if (sgate) {
@@ -331,7 +332,7 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B) {
   CKS(launch_route_publish(stream, logits_d, B, M, k, cfg.route_mode, cfg.routing_bias, sel_d,
                            wts_d, counts_d, offsets_d, perm_d, inv_d, &hctrl_dev[l].mask,
                            dev_of(out_sel(l)), dev_of(out_logits(l)),
-                           const_cast<uint32_t*>(&dev_of(out(l))->done)));
+                           const_cast<uint32_t*>(&dev_of(out(l))->done), stats_d + 8 * l + 6));
   ++launches;
   if (cfg.shared_ff) {  // always resident: runs while the host decides the layer
     const char* sw = shared_w + (int64_t)l * sstride;
@@ -346,9 +347,13 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   const int M = cfg.M, k = cfg.top_k, d = cfg.d;
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
   CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + 8 * l,
-                  persistent ? counters_d : nullptr));
+                  ffn_mode != 2 ? counters_d : nullptr));
   ++launches;
-  if (persistent) {
+  if (ffn_mode == 0) {
+    CKS(expert_ffn_stream(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + 8 * l,
+                          counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
+    launches += 1;
+  } else if (ffn_mode == 1) {
     CKS(expert_ffn_persistent(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready,
                               stats_d + 8 * l, counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
     launches += 1;
@@ -357,8 +362,8 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
                         std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
     launches += 2;
   }
-  CKS(ef_combine(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
-                 sgate ? sgl_d : nullptr, B, d, k, 1e-6f));
+  CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
+                      sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + 8 * l + 5));
   ++launches;
 }
 
@@ -548,11 +553,23 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
     step_ms += ms;
     CK(cudaMemcpy(stats_h.data(), stats_d, sizeof(unsigned long long) * 8 * L,
                   cudaMemcpyDeviceToHost));
+    static const bool dump = getenv("EF_STATS_DUMP") != nullptr;
     for (int j = 0; j < L; ++j) {
       const unsigned long long* sj = &stats_h[8 * j];
       stall_ms += sj[2] * 1e-6;
       if (sj[1] >= sj[0]) bubble_ms += (sj[1] - sj[0]) * 1e-6;
       if (sj[3] != ~0ull && sj[4] > sj[3]) ffn_ms += (sj[4] - sj[3]) * 1e-6;
+      if (dump) {  // per-layer device timeline (us)
+        auto us = [](unsigned long long a, unsigned long long b) {
+          return ((double)b - (double)a) * 1e-3;
+        };
+        fprintf(stderr,
+                "layer %2d router->route %6.1f route->gate %6.1f wait %6.1f go->ffn %6.1f "
+                "ffn %7.1f stall %7.1f ffn->combine_end %6.1f\n",
+                j, us(sj[7], sj[6]), us(sj[6], sj[0]), us(sj[0], sj[1]),
+                sj[3] != ~0ull ? us(sj[1], sj[3]) : 0.0, sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0,
+                sj[2] * 1e-3, us(sj[4], sj[5]));
+      }
     }
     cudaEventDestroy(t_begin);
     cudaEventDestroy(t_end);
@@ -651,7 +668,8 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     const char* dbg = getenv("EF_PIPE_DEBUG");
     e->debug = dbg && dbg[0] == '1';
     const char* ffn = getenv("EF_FFN");
-    e->persistent = !(ffn && std::string(ffn) == "split");
+    if (ffn && std::string(ffn) == "persistent") e->ffn_mode = 1;
+    if (ffn && std::string(ffn) == "stream") e->ffn_mode = 0;
     CK(cudaMalloc(&e->counters_d, sizeof(int) * (kMaxActive + 1)));
     *out = e.release();
   });

@@ -110,7 +110,7 @@ __global__ void rmsnorm_kernel(const float* __restrict__ h, float* __restrict__ 
 extern "C" int ef_rmsnorm(void* stream, const float* h, float* x, int B, int d, float eps) {
   EF_CHECK_ARG(B >= 0 && d > 0, "bad rmsnorm shape");
   if (B == 0) return EF_OK;
-  rmsnorm_kernel<<<B, 256, 0, S(stream)>>>(h, x, d, eps);
+  rmsnorm_kernel<<<B, 1024, 0, S(stream)>>>(h, x, d, eps);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -118,10 +118,18 @@ extern "C" int ef_rmsnorm(void* stream, const float* h, float* x, int B, int d, 
 // ============================================================ (a)(b) router GEMV
 // One warp per router row (r, m); all B tokens accumulate in registers while
 // the row streams through once.  x is tiny and stays in L1/L2.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <typename WT, int MAXB>
 __global__ void router_kernel(const float* __restrict__ x, const WT* __restrict__ w, int rows,
-                              int B, int d, int M, float* __restrict__ logits) {
+                              int B, int d, int M, float* __restrict__ logits,
+                              unsigned long long* stamp) {
   constexpr int V = WTraits<WT>::kPer16;
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = gtimer();
   const int t0 = blockIdx.y * MAXB;  // token chunk of this CTA row
   const int nb = min(MAXB, B - t0);
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -161,16 +169,30 @@ __global__ void router_kernel(const float* __restrict__ x, const WT* __restrict_
 
 template <typename WT>
 static void launch_router(cudaStream_t st, const float* x, const void* w, int R, int B, int d,
-                          int M, float* logits) {
+                          int M, float* logits, unsigned long long* stamp = nullptr) {
   const int rows = R * M, threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
   // one launch; grid.y walks token chunks of 8 (bounds the accumulators)
   if (B == 1)
-    router_kernel<WT, 1><<<dim3(blocks, 1), threads, 0, st>>>(x, (const WT*)w, rows, B, d, M, logits);
+    router_kernel<WT, 1><<<dim3(blocks, 1), threads, 0, st>>>(x, (const WT*)w, rows, B, d, M, logits,
+                                                              stamp);
   else
     router_kernel<WT, 8><<<dim3(blocks, (B + 7) / 8), threads, 0, st>>>(x, (const WT*)w, rows, B, d,
-                                                                          M, logits);
+                                                                          M, logits, stamp);
 }
+
+namespace ef {
+int router_logits_stamped(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
+                          int d, int M, float* logits, unsigned long long* stamp) {
+  if (B == 0) return EF_OK;
+  if (dtype == EF_BF16)
+    launch_router<__nv_bfloat16>(st, x, w, R, B, d, M, logits, stamp);
+  else
+    launch_router<float>(st, x, w, R, B, d, M, logits, stamp);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+}  // namespace ef
 
 extern "C" int ef_router_logits(void* stream, const float* x, const void* w, int dtype, int R,
                                 int B, int d, int M, float* logits) {
@@ -197,11 +219,12 @@ __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
     uint64_t mhi, int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts,
     int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv,
     const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
-    volatile uint32_t* host_done) {
+    volatile uint32_t* host_done, unsigned long long* stamp) {
   __shared__ int32_t warp_cnt[32][kMaxExperts];
   __shared__ int32_t base[kMaxExperts];
   __shared__ int32_t total[kMaxExperts];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (stamp && tid == 0) *stamp = gtimer();
   if (mask_src) {  // engine pipeline: the host publishes the residency mask before go(l-1)
     mlo = mask_src[0];
     mhi = mask_src[1];
@@ -295,15 +318,14 @@ __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
   }
   __syncthreads();
   for (int f = tid; f < N; f += blockDim.x) perm[inv[f]] = f;
-  if (host_done) {  // publish the selection and row-0 logits to mapped host memory
-    for (int f = tid; f < N; f += blockDim.x) host_sel[f] = sel[f];
-    for (int i = tid; i < B * M; i += blockDim.x) host_logits[i] = logits[i];
+  if (host_done && wid == 0) {
+    // publish the selection and row-0 logits to mapped host memory from one
+    // warp: a system-scope fence costs microseconds per warp that issues it
+    for (int f = lane; f < N; f += 32) host_sel[f] = sel[f];
+    for (int i = lane; i < B * M; i += 32) host_logits[i] = logits[i];
     __threadfence_system();
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence_system();
-      *host_done = 1u;
-    }
+    __syncwarp();
+    if (lane == 0) *host_done = 1u;
   }
 }
 
@@ -314,7 +336,8 @@ extern "C" int ef_route_permute(void* stream, const float* logits, int B, int M,
   EF_CHECK_ARG(mode == EF_ROUTE_MIXTRAL || mode == EF_ROUTE_SOFTMAX_TOPK, "bad routing mode");
   route_permute_kernel<<<1, kRouteThreads, 0, S(stream)>>>(logits, B, M, k, mode, bias, mlo, mhi,
                                                            sel, wts, counts, offsets, perm, inv,
-                                                           nullptr, nullptr, nullptr, nullptr);
+                                                           nullptr, nullptr, nullptr, nullptr,
+                                                           nullptr);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -390,7 +413,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-template <typename WT, int NT, int R, bool DUAL, typename XL>
+template <typename WT, int NT, int R, bool DUAL, typename XL, int U = 1>
 __global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs, int64_t offA,
                                                        int64_t offB, int rows, int cols, XL xl,
                                                        WT* act_out, float* y_out, int out_ld) {
@@ -449,29 +472,42 @@ __global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs
 #pragma unroll
     for (int t = 0; t < NT; ++t) xr[t] = xl.row(p0 + tc + (t < nt ? t : 0));
 
-    for (int c = lane * V; c < cols; c += 32 * V) {
-      uint4 wa[R], wb[R];
+    // U column chunks x R rows (x2 when DUAL) of 16-byte loads in flight per lane
+    for (int c0 = lane * V; c0 < cols; c0 += 32 * V * U) {
+      uint4 wa[U][R], wb[U][R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        int j = min(j0 + r, rows - 1);
-        wa[r] = ld_stream16(A + (int64_t)j * cols + c);
-        if (DUAL) wb[r] = ld_stream16(Bm + (int64_t)j * cols + c);
-      }
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        if (t < nt) {
-          float xv[V];
-          xl.load(xr[t], c, xv);
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 32 * V;
+        if (c < cols) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            float f[V];
-            WTraits<WT>::unpack(wa[r], f);
+            int j = min(j0 + r, rows - 1);
+            wa[u][r] = ld_stream16(A + (int64_t)j * cols + c);
+            if (DUAL) wb[u][r] = ld_stream16(Bm + (int64_t)j * cols + c);
+          }
+        }
+      }
 #pragma unroll
-            for (int q = 0; q < V; ++q) accA[r][t] = fmaf(f[q], xv[q], accA[r][t]);
-            if (DUAL) {
-              WTraits<WT>::unpack(wb[r], f);
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 32 * V;
+        if (c < cols) {
 #pragma unroll
-              for (int q = 0; q < V; ++q) accB[r][t] = fmaf(f[q], xv[q], accB[r][t]);
+          for (int t = 0; t < NT; ++t) {
+            if (t < nt) {
+              float xv[V];
+              xl.load(xr[t], c, xv);
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                float f[V];
+                WTraits<WT>::unpack(wa[u][r], f);
+#pragma unroll
+                for (int q = 0; q < V; ++q) accA[r][t] = fmaf(f[q], xv[q], accA[r][t]);
+                if (DUAL) {
+                  WTraits<WT>::unpack(wb[u][r], f);
+#pragma unroll
+                  for (int q = 0; q < V; ++q) accB[r][t] = fmaf(f[q], xv[q], accB[r][t]);
+                }
+              }
             }
           }
         }
@@ -509,11 +545,14 @@ static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& 
   dim3 gu((ff + WARPS * R - 1) / (WARPS * R), n_active);
   ffn_gemv_kernel<WT, NT, R, true, XGather<WT>>
       <<<gu, 128, 0, st>>>(al, cs, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
-  dim3 gd((d + WARPS * R - 1) / (WARPS * R), n_active);
+  // down projection: one W2 row per warp, 4 column chunks in flight per lane
+  // (d rows only: R=4 left most SMs idle on Mixtral's 4096 x 14336 W2)
+  constexpr int RD = 1, UD = 4;
+  dim3 gd((d + WARPS * RD - 1) / (WARPS * RD), n_active);
   XAct<WT> xa{act, ff};
   CtrlSrc cs2 = cs;
   cs2.wait_ready = false;
-  ffn_gemv_kernel<WT, NT, R, false, XAct<WT>>
+  ffn_gemv_kernel<WT, NT, RD, false, XAct<WT>, UD>
       <<<gd, 128, 0, st>>>(al, cs2, 2 * (int64_t)ff * d * es, 0, d, ff, xa, nullptr, y, d);
 }
 
@@ -794,6 +833,307 @@ __global__ void __launch_bounds__(kPWarps * 32) ffn_persist_kernel(PersistArgs p
   if (started && threadIdx.x == 0) atomicMax(&p.stats[4], globaltimer());
 }
 
+// ------------------------------------------------------------ bulk-streaming FFN
+// The engine's default decode FFN.  One CTA per SM; a producer warp streams
+// weight tiles HBM -> shared memory with cp.async.bulk (one bulk copy per
+// contiguous row block, mbarrier transaction counts), 8 consumer warps dot
+// them against the token vectors.  Bytes in flight per SM = STAGES x tile, no
+// longer tied to register pressure or occupancy.
+//   up tile   = rows [j0, j0+RU) of W1 and of W3 (two copies, one stage);
+//               warp w computes one row-dot, g/u exchanged through smem,
+//               act = T(silu(g) * u) stored to global
+//   down tile = rows [i0, i0+RD) of W2 (one copy); WPR warps per row split the
+//               columns, partials reduced through smem, y stored
+// Tiles are claimed dynamically by the producer (atomic counter): every up
+// tile precedes every down tile in claim order, so a down tile waiting for
+// its expert's up tiles only waits on tiles running CTAs already hold.  The
+// producer waits on an expert's ready flag before its first copy; consumers
+// keep computing the stages already loaded.
+constexpr int kSWarps = 8;                 // consumer warps
+constexpr int kSThreads = (kSWarps + 1) * 32;
+constexpr int kSStages = 3;
+constexpr int kSStageBytes = 64 * 1024;
+
+struct StreamArgs {
+  const DevCtrl* ctrl;
+  const char* slab;
+  int64_t stride;
+  const volatile uint32_t* ready;
+  unsigned long long* stats;
+  int* counters;  // [0] tile counter, [1 + a] up tiles done of active expert a
+  const float* x;
+  const int32_t* perm;
+  int k, d, ff;
+  int RU, RD, WPR;  // rows per up tile, rows per down tile, warps per down row
+  void* act;
+  float* y;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void sbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void sbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void sbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void sbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  const long long c0 = clock64();
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (!done && clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+  } while (!done);
+}
+
+template <typename WT, int NT>
+__global__ void __launch_bounds__(kSThreads, 1) ffn_stream_kernel(StreamArgs p) {
+  constexpr int V = WTraits<WT>::kPer16;
+  constexpr int64_t es = sizeof(WT);
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint8_t* stage_buf = sm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kSStages * kSStageBytes);
+  uint64_t* empty = full + kSStages;
+  int* stage_tile = reinterpret_cast<int*>(empty + kSStages);
+  float* red = reinterpret_cast<float*>(stage_tile + kSStages);  // [kSWarps][NT] partials
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_active = p.ctrl->n_active;
+  const int n_up = (p.ff + p.RU - 1) / p.RU;
+  const int n_dn = (p.d + p.RD - 1) / p.RD;
+  const int total_up = n_active * n_up;
+  const int total = total_up + n_active * n_dn;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSStages; ++s) {
+      sbar_init(&full[s], 1);
+      sbar_init(&empty[s], kSWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kSWarps) {  // ---------------- producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int last_ready_a = -1;
+      bool started = false;
+      for (;;) {
+        const int t = atomicAdd(&p.counters[0], 1);
+        sbar_wait(&empty[stage], phase ^ 1);
+        if (t >= total) {  // sentinel: tell the consumers to stop
+          stage_tile[stage] = -1;
+          sbar_arrive(&full[stage]);
+          break;
+        }
+        const bool up = t < total_up;
+        const int a = up ? t / n_up : (t - total_up) / n_dn;
+        const int4 e = p.ctrl->ent[a];
+        if (a != last_ready_a && p.ready[e.x] < (unsigned)e.w) {
+          unsigned long long t0 = globaltimer();
+          const long long c0 = clock64();
+          while (p.ready[e.x] < (unsigned)e.w) {
+            __nanosleep(256);
+            if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+          }
+          unsigned long long t1 = globaltimer();
+          if (t1 > t0) atomicMax(&p.stats[2], t1 - t0);
+        }
+        last_ready_a = a;
+        if (!started) {
+          atomicMin(&p.stats[3], globaltimer());
+          started = true;
+        }
+        const char* w = p.slab + (int64_t)e.x * p.stride;
+        uint8_t* dst = stage_buf + (int64_t)stage * kSStageBytes;
+        stage_tile[stage] = t;
+        if (up) {
+          const int j0 = (t % n_up) * p.RU, nr = min(p.RU, p.ff - j0);
+          const uint32_t bytes = (uint32_t)(nr * p.d * es);
+          sbar_expect_tx(&full[stage], 2 * bytes);
+          bulk_g2s(dst, w + (int64_t)j0 * p.d * es, bytes, &full[stage]);
+          bulk_g2s(dst + (int64_t)p.RU * p.d * es, w + ((int64_t)p.ff + j0) * p.d * es, bytes,
+                   &full[stage]);
+        } else {
+          const int i0 = ((t - total_up) % n_dn) * p.RD, nr = min(p.RD, p.d - i0);
+          const uint32_t bytes = (uint32_t)(nr * p.ff * es);
+          sbar_expect_tx(&full[stage], bytes);
+          bulk_g2s(dst, w + (2 * (int64_t)p.ff * p.d + (int64_t)i0 * p.ff) * es, bytes,
+                   &full[stage]);
+        }
+        if (++stage == kSStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  WT* act = reinterpret_cast<WT*>(p.act);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    sbar_wait(&full[stage], phase);
+    const int t = stage_tile[stage];
+    if (t < 0) break;
+    const bool up = t < total_up;
+    const int a = up ? t / n_up : (t - total_up) / n_dn;
+    const int4 e = p.ctrl->ent[a];
+    const int p0 = e.y, n_all = e.z;
+    const uint8_t* tile = stage_buf + (int64_t)stage * kSStageBytes;
+    if (up) {
+      const int j0 = (t % n_up) * p.RU, nr = min(p.RU, p.ff - j0);
+      const int rows_total = 2 * p.RU;  // W1 rows then W3 rows (RU each) in the stage
+      for (int tc = 0; tc < n_all; tc += NT) {
+        const int nt = min(NT, n_all - tc);
+        const float* xr[NT];
+#pragma unroll
+        for (int q = 0; q < NT; ++q)
+          xr[q] = p.x + (int64_t)(p.perm[p0 + tc + (q < nt ? q : 0)] / p.k) * p.d;
+        for (int rr = warp; rr < rows_total; rr += kSWarps) {
+          const int mat = rr / p.RU, r = rr % p.RU;
+          float acc[NT];
+#pragma unroll
+          for (int q = 0; q < NT; ++q) acc[q] = 0.f;
+          if (r < nr) {
+            const WT* row = reinterpret_cast<const WT*>(tile) + (int64_t)(mat * p.RU + r) * p.d;
+            for (int c = lane * V; c < p.d; c += 32 * V) {
+              float f[V];
+              WTraits<WT>::unpack(*reinterpret_cast<const uint4*>(row + c), f);
+#pragma unroll
+              for (int q = 0; q < NT; ++q) {
+                if (q < nt) {
+                  const float4* xp = reinterpret_cast<const float4*>(xr[q] + c);
+#pragma unroll
+                  for (int v4 = 0; v4 < V / 4; ++v4) {
+                    float4 xv = __ldg(xp + v4);
+                    acc[q] = fmaf(f[4 * v4 + 0], WTraits<WT>::cast(xv.x), acc[q]);
+                    acc[q] = fmaf(f[4 * v4 + 1], WTraits<WT>::cast(xv.y), acc[q]);
+                    acc[q] = fmaf(f[4 * v4 + 2], WTraits<WT>::cast(xv.z), acc[q]);
+                    acc[q] = fmaf(f[4 * v4 + 3], WTraits<WT>::cast(xv.w), acc[q]);
+                  }
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < NT; ++q) {
+            float v = warp_sum(acc[q]);
+            if (lane == 0) red[rr * NT + q] = v;  // red holds 2*RU*NT partials
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));  // consumers only
+        for (int i = threadIdx.x; i < nr * nt; i += kSWarps * 32) {
+          const int r = i / nt, q = i % nt;
+          const float g = red[r * NT + q], u = red[(p.RU + r) * NT + q];
+          WTraits<WT>::store(act + (int64_t)(p0 + tc + q) * p.ff + j0 + r, g / (1.0f + expf(-g)) * u);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
+      }
+      // this stage is consumed; publish the act rows, then count the tile
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
+      if (lane == 0) sbar_arrive(&empty[stage]);
+      if (threadIdx.x == 0) atomicAdd(&p.counters[1 + a], 1);
+    } else {
+      const int i0 = ((t - total_up) % n_dn) * p.RD, nr = min(p.RD, p.d - i0);
+      if (threadIdx.x == 0) {  // wait for this expert's up tiles (act complete)
+        volatile int* done = p.counters + 1 + a;
+        const long long c0 = clock64();
+        while (*done < n_up) {
+          __nanosleep(64);
+          if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+        }
+        __threadfence();
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
+      const int r = warp / p.WPR, part = warp % p.WPR;
+      const int span = ((p.ff + p.WPR - 1) / p.WPR + 32 * V - 1) / (32 * V) * (32 * V);
+      const int c_begin = part * span, c_end = min(p.ff, c_begin + span);
+      for (int tc = 0; tc < n_all; tc += NT) {
+        const int nt = min(NT, n_all - tc);
+        float acc[NT];
+#pragma unroll
+        for (int q = 0; q < NT; ++q) acc[q] = 0.f;
+        if (r < nr) {
+          const WT* row = reinterpret_cast<const WT*>(tile) + (int64_t)r * p.ff;
+          for (int c = c_begin + lane * V; c < c_end; c += 32 * V) {
+            float f[V];
+            WTraits<WT>::unpack(*reinterpret_cast<const uint4*>(row + c), f);
+#pragma unroll
+            for (int q = 0; q < NT; ++q) {
+              if (q < nt) {
+                uint4 av = __ldcg(reinterpret_cast<const uint4*>(act + (int64_t)(p0 + tc + q) * p.ff + c));
+                float fx[V];
+                WTraits<WT>::unpack(av, fx);
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[q] = fmaf(f[i], fx[i], acc[q]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          float v = warp_sum(acc[q]);
+          if (lane == 0) red[warp * NT + q] = v;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
+        for (int i = threadIdx.x; i < nr * nt; i += kSWarps * 32) {
+          const int rr = i / nt, q = i % nt;
+          float v = 0.f;
+          for (int w = 0; w < p.WPR; ++w) v += red[(rr * p.WPR + w) * NT + q];
+          p.y[(int64_t)(p0 + tc + q) * p.d + i0 + rr] = v;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
+      }
+      if (lane == 0) sbar_arrive(&empty[stage]);
+    }
+    if (++stage == kSStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  if (threadIdx.x == 0) atomicMax(&p.stats[4], globaltimer());
+}
+
+template <typename WT, int NT>
+static int launch_stream_nt(cudaStream_t st, const StreamArgs& sa) {
+  constexpr int smem = kSStages * kSStageBytes + 2 * kSStages * 8 + kSStages * 4 + 16 * NT * 4 + 64;
+  static int grid = 0;
+  if (!grid) {
+    if (cudaFuncSetAttribute(ffn_stream_kernel<WT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess)
+      return EF_ECUDA;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev);
+  }
+  ffn_stream_kernel<WT, NT><<<grid, kSThreads, smem, st>>>(sa);
+  return EF_OK;
+}
+
 template <typename WT, int NT>
 static int launch_persist_nt(cudaStream_t st, const PersistArgs& pa) {
   static int grid = 0;
@@ -810,30 +1150,46 @@ static int launch_persist_nt(cudaStream_t st, const PersistArgs& pa) {
 }
 
 // ------------------------------------------------------------ pipeline glue
+__device__ __forceinline__ uint2 ld_acquire_sys_v2(const volatile void* p) {
+  uint2 v;
+  asm volatile("ld.acquire.sys.global.v2.u32 {%0,%1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int4 ld_volatile_v4(const volatile void* p) {
+  int4 v;
+  asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// One warp: spin on the host's go flag (8-byte acquire load returns go and
+// n_active together), copy the decision with one 16-byte PCIe read per entry.
 __global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats,
                             int* counters) {
-  __shared__ int n_sh;
+  const int lane = threadIdx.x;
   if (counters)  // fresh tile / completion counters for this layer's persistent FFN
-    for (int i = threadIdx.x; i <= kMaxActive; i += blockDim.x) counters[i] = 0;
-  if (threadIdx.x == 0) {
+    for (int i = lane; i <= kMaxActive; i += 32) counters[i] = 0;
+  uint2 gn = make_uint2(0, 0);
+  if (lane == 0) {
     stats[0] = globaltimer();
     const long long c0 = clock64();
-    while (hc->go == 0u) {
-      __nanosleep(128);
+    for (;;) {
+      gn = ld_acquire_sys_v2(&hc->go);
+      if (gn.x != 0u) break;
+      __nanosleep(64);
       if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");  // host died: fail loudly
     }
     stats[1] = globaltimer();
-    __threadfence_system();
-    n_sh = hc->n_active;
   }
-  __syncthreads();
-  int n = n_sh;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    volatile int* src = reinterpret_cast<volatile int*>(&hc->ent[i]);
-    dc->ent[i] = make_int4(src[0], src[1], src[2], src[3]);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  const int n = __shfl_sync(0xffffffffu, (int)gn.y, 0);
+  for (int i = lane; i < n; i += 32) dc->ent[i] = ld_volatile_v4(&hc->ent[i]);
+  __syncwarp();
+  if (lane == 0) {
     dc->n_active = n;
     hc->go = 0u;  // consumed; the host sets it again for the next token's layer
   }
@@ -864,12 +1220,33 @@ int expert_ffn_persistent(cudaStream_t st, const float* x, const int32_t* perm, 
 // Test entry: run the persistent FFN on an explicit active list (slots are
 // treated as resident).  scratch: device buffer >= sizeof(DevCtrl) +
 // 4*(kMaxActive+1) + 8*8 + 4*max_slot+4 bytes.
+int expert_ffn_stream(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
+                      int64_t stride, const void* dctrl, const uint32_t* ready,
+                      unsigned long long* stats, int* counters, int max_rows, int d, int ff,
+                      int dtype, void* act, float* y);
+
+extern "C" int ef_expert_ffn_ctrl_test(void* stream, const float* x, const int32_t* perm, int k,
+                                       const void* slab, int64_t stride, const int32_t* act_slot,
+                                       const int32_t* act_off, const int32_t* act_rows,
+                                       int n_active, int max_rows, int d, int ff, int dtype,
+                                       void* act, float* y, void* scratch, int mode);
+
 extern "C" int ef_expert_ffn_persistent_test(void* stream, const float* x, const int32_t* perm,
                                              int k, const void* slab, int64_t stride,
                                              const int32_t* act_slot, const int32_t* act_off,
                                              const int32_t* act_rows, int n_active, int max_rows,
                                              int d, int ff, int dtype, void* act, float* y,
                                              void* scratch) {
+  return ef_expert_ffn_ctrl_test(stream, x, perm, k, slab, stride, act_slot, act_off, act_rows,
+                                 n_active, max_rows, d, ff, dtype, act, y, scratch, 0);
+}
+
+// mode 0: persistent register-streaming FFN, 1: bulk-copy streaming FFN
+extern "C" int ef_expert_ffn_ctrl_test(void* stream, const float* x, const int32_t* perm, int k,
+                                       const void* slab, int64_t stride, const int32_t* act_slot,
+                                       const int32_t* act_off, const int32_t* act_rows,
+                                       int n_active, int max_rows, int d, int ff, int dtype,
+                                       void* act, float* y, void* scratch, int mode) {
   EF_CHECK_ARG(n_active >= 0 && n_active <= kMaxActive, "too many active experts");
   DevCtrl h{};
   h.n_active = n_active;
@@ -890,13 +1267,61 @@ extern "C" int ef_expert_ffn_persistent_test(void* stream, const float* x, const
   EF_CUDA_RET(cudaMemsetAsync(stats, 0, 64, st));
   EF_CUDA_RET(cudaMemsetAsync(ready, 0, 4 * (max_slot + 1), st));
   EF_CUDA_RET(cudaStreamSynchronize(st));  // h is on the host stack
+  if (mode == 1)
+    return expert_ffn_stream(st, x, perm, k, reinterpret_cast<const char*>(slab), stride, dc,
+                             ready, stats, counters, max_rows, d, ff, dtype, act, y);
   return expert_ffn_persistent(st, x, perm, k, reinterpret_cast<const char*>(slab), stride, dc,
                                ready, stats, counters, max_rows, d, ff, dtype, act, y);
 }
 
+// Tile geometry of the streaming FFN: up tile = RU rows of W1 and W3,
+// down tile = RD rows of W2, both within one stage; WPR warps per down row.
+static bool stream_geometry(int d, int ff, int64_t es, int* RU, int* RD, int* WPR) {
+  int ru = (int)std::min<int64_t>(kSWarps, kSStageBytes / (2 * (int64_t)d * es));
+  int rd = (int)std::min<int64_t>(16, kSStageBytes / ((int64_t)ff * es));
+  if (ru < 1 || rd < 1) return false;
+  // WPR must divide kSWarps and cover rd rows with kSWarps warps
+  int wpr = kSWarps / std::min(rd, kSWarps);
+  if (rd > kSWarps) {
+    rd = kSWarps;
+    wpr = 1;
+  }
+  *RU = ru;
+  *RD = rd;
+  *WPR = wpr;
+  return 2 * ru * (int)1 <= 16 && rd * wpr <= kSWarps;
+}
+
+int expert_ffn_stream(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
+                      int64_t stride, const void* dctrl, const uint32_t* ready,
+                      unsigned long long* stats, int* counters, int max_rows, int d, int ff,
+                      int dtype, void* act, float* y) {
+  const int64_t es = dtype == EF_BF16 ? 2 : 4;
+  StreamArgs sa{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, counters, x,
+                perm, k, d, ff, 0, 0, 0, act, y};
+  EF_CHECK_ARG(stream_geometry(d, ff, es, &sa.RU, &sa.RD, &sa.WPR),
+               "expert rows do not fit the streaming FFN stage");
+  EF_CHECK_ARG(d % 256 == 0 && ff % 8 == 0, "d must be a multiple of 256 and ff of 8");
+  int rc;
+  if (dtype == EF_BF16) {
+    if (max_rows <= 1) rc = launch_stream_nt<__nv_bfloat16, 1>(st, sa);
+    else if (max_rows <= 2) rc = launch_stream_nt<__nv_bfloat16, 2>(st, sa);
+    else if (max_rows <= 4) rc = launch_stream_nt<__nv_bfloat16, 4>(st, sa);
+    else rc = launch_stream_nt<__nv_bfloat16, 8>(st, sa);
+  } else {
+    if (max_rows <= 1) rc = launch_stream_nt<float, 1>(st, sa);
+    else if (max_rows <= 2) rc = launch_stream_nt<float, 2>(st, sa);
+    else if (max_rows <= 4) rc = launch_stream_nt<float, 4>(st, sa);
+    else rc = launch_stream_nt<float, 8>(st, sa);
+  }
+  if (rc != EF_OK) return rc;
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
 int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats,
                 int* counters) {
-  gate_kernel<<<1, 64, 0, st>>>(reinterpret_cast<HostCtrl*>(host_ctrl_dev),
+  gate_kernel<<<1, 32, 0, st>>>(reinterpret_cast<HostCtrl*>(host_ctrl_dev),
                                 reinterpret_cast<DevCtrl*>(dctrl), stats, counters);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
@@ -925,10 +1350,11 @@ int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L) {
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
                          float bias, int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
                          int32_t* perm, int32_t* inv, const void* mask_src, int32_t* host_sel,
-                         float* host_logits, uint32_t* host_done) {
+                         float* host_logits, uint32_t* host_done, unsigned long long* stamp) {
   route_permute_kernel<<<1, kRouteThreads, 0, st>>>(
       logits, B, M, k, mode, bias, 0ull, 0ull, sel, wts, counts, offsets, perm, inv,
-      reinterpret_cast<const volatile uint64_t*>(mask_src), host_sel, host_logits, host_done);
+      reinterpret_cast<const volatile uint64_t*>(mask_src), host_sel, host_logits, host_done,
+      stamp);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -974,7 +1400,8 @@ extern "C" int ef_gather_rows_bf16(void* stream, const float* x, const int32_t* 
 __global__ void combine_kernel(float* __restrict__ h, float* __restrict__ x,
                                const float* __restrict__ y, const int32_t* __restrict__ inv,
                                const float* __restrict__ wts, const float* __restrict__ ys,
-                               const float* __restrict__ gate_logit, int d, int k, float eps) {
+                               const float* __restrict__ gate_logit, int d, int k, float eps,
+                               unsigned long long* stamp) {
   __shared__ float red[32];
   const int t = blockIdx.x;
   float g = 1.f;
@@ -993,14 +1420,26 @@ __global__ void combine_kernel(float* __restrict__ h, float* __restrict__ x,
   ss = block_sum(ss, red);
   float invn = 1.0f / sqrtf(ss / (float)d + eps);
   for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)t * d + i] = hr[i] * invn;
+  if (stamp && threadIdx.x == 0) atomicMax(stamp, gtimer());
 }
+
+namespace ef {
+int combine_stamped(cudaStream_t st, float* h, float* x, const float* y, const int32_t* inv,
+                    const float* wts, const float* ys, const float* gate_logit, int B, int d, int k,
+                    float eps, unsigned long long* stamp) {
+  if (B == 0) return EF_OK;
+  combine_kernel<<<B, 1024, 0, st>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps, stamp);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+}  // namespace ef
 
 extern "C" int ef_combine(void* stream, float* h, float* x, const float* y, const int32_t* inv,
                           const float* wts, const float* ys, const float* gate_logit, int B,
                           int d, int k, float eps) {
   EF_CHECK_ARG(B >= 0 && d > 0 && k >= 1, "bad combine shape");
   if (B == 0) return EF_OK;
-  combine_kernel<<<B, 256, 0, S(stream)>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps);
+  combine_kernel<<<B, 1024, 0, S(stream)>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps, nullptr);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -1024,14 +1463,18 @@ static void preload_dtype(int& n) {
   preload(ffn_persist_kernel<WT, 2>, n);
   preload(ffn_persist_kernel<WT, 4>, n);
   preload(ffn_persist_kernel<WT, 8>, n);
+  preload(ffn_stream_kernel<WT, 1>, n);
+  preload(ffn_stream_kernel<WT, 2>, n);
+  preload(ffn_stream_kernel<WT, 4>, n);
+  preload(ffn_stream_kernel<WT, 8>, n);
   preload(ffn_gemv_kernel<WT, 1, 4, true, XGather<WT>>, n);
   preload(ffn_gemv_kernel<WT, 2, 4, true, XGather<WT>>, n);
   preload(ffn_gemv_kernel<WT, 4, 4, true, XGather<WT>>, n);
   preload(ffn_gemv_kernel<WT, 8, 4, true, XGather<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 1, 4, false, XAct<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 2, 4, false, XAct<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 4, 4, false, XAct<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 8, 4, false, XAct<WT>>, n);
+  preload(ffn_gemv_kernel<WT, 1, 1, false, XAct<WT>, 4>, n);
+  preload(ffn_gemv_kernel<WT, 2, 1, false, XAct<WT>, 4>, n);
+  preload(ffn_gemv_kernel<WT, 4, 1, false, XAct<WT>, 4>, n);
+  preload(ffn_gemv_kernel<WT, 8, 1, false, XAct<WT>, 4>, n);
 }
 
 int preload_pipeline_kernels() {

@@ -46,8 +46,17 @@ int expert_ffn_persistent(cudaStream_t st, const float* x, const int32_t* perm, 
 int launch_set_ready(cudaStream_t st, uint32_t* ready, int slot, uint32_t seq);
 int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L);
 int preload_pipeline_kernels();
+int expert_ffn_stream(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
+                      int64_t stride, const void* dctrl, const uint32_t* ready,
+                      unsigned long long* stats, int* counters, int max_rows, int d, int ff,
+                      int dtype, void* act, float* y);
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
                          float bias, int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
                          int32_t* perm, int32_t* inv, const void* mask_src, int32_t* host_sel,
-                         float* host_logits, uint32_t* host_done);
+                         float* host_logits, uint32_t* host_done, unsigned long long* stamp);
+int router_logits_stamped(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
+                          int d, int M, float* logits, unsigned long long* stamp);
+int combine_stamped(cudaStream_t st, float* h, float* x, const float* y, const int32_t* inv,
+                    const float* wts, const float* ys, const float* gate_logit, int B, int d, int k,
+                    float eps, unsigned long long* stamp);
 }  // namespace ef

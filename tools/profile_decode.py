@@ -21,12 +21,16 @@ ap.add_argument("--layers", type=int, default=2)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--bias", type=float, default=1e4)
+ap.add_argument("--policy", default="static")
+ap.add_argument("--budget-frac", type=float, default=1.0)
 args = ap.parse_args()
 base = PRESETS[args.config]
 cfg = MoEConfig(base.name + f"-{args.layers}l", args.layers, base.num_experts, base.top_k,
                 base.d_model, base.d_ff, base.dtype, base.route_mode, base.shared_ff,
                 base.shared_gate)
-eng = MoEEngine(cfg, budget_experts=cfg.total_experts, policy=ef.PolicyConfig("s", "static"),
+pol = ef.PolicyConfig("p", args.policy, predictor="pregate" if args.policy != "static" else "none")
+eng = MoEEngine(cfg, budget_experts=max(cfg.top_k, int(args.budget_frac * cfg.total_experts)),
+                policy=pol,
                 link_bw=55_000_000_000, layer_time_s=1e-4, max_batch=args.batch,
                 routing_bias=args.bias, timing=True)
 h = synthetic_hidden(cfg, 0, 0, args.batch, torch.device("cuda", 0))
