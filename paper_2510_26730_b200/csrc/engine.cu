@@ -228,15 +228,31 @@ struct ef_engine {
       if (st->resident(layer, e)) m[e >> 6] |= 1ull << (e & 63);
   }
 
-  void enqueue_layer(cudaStream_t stream, int l, int B, float* h);
-  void enqueue_front(cudaStream_t stream, int l, int B);
+  void enqueue_layer(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask);
+  void enqueue_front(cudaStream_t stream, int l, int B, int R, const uint64_t* mask);
+  std::vector<int> layer_R;  // router matrices scored at each layer this step
   void enqueue_back(cudaStream_t stream, int l, int B, float* h);
   bool debug = false;  // EF_PIPE_DEBUG=1: no run-ahead, sync + check after each half-layer
   int ffn_mode = 2;  // EF_FFN: split (GEMV pair, default) | stream (bulk-copy) | persistent
   int* counters_d = nullptr;
+  // EF_FUSE bit mask: 1 router+route in one kernel, 2 gate folded into the
+  // up kernel, 4 combine folded into the down kernel's last CTA
+  int fuse = 11;
+  int fuse_combine_max_b = 8;  // last-CTA combine only pays for small batches
+  int* fuse_d = nullptr;       // [0] route counter [1] combine counter [2] gate flag
+  unsigned gate_seq = 0;
+  float* cur_h = nullptr;  // the step's hidden state (combine-in-router writes it)
+  // EF_FUSE bit 8: combine(l-1) folded into router_route(l), small batches
+  bool comb_in_router(int l, int B) const {
+    return (fuse & 8) && (fuse & 1) && l > 0 && l < cfg.L && cfg.M <= 128 && B <= 8 &&
+           (int64_t)B * cfg.d * 4 <= 128 * 1024;
+  }
   void abort_pipeline(cudaStream_t stream, int from, int enq);
   void init_weights();
   void step(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
+  void step_on(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
+  cudaStream_t compute_stream = nullptr;
+  cudaEvent_t join_in = nullptr, join_out = nullptr;
   ~ef_engine();
 };
 
@@ -300,7 +316,7 @@ ef_engine::~ef_engine() {
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
-                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d})
+                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d})
     if (p) cudaFree(p);
   for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring})
     if (p) cudaFreeHost(p);
@@ -308,32 +324,58 @@ ef_engine::~ef_engine() {
     if (p) cudaFreeHost(p);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (side_stream) cudaStreamDestroy(side_stream);
+  if (compute_stream) cudaStreamDestroy(compute_stream);
+  if (join_in) cudaEventDestroy(join_in);
+  if (join_out) cudaEventDestroy(join_out);
 }
 
 // Enqueue every kernel of layer l: router (+ pre-gate rows), route (publishes
 // to the host), shared expert, gate, routed FFN, combine + next rmsnorm.
-void ef_engine::enqueue_layer(cudaStream_t stream, int l, int B, float* h) {
-  enqueue_front(stream, l, B);
+void ef_engine::enqueue_layer(cudaStream_t stream, int l, int B, float* h, int R,
+                              const uint64_t* mask) {
+  enqueue_front(stream, l, B, R, mask);
   enqueue_back(stream, l, B, h);
 }
 
-void ef_engine::enqueue_front(cudaStream_t stream, int l, int B) {
+// (a)+(b): router over layer l and pre-gate rows l+1..l+R-1, then route.
+// R and the bias mask are final once layer l-1 has been decided.
+void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const uint64_t* mask) {
   const int M = cfg.M, k = cfg.top_k, d = cfg.d;
-  const int R = std::min(Rmax, cfg.L - l);  // (a)+(b): layer l and pre-gate rows l+1..l+R-1
-  CKS(router_logits_stamped(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
-                            B, d, M, logits_d, stats_d + 8 * l + 7));
-  ++launches;
+  R = std::max(1, std::min(R, cfg.L - l));
+  layer_R[l] = R;
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
-  if (sgate) {
-    CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
-                         1, sgl_d));
+  if ((fuse & 1) && M <= 128) {
+    CombineIn ci{cur_h, y_d, cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, 1e-6f,
+                 l > 0 ? stats_d + kStats * (l - 1) + 5 : nullptr};
+    CKS(router_route_fused(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
+                           B, d, M, logits_d, stats_d + kStats * l + 7, k, cfg.route_mode,
+                           cfg.routing_bias, mask[0], mask[1], sel_d, wts_d, counts_d, offsets_d,
+                           perm_d, inv_d, dev_of(out_sel(l)), dev_of(out_logits(l)),
+                           const_cast<uint32_t*>(&dev_of(out(l))->done),
+                           stats_d + kStats * l + 6, fuse_d,
+                           comb_in_router(l, B) ? &ci : nullptr));
+    ++launches;
+    if (sgate) {
+      CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
+                           1, sgl_d));
+      ++launches;
+    }
+  } else {
+    CKS(router_logits_stamped(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype,
+                              R, B, d, M, logits_d, stats_d + kStats * l + 7));
+    ++launches;
+    if (sgate) {
+      CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
+                           1, sgl_d));
+      ++launches;
+    }
+    CKS(launch_route_publish(stream, logits_d, B, M, k, cfg.route_mode, cfg.routing_bias, mask[0],
+                             mask[1], sel_d, wts_d, counts_d, offsets_d, perm_d, inv_d, nullptr,
+                             dev_of(out_sel(l)), dev_of(out_logits(l)),
+                             const_cast<uint32_t*>(&dev_of(out(l))->done),
+                             stats_d + kStats * l + 6));
     ++launches;
   }
-  CKS(launch_route_publish(stream, logits_d, B, M, k, cfg.route_mode, cfg.routing_bias, sel_d,
-                           wts_d, counts_d, offsets_d, perm_d, inv_d, &hctrl_dev[l].mask,
-                           dev_of(out_sel(l)), dev_of(out_logits(l)),
-                           const_cast<uint32_t*>(&dev_of(out(l))->done), stats_d + 8 * l + 6));
-  ++launches;
   if (cfg.shared_ff) {  // always resident: runs while the host decides the layer
     const char* sw = shared_w + (int64_t)l * sstride;
     int32_t z = 0, nb = B;
@@ -346,24 +388,42 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B) {
 void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   const int M = cfg.M, k = cfg.top_k, d = cfg.d;
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
-  CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + 8 * l,
+  const bool comb_next = comb_in_router(l + 1, B);
+  if ((fuse & 2) && ffn_mode == 2) {
+    const bool comb = !comb_next && (fuse & 4) && B <= fuse_combine_max_b;
+    ++gate_seq;
+    CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
+                         reinterpret_cast<volatile unsigned*>(fuse_d + 2), gate_seq, ready,
+                         stats_d + kStats * l, std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d,
+                         y_d, comb ? fuse_d + 1 : nullptr, h, x_d, inv_d, wts_d,
+                         cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, B, 1e-6f));
+    launches += 2;
+    if (!comb && !comb_next) {
+      CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
+                          sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
+      ++launches;
+    }
+    return;
+  }
+  CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + kStats * l,
                   ffn_mode != 2 ? counters_d : nullptr));
   ++launches;
   if (ffn_mode == 0) {
-    CKS(expert_ffn_stream(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + 8 * l,
+    CKS(expert_ffn_stream(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
                           counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
     launches += 1;
   } else if (ffn_mode == 1) {
     CKS(expert_ffn_persistent(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready,
-                              stats_d + 8 * l, counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
+                              stats_d + kStats * l, counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
     launches += 1;
   } else {
-    CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + 8 * l,
+    CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
                         std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
     launches += 2;
   }
+  if (comb_next) return;
   CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
-                      sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + 8 * l + 5));
+                      sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
   ++launches;
 }
 
@@ -387,7 +447,24 @@ void ef_engine::abort_pipeline(cudaStream_t stream, int from, int enq) {
   deferred_free.clear();
 }
 
-void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens_in) {
+void ef_engine::step(cudaStream_t caller, float* h, int B, const std::vector<int64_t>& tokens_in) {
+  // Run the token on the engine's own non-blocking, high-priority stream
+  // (the caller's may be the legacy default stream, whose implicit
+  // cross-stream ordering costs microseconds per launch); join both ways.
+  cudaStream_t stream = compute_stream ? compute_stream : caller;
+  if (stream != caller) {
+    CK(cudaEventRecord(join_in, caller));
+    CK(cudaStreamWaitEvent(stream, join_in, 0));
+  }
+  step_on(stream, h, B, tokens_in);
+  if (stream != caller) {
+    CK(cudaEventRecord(join_out, stream));
+    CK(cudaStreamWaitEvent(caller, join_out, 0));
+  }
+}
+
+void ef_engine::step_on(cudaStream_t stream, float* h, int B,
+                        const std::vector<int64_t>& tokens_in) {
   using clk = std::chrono::steady_clock;
   const int L = cfg.L, M = cfg.M, k = cfg.top_k;
   if (B < 1 || B > cfg.max_batch) throw ValueError("batch size outside [1, max_batch]");
@@ -399,13 +476,11 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
     CK(cudaEventCreate(&t_end));
     CK(cudaEventRecord(t_begin, stream));
   }
+  cur_h = h;
   CKS(launch_init_stats(stream, stats_d, L));
   CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
   launches += 2;
   residency_mask(0, cur_mask);
-  hctrl[0].mask[0] = cur_mask[0];
-  hctrl[0].mask[1] = cur_mask[1];
-  std::atomic_thread_fence(std::memory_order_seq_cst);
 
   std::vector<int64_t> gsizes(B, 1);
   double host_acc = 0;
@@ -419,19 +494,18 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
                     std::to_string(layer) + ": " + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
   };
   try {
+    // layer 0 scores every pre-gate row a boundary could ask for (its horizon
+    // is only known after the token's layer-0 routing); later layers score
+    // exactly the planned horizon
     if (debug) {
       dbg_sync("init/rmsnorm", 0);
-      enqueue_front(stream, 0, B);
+      enqueue_front(stream, 0, B, Rmax, cur_mask);
       dbg_sync("router/route/shared", 0);
     } else {
-      enqueue_layer(stream, 0, B, h);
+      enqueue_layer(stream, 0, B, h, Rmax, cur_mask);
     }
     enq = 1;
     for (l = 0; l < L; ++l) {
-      if (!debug && enq < L) {  // keep the GPU one layer ahead of the host
-        enqueue_layer(stream, enq, B, h);
-        ++enq;
-      }
       // ---- wait for route(l) to publish its selection
       HostOut* ho = out(l);
       auto w0 = clk::now();
@@ -447,7 +521,7 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
       auto h0 = clk::now();
       const int32_t* sel = out_sel(l);
       const float* lg0 = out_logits(l);
-      const int R = std::min(Rmax, L - l);
+      const int R = layer_R[l];
       // ---- scheduler view of this layer's routing (workload.py:161-179 contract)
       LayerRouting r;
       r.gate.resize(M);
@@ -511,25 +585,30 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
       hc.n_active = n;
       ffn_bytes += (int64_t)n * stride;
       ffn_launches += 2;
-      if (l + 1 < L) {
-        residency_mask(l + 1, cur_mask);
-        hctrl[l + 1].mask[0] = cur_mask[0];
-        hctrl[l + 1].mask[1] = cur_mask[1];
-      }
       std::atomic_thread_fence(std::memory_order_seq_cst);
       _mm_sfence();
       hc.go = 1u;
       host_acc += std::chrono::duration<double, std::milli>(clk::now() - h0).count();
-      if (debug) {
+      // enqueue layer l+1 while FFN(l) runs: its horizon and bias mask are final now
+      if (l + 1 < L) {
+        residency_mask(l + 1, cur_mask);
+        const int R1 = 1 + st->planned_horizon(l + 1);
+        if (debug) {
+          dbg_sync("copies", l);
+          enqueue_back(stream, l, B, h);
+          dbg_sync("gate/ffn/combine", l);
+          enqueue_front(stream, l + 1, B, R1, cur_mask);
+          dbg_sync("router/route/shared", l + 1);
+        } else {
+          enqueue_layer(stream, l + 1, B, h, R1, cur_mask);
+        }
+        enq = l + 2;
+      } else if (debug) {
         dbg_sync("copies", l);
         enqueue_back(stream, l, B, h);
         dbg_sync("gate/ffn/combine", l);
-        if (l + 1 < L) {
-          enqueue_front(stream, l + 1, B);
-          dbg_sync("router/route/shared", l + 1);
-          enq = l + 2;
-        }
       }
+
       // slots read by FFN(l) become reusable at the decision of layer l+1
       for (int s : pinned_list) pinned[s] = 0;
       pinned_list.clear();
@@ -551,11 +630,11 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, t_begin, t_end));
     step_ms += ms;
-    CK(cudaMemcpy(stats_h.data(), stats_d, sizeof(unsigned long long) * 8 * L,
+    CK(cudaMemcpy(stats_h.data(), stats_d, sizeof(unsigned long long) * kStats * L,
                   cudaMemcpyDeviceToHost));
     static const bool dump = getenv("EF_STATS_DUMP") != nullptr;
     for (int j = 0; j < L; ++j) {
-      const unsigned long long* sj = &stats_h[8 * j];
+      const unsigned long long* sj = &stats_h[kStats * j];
       stall_ms += sj[2] * 1e-6;
       if (sj[1] >= sj[0]) bubble_ms += (sj[1] - sj[0]) * 1e-6;
       if (sj[3] != ~0ull && sj[4] > sj[3]) ffn_ms += (sj[4] - sj[3]) * 1e-6;
@@ -564,11 +643,13 @@ void ef_engine::step(cudaStream_t stream, float* h, int B, const std::vector<int
           return ((double)b - (double)a) * 1e-3;
         };
         fprintf(stderr,
-                "layer %2d router->route %6.1f route->gate %6.1f wait %6.1f go->ffn %6.1f "
-                "ffn %7.1f stall %7.1f ffn->combine_end %6.1f\n",
-                j, us(sj[7], sj[6]), us(sj[6], sj[0]), us(sj[0], sj[1]),
-                sj[3] != ~0ull ? us(sj[1], sj[3]) : 0.0, sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0,
-                sj[2] * 1e-3, us(sj[4], sj[5]));
+                "layer %2d router %5.1f route %5.1f pub->gate %5.1f wait %6.1f gate %5.1f "
+                "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f\n",
+                j, us(sj[7], sj[6]), us(sj[6], sj[9]), us(sj[9], sj[0]), us(sj[0], sj[1]),
+                us(sj[1], sj[8]), sj[10] != ~0ull ? us(sj[8], sj[10]) : 0.0,
+                sj[3] != ~0ull && sj[10] != ~0ull ? us(sj[10], sj[3]) : 0.0,
+                sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0, sj[2] * 1e-3, us(sj[4], sj[5]),
+                j + 1 < L ? us(sj[7], stats_h[kStats * (j + 1) + 7]) : 0.0);
       }
     }
     cudaEventDestroy(t_begin);
@@ -638,8 +719,8 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     CK(cudaMalloc(&e->dctrl, sizeof(DevCtrl) * L));
     CK(cudaMalloc(&e->ready, sizeof(uint32_t) * e->P));
     CK(cudaMemset(e->ready, 0, sizeof(uint32_t) * e->P));
-    CK(cudaMalloc(&e->stats_d, sizeof(unsigned long long) * 8 * L));
-    e->stats_h.assign(8 * L, 0);
+    CK(cudaMalloc(&e->stats_d, sizeof(unsigned long long) * kStats * L));
+    e->stats_h.assign(kStats * L, 0);
     // mapped control blocks
     CK(cudaHostAlloc(&e->hctrl, sizeof(HostCtrl) * L, cudaHostAllocMapped));
     std::memset((void*)e->hctrl, 0, sizeof(HostCtrl) * L);
@@ -658,9 +739,15 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     CK(cudaStreamCreateWithPriority(&e->copy_stream, cudaStreamNonBlocking, prio_hi));
     CK(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking));
+    if (!getenv("EF_CALLER_STREAM")) {
+      CK(cudaStreamCreateWithPriority(&e->compute_stream, cudaStreamNonBlocking, prio_hi));
+      CK(cudaEventCreateWithFlags(&e->join_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&e->join_out, cudaEventDisableTiming));
+    }
     e->slot_seq.assign(e->P, 0);
     e->pinned.assign(e->P, 0);
     e->phys_of.assign((size_t)L * M, -1);
+    e->layer_R.assign(L, 1);
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
     e->init_weights();
@@ -671,6 +758,10 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     if (ffn && std::string(ffn) == "persistent") e->ffn_mode = 1;
     if (ffn && std::string(ffn) == "stream") e->ffn_mode = 0;
     CK(cudaMalloc(&e->counters_d, sizeof(int) * (kMaxActive + 1)));
+    CK(cudaMalloc(&e->fuse_d, sizeof(int) * 4));
+    CK(cudaMemset(e->fuse_d, 0, sizeof(int) * 4));
+    const char* fz = getenv("EF_FUSE");
+    if (fz) e->fuse = atoi(fz);
     *out = e.release();
   });
 }

@@ -107,6 +107,31 @@ __global__ void rmsnorm_kernel(const float* __restrict__ h, float* __restrict__ 
   for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)blockIdx.x * d + i] = hr[i] * inv;
 }
 
+// h[t] += sum_r wts[t,r] * y[inv[t,r]] (rank order) + g_t * ys[t]; x[t] = rmsnorm(h[t]).
+// Any block size; all threads of the block must call it.
+__device__ void combine_token(int t, float* __restrict__ h, float* __restrict__ x,
+                              const float* __restrict__ y, const int32_t* __restrict__ inv,
+                              const float* __restrict__ wts, const float* __restrict__ ys,
+                              const float* __restrict__ gate_logit, int d, int k, float eps,
+                              float* red) {
+  float g = 1.f;
+  if (gate_logit) g = 1.0f / (1.0f + expf(-gate_logit[t]));
+  float* hr = h + (int64_t)t * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float acc = 0.f;
+    for (int r = 0; r < k; ++r)
+      acc = fmaf(wts[t * k + r], __ldcg(y + (int64_t)inv[t * k + r] * d + i), acc);
+    if (ys) acc = fmaf(g, ys[(int64_t)t * d + i], acc);
+    float v = hr[i] + acc;
+    hr[i] = v;
+    ss += v * v;
+  }
+  ss = block_sum(ss, red);
+  float invn = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)t * d + i] = hr[i] * invn;
+}
+
 extern "C" int ef_rmsnorm(void* stream, const float* h, float* x, int B, int d, float eps) {
   EF_CHECK_ARG(B >= 0 && d > 0, "bad rmsnorm shape");
   if (B == 0) return EF_OK;
@@ -214,58 +239,103 @@ extern "C" int ef_router_logits(void* stream, const float* x, const void* w, int
 constexpr int kRouteThreads = 1024;
 constexpr int kMaxExperts = 256;
 
-__global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
-    const float* __restrict__ logits, int B, int M, int k, int mode, float bias, uint64_t mlo,
-    uint64_t mhi, int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts,
-    int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-    const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
-    volatile uint32_t* host_done, unsigned long long* stamp) {
-  __shared__ int32_t warp_cnt[32][kMaxExperts];
-  __shared__ int32_t base[kMaxExperts];
-  __shared__ int32_t total[kMaxExperts];
+struct RouteSmem {
+  int32_t warp_cnt[32][kMaxExperts];
+  int32_t base[kMaxExperts];
+  int32_t total[kMaxExperts];
+  uint64_t mask[2];
+};
+
+// Route body, usable by any block size (the standalone kernel runs it with
+// 1024 threads, the fused router kernel with the last router CTA).
+__device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int B, int M, int k,
+                           int mode, float bias, uint64_t mlo, uint64_t mhi,
+                           int32_t* __restrict__ sel, float* __restrict__ wts,
+                           int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
+                           int32_t* __restrict__ perm, int32_t* __restrict__ inv,
+                           const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
+                           volatile uint32_t* host_done, unsigned long long* stamp) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (stamp && tid == 0) *stamp = gtimer();
-  if (mask_src) {  // engine pipeline: the host publishes the residency mask before go(l-1)
-    mlo = mask_src[0];
-    mhi = mask_src[1];
+  if (mask_src) {  // mask in mapped host memory: one PCIe read, broadcast through smem
+    if (tid == 0) {
+      sm.mask[0] = mask_src[0];
+      sm.mask[1] = mask_src[1];
+    }
+    __syncthreads();
+    mlo = sm.mask[0];
+    mhi = sm.mask[1];
   }
 
-  // ---- top-k and weights: one thread per token
-  for (int t = tid; t < B; t += blockDim.x) {
+  // ---- top-k and weights: one warp per token, logits in registers (M <= 128),
+  // k rounds of a warp arg-max keyed (value desc, index asc) — SURVEY H6
+  for (int t = wid; t < B; t += blockDim.x / 32) {
     const float* lg = logits + (int64_t)t * M;
-    int chosen[16];
-    float mx_all = -INFINITY;
-    for (int e = 0; e < M; ++e) mx_all = fmaxf(mx_all, lg[e]);
+    float v[4], key[4];
+    bool taken[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = lane + 32 * i;
+      v[i] = e < M ? lg[e] : -INFINITY;
+      const bool res = e < 64 ? ((mlo >> e) & 1ull) : ((mhi >> (e - 64)) & 1ull);
+      key[i] = (e < M && res && bias != 0.f) ? __fadd_rn(v[i], bias) : v[i];
+      taken[i] = e >= M;
+    }
+    float mx_all = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx_all = fmaxf(mx_all, __shfl_xor_sync(0xffffffffu, mx_all, o));
+    float chosen_v[16];
+    int chosen_e[16];
     for (int r = 0; r < k; ++r) {
-      float best = -INFINITY;
-      int be = -1;
-      for (int e = 0; e < M; ++e) {
-        bool used = false;
-        for (int q = 0; q < r; ++q) used |= (chosen[q] == e);
-        if (used) continue;
-        bool res = e < 64 ? ((mlo >> e) & 1ull) : ((mhi >> (e - 64)) & 1ull);
-        float key = (res && bias != 0.f) ? __fadd_rn(lg[e], bias) : lg[e];
-        if (be < 0 || key > best) {
-          best = key;
+      float bk = 0.f;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = lane + 32 * i;
+        if (!taken[i] && (be == 0x7fffffff || key[i] > bk)) {
+          bk = key[i];
           be = e;
         }
       }
-      chosen[r] = be;
-      sel[t * k + r] = be;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        const bool other_better =
+            oe != 0x7fffffff && (be == 0x7fffffff || ok > bk || (ok == bk && oe < be));
+        if (other_better) {
+          bk = ok;
+          be = oe;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (lane + 32 * i == be) taken[i] = true;
+      chosen_e[r] = be;
+      chosen_v[r] = lg[be];  // raw logit (weights ignore the bias)
+    }
+    if (lane == 0) {
+      for (int r = 0; r < k; ++r) sel[t * k + r] = chosen_e[r];
     }
     if (mode == EF_ROUTE_MIXTRAL) {
-      float mx = -INFINITY;
-      for (int r = 0; r < k; ++r) mx = fmaxf(mx, lg[chosen[r]]);
-      float ev[16], s = 0.f;
-      for (int r = 0; r < k; ++r) {
-        ev[r] = expf(lg[chosen[r]] - mx);
-        s += ev[r];
+      if (lane == 0) {
+        float mx = -INFINITY;
+        for (int r = 0; r < k; ++r) mx = fmaxf(mx, chosen_v[r]);
+        float ev[16], sum = 0.f;
+        for (int r = 0; r < k; ++r) {
+          ev[r] = expf(chosen_v[r] - mx);
+          sum += ev[r];
+        }
+        for (int r = 0; r < k; ++r) wts[t * k + r] = ev[r] / sum;
       }
-      for (int r = 0; r < k; ++r) wts[t * k + r] = ev[r] / s;
     } else {
-      float s = 0.f;
-      for (int e = 0; e < M; ++e) s += expf(lg[e] - mx_all);
-      for (int r = 0; r < k; ++r) wts[t * k + r] = expf(lg[chosen[r]] - mx_all) / s;
+      float part = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (lane + 32 * i < M) part += expf(v[i] - mx_all);
+      const float sum = warp_sum(part);
+      if (lane == 0)
+        for (int r = 0; r < k; ++r) wts[t * k + r] = expf(chosen_v[r] - mx_all) / sum;
     }
   }
   __syncthreads();
@@ -273,47 +343,47 @@ __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
   // ---- stable counting sort by expert over flat slots f = t*k + r
   const int N = B * k;
   for (int e = tid; e < M; e += blockDim.x) {
-    base[e] = 0;
-    total[e] = 0;
+    sm.base[e] = 0;
+    sm.total[e] = 0;
   }
   __syncthreads();
   for (int c0 = 0; c0 < N; c0 += blockDim.x) {
-    for (int i = tid; i < 32 * M; i += blockDim.x) warp_cnt[i / M][i % M] = 0;
+    for (int i = tid; i < 32 * M; i += blockDim.x) sm.warp_cnt[i / M][i % M] = 0;
     __syncthreads();
     int f = c0 + tid;
     int e = (f < N) ? sel[f] : -1;
     unsigned same = __match_any_sync(0xffffffffu, e);
     int rank_in_warp = __popc(same & ((1u << lane) - 1u));
-    if (e >= 0 && rank_in_warp == 0) warp_cnt[wid][e] = __popc(same);
+    if (e >= 0 && rank_in_warp == 0) sm.warp_cnt[wid][e] = __popc(same);
     __syncthreads();
     // exclusive prefix over warps, per expert
     for (int x = tid; x < M; x += blockDim.x) {
-      int run = base[x];
+      int run = sm.base[x];
       for (int w = 0; w < 32; ++w) {
-        int c = warp_cnt[w][x];
-        warp_cnt[w][x] = run;
+        int c = sm.warp_cnt[w][x];
+        sm.warp_cnt[w][x] = run;
         run += c;
       }
-      base[x] = run;
+      sm.base[x] = run;
     }
     __syncthreads();
-    if (e >= 0) perm[f] = warp_cnt[wid][e] + rank_in_warp;  // rank within expert (temp)
+    if (e >= 0) perm[f] = sm.warp_cnt[wid][e] + rank_in_warp;  // rank within expert (temp)
     __syncthreads();
   }
   // counts and offsets
   if (tid == 0) {
     int run = 0;
     for (int x = 0; x < M; ++x) {
-      counts[x] = base[x];
+      counts[x] = sm.base[x];
       offsets[x] = run;
-      total[x] = run;
-      run += base[x];
+      sm.total[x] = run;
+      run += sm.base[x];
     }
     offsets[M] = run;
   }
   __syncthreads();
   for (int f = tid; f < N; f += blockDim.x) {
-    int pos = total[sel[f]] + perm[f];
+    int pos = sm.total[sel[f]] + perm[f];
     inv[f] = pos;
   }
   __syncthreads();
@@ -325,9 +395,214 @@ __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
     for (int i = lane; i < B * M; i += 32) host_logits[i] = logits[i];
     __threadfence_system();
     __syncwarp();
-    if (lane == 0) *host_done = 1u;
+    if (lane == 0) {
+      *host_done = 1u;
+      if (stamp) stamp[3] = gtimer();  // slot 9: selection published
+    }
   }
 }
+
+__global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
+    const float* __restrict__ logits, int B, int M, int k, int mode, float bias, uint64_t mlo,
+    uint64_t mhi, int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts,
+    int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv,
+    const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
+    volatile uint32_t* host_done, unsigned long long* stamp) {
+  __shared__ RouteSmem sm;
+  route_body(sm, logits, B, M, k, mode, bias, mlo, mhi, sel, wts, counts, offsets, perm, inv,
+             mask_src, host_sel, host_logits, host_done, stamp);
+}
+
+// Engine decode path: router GEMV rows, then the last CTA to finish runs
+// the route body (top-k, weights, permutation, host publish) — one kernel
+// boundary instead of two on the per-layer critical path.
+struct RouteArgs {
+  int B, M, k, mode;
+  float bias;
+  uint64_t mlo, mhi;
+  int32_t *sel, *counts, *offsets, *perm, *inv, *host_sel;
+  float *wts, *host_logits;
+  uint32_t* host_done;
+  unsigned long long* stamp_route;
+  int* counter;
+};
+
+// Previous layer's combine folded into the router (small batches): every CTA
+// recomputes h + sum_r w*y (+ g*ys) and the rmsnorm scale for its tokens into
+// shared memory; the last CTA writes h and x back once all CTAs have read h.
+struct CombArgs {
+  float* h;  // null: x comes from global memory as usual
+  float* x_out;
+  const float* y;
+  const int32_t* inv;
+  const float* wts;
+  const float* ys;
+  const float* gate_logit;
+  int k;
+  float eps;
+  unsigned long long* stamp;
+};
+constexpr int kCombSmemMax = 128 * 1024;
+
+template <typename WT, int MAXB>
+__global__ void __launch_bounds__(256) router_route_kernel(const float* __restrict__ x,
+                                                           const WT* __restrict__ w, int rows,
+                                                           int d, float* __restrict__ logits,
+                                                           unsigned long long* stamp,
+                                                           RouteArgs ra, CombArgs cb) {
+  constexpr int V = WTraits<WT>::kPer16;
+  const int B = ra.B, M = ra.M;
+  const int t0 = blockIdx.y * MAXB;
+  const int nb = min(MAXB, B - t0);
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = gtimer();
+  extern __shared__ float hs[];  // [nb][d] combined, un-normalised rows (cb.h only)
+  __shared__ float invn_s[MAXB];
+  __shared__ float red[32];
+  const bool comb = cb.h != nullptr;
+  if (comb) {
+    for (int t = 0; t < nb; ++t) {
+      const int tt = t0 + t;
+      const float g = cb.gate_logit ? 1.0f / (1.0f + expf(-cb.gate_logit[tt])) : 1.f;
+      float ss = 0.f;
+      for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float acc = 0.f;
+        for (int r = 0; r < cb.k; ++r)
+          acc = fmaf(cb.wts[tt * cb.k + r], __ldcg(cb.y + (int64_t)cb.inv[tt * cb.k + r] * d + i),
+                     acc);
+        if (cb.ys) acc = fmaf(g, cb.ys[(int64_t)tt * d + i], acc);
+        const float v = cb.h[(int64_t)tt * d + i] + acc;
+        hs[t * d + i] = v;
+        ss += v * v;
+      }
+      ss = block_sum(ss, red);
+      if (threadIdx.x == 0) invn_s[t] = 1.0f / sqrtf(ss / (float)d + cb.eps);
+    }
+    __syncthreads();
+  }
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp < rows) {
+    const WT* wr = w + (int64_t)warp * d;
+    float acc[MAXB];
+#pragma unroll
+    for (int t = 0; t < MAXB; ++t) acc[t] = 0.f;
+    // four 16-byte chunks in flight per lane
+    for (int c0 = lane * V; c0 < d; c0 += 4 * 32 * V) {
+      uint4 wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u * 32 * V < d) wv[u] = ld_stream16(wr + c0 + u * 32 * V);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 32 * V;
+        if (c < d) {
+          float f[V];
+          WTraits<WT>::unpack(wv[u], f);
+#pragma unroll
+          for (int t = 0; t < MAXB; ++t) {
+            if (t < nb) {
+              const float4* xp = reinterpret_cast<const float4*>(x + (int64_t)(t0 + t) * d + c);
+              const float4* hp = reinterpret_cast<const float4*>(hs + t * d + c);
+#pragma unroll
+              for (int q = 0; q < V / 4; ++q) {
+                float4 xv;
+                if (comb) {  // x = v * invn, the same fp32 product the combine kernel stores
+                  xv = hp[q];
+                  const float s = invn_s[t];
+                  xv.x *= s;
+                  xv.y *= s;
+                  xv.z *= s;
+                  xv.w *= s;
+                } else {
+                  xv = __ldg(xp + q);
+                }
+                acc[t] = fmaf(f[4 * q + 0], xv.x, acc[t]);
+                acc[t] = fmaf(f[4 * q + 1], xv.y, acc[t]);
+                acc[t] = fmaf(f[4 * q + 2], xv.z, acc[t]);
+                acc[t] = fmaf(f[4 * q + 3], xv.w, acc[t]);
+              }
+            }
+          }
+        }
+      }
+    }
+    const int r = warp / M, m = warp % M;
+#pragma unroll
+    for (int t = 0; t < MAXB; ++t) {
+      if (t < nb) {
+        float sum = warp_sum(acc[t]);
+        if (lane == 0) logits[((int64_t)r * B + t0 + t) * M + m] = sum;
+      }
+    }
+  }
+  __shared__ RouteSmem sm;
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    last = atomicAdd(ra.counter, 1) == (int)(gridDim.x * gridDim.y) - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (comb) {  // every CTA has read h: publish h and x for the rest of the layer
+    for (int t = 0; t < nb; ++t) {
+      const int tt = t0 + t;
+      for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const float v = hs[t * d + i];
+        cb.h[(int64_t)tt * d + i] = v;
+        cb.x_out[(int64_t)tt * d + i] = v * invn_s[t];
+      }
+    }
+    if (cb.stamp && threadIdx.x == 0) *cb.stamp = gtimer();
+  }
+  route_body(sm, logits, B, M, ra.k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.sel, ra.wts, ra.counts,
+             ra.offsets, ra.perm, ra.inv, nullptr, ra.host_sel, ra.host_logits, ra.host_done,
+             ra.stamp_route);
+  if (threadIdx.x == 0) *ra.counter = 0;  // ready for the next launch
+}
+
+namespace ef {
+int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
+                       int d, int M, float* logits, unsigned long long* stamp_router, int k,
+                       int mode, float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
+                       int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
+                       int32_t* host_sel, float* host_logits, uint32_t* host_done,
+                       unsigned long long* stamp_route, int* counter, const CombineIn* ci) {
+  EF_CHECK_ARG(M <= 128 && k <= 16 && B >= 1, "bad fused route shape");
+  RouteArgs ra{B, M, k, mode, bias, mlo, mhi, sel, counts, offsets, perm, inv, host_sel, wts,
+               host_logits, host_done, stamp_route, counter};
+  CombArgs cb{};
+  size_t smem = 0;
+  if (ci) {
+    EF_CHECK_ARG(B <= 8 && (size_t)B * d * 4 <= (size_t)kCombSmemMax,
+                 "combine-in-router needs B*d*4 <= 128 KiB");
+    // the previous layer's y / inv / wts are read before route_body of this
+    // layer overwrites inv / wts (only the last CTA routes)
+    cb = CombArgs{ci->h, const_cast<float*>(x), ci->y, inv, wts, ci->ys, ci->gate_logit, k,
+                  ci->eps, ci->stamp};
+    smem = (size_t)B * d * 4;
+  }
+  const int rows = R * M, threads = 256;
+  const int blocks = (rows * 32 + threads - 1) / threads;
+  if (dtype == EF_BF16) {
+    if (B == 1)
+      router_route_kernel<__nv_bfloat16, 1><<<dim3(blocks, 1), threads, smem, st>>>(
+          x, (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb);
+    else
+      router_route_kernel<__nv_bfloat16, 8><<<dim3(blocks, (B + 7) / 8), threads, smem, st>>>(
+          x, (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb);
+  } else {
+    if (B == 1)
+      router_route_kernel<float, 1><<<dim3(blocks, 1), threads, smem, st>>>(
+          x, (const float*)w, rows, d, logits, stamp_router, ra, cb);
+    else
+      router_route_kernel<float, 8><<<dim3(blocks, (B + 7) / 8), threads, smem, st>>>(
+          x, (const float*)w, rows, d, logits, stamp_router, ra, cb);
+  }
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+}  // namespace ef
 
 extern "C" int ef_route_permute(void* stream, const float* logits, int B, int M, int k, int mode,
                                 float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
@@ -406,6 +681,7 @@ struct CtrlSrc {
 // ~10 s at 2 GHz: a spin this long means the host side died; fail loudly
 // instead of hanging the GPU.
 constexpr long long kSpinTimeoutCycles = 20000000000LL;
+constexpr int kStatsPerLayer = 16;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -413,21 +689,109 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Kernel fusions of the engine's decode pipeline (split FFN path):
+//  * gate in the up kernel: warp 0 of CTA (0,0) waits for the host's go flag
+//    and copies the decision into DevCtrl, then raises a device flag the
+//    other CTAs wait on (one PCIe round trip, no separate gate launch);
+//  * combine in the down kernel: the last CTA to finish does the weighted
+//    combine + residual + next rmsnorm for all tokens (small batches).
+struct FuseArgs {
+  volatile HostCtrl* hc;
+  DevCtrl* dc;
+  volatile unsigned* dflag;
+  unsigned seq;
+  int* counter;
+  float* h;
+  float* x;
+  const float* y;
+  const int32_t* inv;
+  const float* wts;
+  const float* ys;
+  const float* gate_logit;
+  int B, d, k;
+  float eps;
+  unsigned long long* stamp_combine;
+};
+
+__device__ __forceinline__ uint2 ld_acquire_sys_v2_(const volatile void* p) {
+  uint2 v;
+  asm volatile("ld.acquire.sys.global.v2.u32 {%0,%1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ int4 ld_volatile_v4_(const volatile void* p) {
+  int4 v;
+  asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const volatile unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One full warp: wait for go, copy the decision, publish it on the device.
+__device__ void gate_duty(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats,
+                          volatile unsigned* dflag, unsigned seq) {
+  const int lane = threadIdx.x & 31;
+  uint2 gn = make_uint2(0, 0);
+  if (lane == 0) {
+    if (stats) stats[0] = globaltimer();
+    const long long c0 = clock64();
+    for (;;) {
+      gn = ld_acquire_sys_v2_(&hc->go);
+      if (gn.x != 0u) break;
+      __nanosleep(64);
+      if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+    }
+    if (stats) stats[1] = globaltimer();
+  }
+  const int n = __shfl_sync(0xffffffffu, (int)gn.y, 0);
+  for (int i = lane; i < n; i += 32) dc->ent[i] = ld_volatile_v4_(&hc->ent[i]);
+  __syncwarp();
+  if (lane == 0) {
+    dc->n_active = n;
+    __threadfence();
+    if (dflag) *dflag = seq;
+    hc->go = 0u;
+    if (stats) stats[8] = globaltimer();
+  }
+  __syncwarp();
+}
+
 template <typename WT, int NT, int R, bool DUAL, typename XL, int U = 1>
-__global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs, int64_t offA,
-                                                       int64_t offB, int rows, int cols, XL xl,
-                                                       WT* act_out, float* y_out, int out_ld) {
+__global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs, FuseArgs fz,
+                                                       int64_t offA, int64_t offB, int rows,
+                                                       int cols, XL xl, WT* act_out, float* y_out,
+                                                       int out_ld) {
   constexpr int V = WTraits<WT>::kPer16;
   constexpr int WARPS = 4;
   const int a = blockIdx.y;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int n_all, p0;
   const char* wbase;
+  if (fz.hc) {  // fused gate (up kernel)
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+      if (wid == 0) gate_duty(fz.hc, fz.dc, cs.stats, fz.dflag, fz.seq);
+    } else if (threadIdx.x == 0) {
+      const long long c0 = clock64();
+      while (ld_acquire_gpu(fz.dflag) < fz.seq) {
+        __nanosleep(64);
+        if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+      }
+    }
+    __syncthreads();
+  }
   if (cs.ctrl) {
     __shared__ int4 e_sh;
     if (threadIdx.x == 0) {
+      if (cs.wait_ready && cs.stats) atomicMin(&cs.stats[10], globaltimer());
       int4 e = make_int4(0, 0, 0, 0);
-      if (a < cs.ctrl->n_active) e = cs.ctrl->ent[a];
+      if (a < __ldcg(&cs.ctrl->n_active)) e = __ldcg(&cs.ctrl->ent[a]);
       if (cs.wait_ready && e.z > 0) {
         unsigned long long t0 = globaltimer();
         unsigned need = (unsigned)e.w;
@@ -454,13 +818,13 @@ __global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs
     p0 = al.p0[a];
     wbase = al.w[a];
   }
-  if (n_all == 0) return;
   const int j0 = (blockIdx.x * WARPS + wid) * R;
-  if (j0 >= rows) return;
+  // no early return: the fused combine counts every CTA of the grid
+  const bool work = n_all > 0 && j0 < rows;
   const WT* A = reinterpret_cast<const WT*>(wbase + offA);
   const WT* Bm = reinterpret_cast<const WT*>(wbase + offB);
 
-  for (int tc = 0; tc < n_all; tc += NT) {
+  for (int tc = 0; work && tc < n_all; tc += NT) {
     const int nt = min(NT, n_all - tc);
     float accA[R][NT], accB[R][NT];
 #pragma unroll
@@ -534,17 +898,37 @@ __global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs
       }
     }
   }
-  if (cs.ctrl && !DUAL && cs.stats && lane == 0) atomicMax(&cs.stats[4], globaltimer());
+  if (work && cs.ctrl && !DUAL && cs.stats && lane == 0) atomicMax(&cs.stats[4], globaltimer());
+  if (!DUAL && fz.counter) {  // fused combine: the last CTA of the grid does it
+    __shared__ int last;
+    __shared__ float red[32];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      last = atomicAdd(fz.counter, 1) == (int)(gridDim.x * gridDim.y) - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      for (int t = 0; t < fz.B; ++t)
+        combine_token(t, fz.h, fz.x, fz.y, fz.inv, fz.wts, fz.ys, fz.gate_logit, fz.d, fz.k,
+                      fz.eps, red);
+      if (threadIdx.x == 0) {
+        *fz.counter = 0;
+        if (fz.stamp_combine) *fz.stamp_combine = gtimer();
+      }
+    }
+  }
 }
 
 template <typename WT, int NT>
 static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& cs, int n_active,
-                          int d, int ff, const XGather<WT>& xg, WT* act, float* y) {
+                          int d, int ff, const XGather<WT>& xg, WT* act, float* y,
+                          const FuseArgs& fz_up, const FuseArgs& fz_dn) {
   constexpr int R = 4, WARPS = 4;
   const int64_t es = sizeof(WT);
   dim3 gu((ff + WARPS * R - 1) / (WARPS * R), n_active);
   ffn_gemv_kernel<WT, NT, R, true, XGather<WT>>
-      <<<gu, 128, 0, st>>>(al, cs, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
+      <<<gu, 128, 0, st>>>(al, cs, fz_up, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
   // down projection: one W2 row per warp, 4 column chunks in flight per lane
   // (d rows only: R=4 left most SMs idle on Mixtral's 4096 x 14336 W2)
   constexpr int RD = 1, UD = 4;
@@ -553,20 +937,21 @@ static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& 
   CtrlSrc cs2 = cs;
   cs2.wait_ready = false;
   ffn_gemv_kernel<WT, NT, RD, false, XAct<WT>, UD>
-      <<<gd, 128, 0, st>>>(al, cs2, 2 * (int64_t)ff * d * es, 0, d, ff, xa, nullptr, y, d);
+      <<<gd, 128, 0, st>>>(al, cs2, fz_dn, 2 * (int64_t)ff * d * es, 0, d, ff, xa, nullptr, y, d);
 }
 
 template <typename WT>
 static void launch_ffn(cudaStream_t st, const ActiveList& al, const CtrlSrc& cs, int n_active,
-                       int max_rows, int d, int ff, const XGather<WT>& xg, WT* act, float* y) {
+                       int max_rows, int d, int ff, const XGather<WT>& xg, WT* act, float* y,
+                       const FuseArgs& fu = FuseArgs{}, const FuseArgs& fd = FuseArgs{}) {
   if (max_rows <= 1)
-    launch_ffn_nt<WT, 1>(st, al, cs, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 1>(st, al, cs, n_active, d, ff, xg, act, y, fu, fd);
   else if (max_rows <= 2)
-    launch_ffn_nt<WT, 2>(st, al, cs, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 2>(st, al, cs, n_active, d, ff, xg, act, y, fu, fd);
   else if (max_rows <= 4)
-    launch_ffn_nt<WT, 4>(st, al, cs, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 4>(st, al, cs, n_active, d, ff, xg, act, y, fu, fd);
   else
-    launch_ffn_nt<WT, 8>(st, al, cs, n_active, d, ff, xg, act, y);
+    launch_ffn_nt<WT, 8>(st, al, cs, n_active, d, ff, xg, act, y, fu, fd);
 }
 
 namespace ef {
@@ -593,6 +978,50 @@ int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k,
   } else {
     XGather<float> xg{x, perm, k, d, identity, identity ? p0[0] : 0};
     launch_ffn<float>(st, al, cs, n_active, max_rows, d, ff, xg, (float*)act, y);
+  }
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// Engine pipeline with the gate folded into the up kernel and (optionally)
+// the combine folded into the down kernel.
+int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
+                     int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
+                     unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
+                     int max_rows, int d, int ff, int dtype, void* act, float* y, int* counter,
+                     float* h, float* xnext, const int32_t* inv, const float* wts, const float* ys,
+                     const float* gate_logit, int B, float eps) {
+  EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
+  ActiveList al{};
+  CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
+  FuseArgs fu{};
+  fu.hc = reinterpret_cast<volatile HostCtrl*>(hctrl_dev);
+  fu.dc = reinterpret_cast<DevCtrl*>(dctrl);
+  fu.dflag = dflag;
+  fu.seq = seq;
+  FuseArgs fd{};
+  if (counter) {
+    fd.counter = counter;
+    fd.h = h;
+    fd.x = xnext;
+    fd.y = y;
+    fd.inv = inv;
+    fd.wts = wts;
+    fd.ys = ys;
+    fd.gate_logit = gate_logit;
+    fd.B = B;
+    fd.d = d;
+    fd.k = k;
+    fd.eps = eps;
+    fd.stamp_combine = stats ? stats + 5 : nullptr;
+  }
+  if (dtype == EF_BF16) {
+    XGather<__nv_bfloat16> xg{x, perm, k, d, false, 0};
+    launch_ffn<__nv_bfloat16>(st, al, cs, max_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y,
+                              fu, fd);
+  } else {
+    XGather<float> xg{x, perm, k, d, false, 0};
+    launch_ffn<float>(st, al, cs, max_active, max_rows, d, ff, xg, (float*)act, y, fu, fd);
   }
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
@@ -1192,6 +1621,7 @@ __global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long lo
   if (lane == 0) {
     dc->n_active = n;
     hc->go = 0u;  // consumed; the host sets it again for the next token's layer
+    stats[8] = globaltimer();
   }
 }
 
@@ -1338,7 +1768,8 @@ int launch_set_ready(cudaStream_t st, uint32_t* ready, int slot, uint32_t seq) {
 }
 
 __global__ void init_stats_kernel(unsigned long long* stats, int L) {
-  for (int i = threadIdx.x; i < L * 8; i += blockDim.x) stats[i] = (i % 8 == 3) ? ~0ull : 0ull;
+  for (int i = threadIdx.x; i < L * kStatsPerLayer; i += blockDim.x)
+    stats[i] = (i % kStatsPerLayer == 3 || i % kStatsPerLayer == 10) ? ~0ull : 0ull;
 }
 
 int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L) {
@@ -1348,11 +1779,12 @@ int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L) {
 }
 
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
-                         float bias, int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
-                         int32_t* perm, int32_t* inv, const void* mask_src, int32_t* host_sel,
-                         float* host_logits, uint32_t* host_done, unsigned long long* stamp) {
+                         float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
+                         int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
+                         const void* mask_src, int32_t* host_sel, float* host_logits,
+                         uint32_t* host_done, unsigned long long* stamp) {
   route_permute_kernel<<<1, kRouteThreads, 0, st>>>(
-      logits, B, M, k, mode, bias, 0ull, 0ull, sel, wts, counts, offsets, perm, inv,
+      logits, B, M, k, mode, bias, mlo, mhi, sel, wts, counts, offsets, perm, inv,
       reinterpret_cast<const volatile uint64_t*>(mask_src), host_sel, host_logits, host_done,
       stamp);
   EF_CUDA_RET(cudaGetLastError());
@@ -1403,23 +1835,7 @@ __global__ void combine_kernel(float* __restrict__ h, float* __restrict__ x,
                                const float* __restrict__ gate_logit, int d, int k, float eps,
                                unsigned long long* stamp) {
   __shared__ float red[32];
-  const int t = blockIdx.x;
-  float g = 1.f;
-  if (gate_logit) g = 1.0f / (1.0f + expf(-gate_logit[t]));
-  float* hr = h + (int64_t)t * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float acc = 0.f;
-    for (int r = 0; r < k; ++r)
-      acc = fmaf(wts[t * k + r], y[(int64_t)inv[t * k + r] * d + i], acc);
-    if (ys) acc = fmaf(g, ys[(int64_t)t * d + i], acc);
-    float v = hr[i] + acc;
-    hr[i] = v;
-    ss += v * v;
-  }
-  ss = block_sum(ss, red);
-  float invn = 1.0f / sqrtf(ss / (float)d + eps);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)t * d + i] = hr[i] * invn;
+  combine_token(blockIdx.x, h, x, y, inv, wts, ys, gate_logit, d, k, eps, red);
   if (stamp && threadIdx.x == 0) atomicMax(stamp, gtimer());
 }
 
@@ -1459,6 +1875,12 @@ template <typename WT>
 static void preload_dtype(int& n) {
   preload(router_kernel<WT, 1>, n);
   preload(router_kernel<WT, 8>, n);
+  preload(router_route_kernel<WT, 1>, n);
+  preload(router_route_kernel<WT, 8>, n);
+  cudaFuncSetAttribute(router_route_kernel<WT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kCombSmemMax);
+  cudaFuncSetAttribute(router_route_kernel<WT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kCombSmemMax);
   preload(ffn_persist_kernel<WT, 1>, n);
   preload(ffn_persist_kernel<WT, 2>, n);
   preload(ffn_persist_kernel<WT, 4>, n);

@@ -12,6 +12,7 @@
 
 namespace ef {
 constexpr int kMaxActive = 80;
+constexpr int kStats = 16;  // per-layer device timeline slots (see engine.cu dump)
 
 struct HostCtrl {
   volatile uint32_t go;
@@ -51,12 +52,39 @@ int expert_ffn_stream(cudaStream_t st, const float* x, const int32_t* perm, int 
                       unsigned long long* stats, int* counters, int max_rows, int d, int ff,
                       int dtype, void* act, float* y);
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
-                         float bias, int32_t* sel, float* wts, int32_t* counts, int32_t* offsets,
-                         int32_t* perm, int32_t* inv, const void* mask_src, int32_t* host_sel,
-                         float* host_logits, uint32_t* host_done, unsigned long long* stamp);
+                         float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
+                         int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
+                         const void* mask_src, int32_t* host_sel, float* host_logits,
+                         uint32_t* host_done, unsigned long long* stamp);
 int router_logits_stamped(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
                           int d, int M, float* logits, unsigned long long* stamp);
 int combine_stamped(cudaStream_t st, float* h, float* x, const float* y, const int32_t* inv,
                     const float* wts, const float* ys, const float* gate_logit, int B, int d, int k,
                     float eps, unsigned long long* stamp);
+// Fused decode pipeline (default for the split FFN): router + route in one
+// kernel (the last CTA routes), gate folded into the up kernel, combine +
+// next rmsnorm folded into the down kernel's last CTA when counter != null.
+// The previous layer's combine, folded into router_route_fused (x is then
+// both the router input and, rewritten by the last CTA, the layer's x).
+struct CombineIn {
+  float* h;
+  const float* y;
+  const float* ys;
+  const float* gate_logit;
+  float eps;
+  unsigned long long* stamp;
+};
+int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
+                       int d, int M, float* logits, unsigned long long* stamp_router, int k,
+                       int mode, float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
+                       int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
+                       int32_t* host_sel, float* host_logits, uint32_t* host_done,
+                       unsigned long long* stamp_route, int* counter,
+                       const CombineIn* comb = nullptr);
+int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
+                     int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
+                     unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
+                     int max_rows, int d, int ff, int dtype, void* act, float* y, int* counter,
+                     float* h, float* xnext, const int32_t* inv, const float* wts, const float* ys,
+                     const float* gate_logit, int B, float eps);
 }  // namespace ef
