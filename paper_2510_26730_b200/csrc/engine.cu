@@ -236,10 +236,9 @@ struct ef_engine {
   int ffn_mode = 2;  // EF_FFN: split (GEMV pair, default) | stream (bulk-copy) | persistent
   int* counters_d = nullptr;
   // EF_FUSE bit mask: 1 router+route in one kernel, 2 gate folded into the
-  // up kernel, 4 combine folded into the down kernel's last CTA
+  // up kernel, 8 combine(l-1) + rmsnorm folded into router_route(l)
   int fuse = 11;
-  int fuse_combine_max_b = 8;  // last-CTA combine only pays for small batches
-  int* fuse_d = nullptr;       // [0] route counter [1] combine counter [2] gate flag
+  int* fuse_d = nullptr;  // [0] route counter [2] gate flag
   unsigned gate_seq = 0;
   float* cur_h = nullptr;  // the step's hidden state (combine-in-router writes it)
   // EF_FUSE bit 8: combine(l-1) folded into router_route(l), small batches
@@ -390,15 +389,13 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
   const bool comb_next = comb_in_router(l + 1, B);
   if ((fuse & 2) && ffn_mode == 2) {
-    const bool comb = !comb_next && (fuse & 4) && B <= fuse_combine_max_b;
     ++gate_seq;
     CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
                          reinterpret_cast<volatile unsigned*>(fuse_d + 2), gate_seq, ready,
                          stats_d + kStats * l, std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d,
-                         y_d, comb ? fuse_d + 1 : nullptr, h, x_d, inv_d, wts_d,
-                         cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, B, 1e-6f));
+                         y_d));
     launches += 2;
-    if (!comb && !comb_next) {
+    if (!comb_next) {
       CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
                           sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
       ++launches;

@@ -107,29 +107,87 @@ __global__ void rmsnorm_kernel(const float* __restrict__ h, float* __restrict__ 
   for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)blockIdx.x * d + i] = hr[i] * inv;
 }
 
+// v = h[t] + (sum_r wts[t,r] * y[inv[t,r]] in rank order + g_t * ys[t]) into
+// vout (may alias h[t]); returns the block-wide sum of v^2.  float4 lanes with
+// P passes in flight so the L2 round trips overlap (d % 4 == 0).  Any block
+// size; all threads of the block must call it.
+__device__ float combine_row(int t, const float* h, float* vout, const float* __restrict__ y,
+                             const int32_t* __restrict__ inv, const float* __restrict__ wts,
+                             const float* __restrict__ ys, const float* __restrict__ gate_logit,
+                             int d, int k, float* red) {
+  constexpr int P = 4;
+  const float g = gate_logit ? 1.0f / (1.0f + expf(-gate_logit[t])) : 1.f;
+  const float* hr = h + (int64_t)t * d;
+  const int step = blockDim.x * 4;
+  float ss = 0.f;
+  for (int base = threadIdx.x * 4; base < d; base += step * P) {
+    float4 hv[P], sv[P], acc[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int i = base + p * step;
+      acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < d) {
+        hv[p] = __ldcg(reinterpret_cast<const float4*>(hr + i));
+        if (ys) sv[p] = __ldcg(reinterpret_cast<const float4*>(ys + (int64_t)t * d + i));
+      }
+    }
+    for (int r = 0; r < k; ++r) {
+      const float w = wts[t * k + r];
+      const float* yr = y + (int64_t)inv[t * k + r] * d;
+      float4 yv[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int i = base + p * step;
+        if (i < d) yv[p] = __ldcg(reinterpret_cast<const float4*>(yr + i));
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        acc[p].x = fmaf(w, yv[p].x, acc[p].x);
+        acc[p].y = fmaf(w, yv[p].y, acc[p].y);
+        acc[p].z = fmaf(w, yv[p].z, acc[p].z);
+        acc[p].w = fmaf(w, yv[p].w, acc[p].w);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int i = base + p * step;
+      if (i < d) {
+        if (ys) {
+          acc[p].x = fmaf(g, sv[p].x, acc[p].x);
+          acc[p].y = fmaf(g, sv[p].y, acc[p].y);
+          acc[p].z = fmaf(g, sv[p].z, acc[p].z);
+          acc[p].w = fmaf(g, sv[p].w, acc[p].w);
+        }
+        float4 v;
+        v.x = hv[p].x + acc[p].x;
+        v.y = hv[p].y + acc[p].y;
+        v.z = hv[p].z + acc[p].z;
+        v.w = hv[p].w + acc[p].w;
+        *reinterpret_cast<float4*>(vout + i) = v;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+    }
+  }
+  return block_sum(ss, red);
+}
+
 // h[t] += sum_r wts[t,r] * y[inv[t,r]] (rank order) + g_t * ys[t]; x[t] = rmsnorm(h[t]).
-// Any block size; all threads of the block must call it.
 __device__ void combine_token(int t, float* __restrict__ h, float* __restrict__ x,
                               const float* __restrict__ y, const int32_t* __restrict__ inv,
                               const float* __restrict__ wts, const float* __restrict__ ys,
                               const float* __restrict__ gate_logit, int d, int k, float eps,
                               float* red) {
-  float g = 1.f;
-  if (gate_logit) g = 1.0f / (1.0f + expf(-gate_logit[t]));
   float* hr = h + (int64_t)t * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float acc = 0.f;
-    for (int r = 0; r < k; ++r)
-      acc = fmaf(wts[t * k + r], __ldcg(y + (int64_t)inv[t * k + r] * d + i), acc);
-    if (ys) acc = fmaf(g, ys[(int64_t)t * d + i], acc);
-    float v = hr[i] + acc;
-    hr[i] = v;
-    ss += v * v;
+  const float ss = combine_row(t, h, hr, y, inv, wts, ys, gate_logit, d, k, red);
+  const float invn = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(hr + i);
+    v.x *= invn;
+    v.y *= invn;
+    v.z *= invn;
+    v.w *= invn;
+    *reinterpret_cast<float4*>(x + (int64_t)t * d + i) = v;
   }
-  ss = block_sum(ss, red);
-  float invn = 1.0f / sqrtf(ss / (float)d + eps);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)t * d + i] = hr[i] * invn;
 }
 
 extern "C" int ef_rmsnorm(void* stream, const float* h, float* x, int B, int d, float eps) {
@@ -461,20 +519,8 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   const bool comb = cb.h != nullptr;
   if (comb) {
     for (int t = 0; t < nb; ++t) {
-      const int tt = t0 + t;
-      const float g = cb.gate_logit ? 1.0f / (1.0f + expf(-cb.gate_logit[tt])) : 1.f;
-      float ss = 0.f;
-      for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        float acc = 0.f;
-        for (int r = 0; r < cb.k; ++r)
-          acc = fmaf(cb.wts[tt * cb.k + r], __ldcg(cb.y + (int64_t)cb.inv[tt * cb.k + r] * d + i),
-                     acc);
-        if (cb.ys) acc = fmaf(g, cb.ys[(int64_t)tt * d + i], acc);
-        const float v = cb.h[(int64_t)tt * d + i] + acc;
-        hs[t * d + i] = v;
-        ss += v * v;
-      }
-      ss = block_sum(ss, red);
+      const float ss = combine_row(t0 + t, cb.h, hs + t * d, cb.y, cb.inv, cb.wts, cb.ys,
+                                   cb.gate_logit, d, cb.k, red);
       if (threadIdx.x == 0) invn_s[t] = 1.0f / sqrtf(ss / (float)d + cb.eps);
     }
     __syncthreads();
@@ -486,14 +532,15 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     float acc[MAXB];
 #pragma unroll
     for (int t = 0; t < MAXB; ++t) acc[t] = 0.f;
-    // four 16-byte chunks in flight per lane
-    for (int c0 = lane * V; c0 < d; c0 += 4 * 32 * V) {
-      uint4 wv[4];
+    // UN 16-byte chunks in flight per lane (a 4096-wide bf16 row in one round trip at B=1)
+    constexpr int UN = MAXB == 1 ? 16 : 8;
+    for (int c0 = lane * V; c0 < d; c0 += UN * 32 * V) {
+      uint4 wv[UN];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < UN; ++u)
         if (c0 + u * 32 * V < d) wv[u] = ld_stream16(wr + c0 + u * 32 * V);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < UN; ++u) {
         const int c = c0 + u * 32 * V;
         if (c < d) {
           float f[V];
@@ -659,7 +706,7 @@ struct XAct {  // act[p] (already in the weight dtype)
   int ff;
   __device__ inline const WT* row(int p) const { return act + (int64_t)p * ff; }
   __device__ inline void load(const WT* r, int c, float* out) const {
-    WTraits<WT>::unpack(*reinterpret_cast<const uint4*>(r + c), out);
+    WTraits<WT>::unpack(__ldg(reinterpret_cast<const uint4*>(r + c)), out);
   }
 };
 
@@ -693,24 +740,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 //  * gate in the up kernel: warp 0 of CTA (0,0) waits for the host's go flag
 //    and copies the decision into DevCtrl, then raises a device flag the
 //    other CTAs wait on (one PCIe round trip, no separate gate launch);
-//  * combine in the down kernel: the last CTA to finish does the weighted
-//    combine + residual + next rmsnorm for all tokens (small batches).
+//  (the combine is folded into the next layer's router instead, see
+//   router_route_kernel: a last-CTA combine here serialised on one SM and
+//   its registers cost the down GEMV occupancy)
 struct FuseArgs {
   volatile HostCtrl* hc;
   DevCtrl* dc;
   volatile unsigned* dflag;
   unsigned seq;
-  int* counter;
-  float* h;
-  float* x;
-  const float* y;
-  const int32_t* inv;
-  const float* wts;
-  const float* ys;
-  const float* gate_logit;
-  int B, d, k;
-  float eps;
-  unsigned long long* stamp_combine;
 };
 
 __device__ __forceinline__ uint2 ld_acquire_sys_v2_(const volatile void* p) {
@@ -764,7 +801,7 @@ __device__ void gate_duty(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long
 }
 
 template <typename WT, int NT, int R, bool DUAL, typename XL, int U = 1>
-__global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs, FuseArgs fz,
+__global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_kernel(ActiveList al, CtrlSrc cs, FuseArgs fz,
                                                        int64_t offA, int64_t offB, int rows,
                                                        int cols, XL xl, WT* act_out, float* y_out,
                                                        int out_ld) {
@@ -899,39 +936,26 @@ __global__ void __launch_bounds__(128) ffn_gemv_kernel(ActiveList al, CtrlSrc cs
     }
   }
   if (work && cs.ctrl && !DUAL && cs.stats && lane == 0) atomicMax(&cs.stats[4], globaltimer());
-  if (!DUAL && fz.counter) {  // fused combine: the last CTA of the grid does it
-    __shared__ int last;
-    __shared__ float red[32];
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      last = atomicAdd(fz.counter, 1) == (int)(gridDim.x * gridDim.y) - 1;
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      for (int t = 0; t < fz.B; ++t)
-        combine_token(t, fz.h, fz.x, fz.y, fz.inv, fz.wts, fz.ys, fz.gate_logit, fz.d, fz.k,
-                      fz.eps, red);
-      if (threadIdx.x == 0) {
-        *fz.counter = 0;
-        if (fz.stamp_combine) *fz.stamp_combine = gtimer();
-      }
-    }
-  }
 }
+
+// Decode GEMV tilings (tools/ffn_lab.cu sweep on B200, Mixtral shapes):
+// gate/up: 2 rows x 2 column chunks per warp (8 x 16 B in flight per lane,
+// few distinct DRAM rows per warp) ran at 6.5 TB/s vs 5.5 TB/s for 4 x 1;
+// down: 1 row x 2 chunks with act through the read-only path, 6.2 TB/s.
+constexpr int kUpR = 2, kUpU = 2, kDnR = 1, kDnU = 2;
 
 template <typename WT, int NT>
 static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& cs, int n_active,
                           int d, int ff, const XGather<WT>& xg, WT* act, float* y,
                           const FuseArgs& fz_up, const FuseArgs& fz_dn) {
-  constexpr int R = 4, WARPS = 4;
+  constexpr int R = kUpR, WARPS = 4;
   const int64_t es = sizeof(WT);
   dim3 gu((ff + WARPS * R - 1) / (WARPS * R), n_active);
-  ffn_gemv_kernel<WT, NT, R, true, XGather<WT>>
+  ffn_gemv_kernel<WT, NT, R, true, XGather<WT>, kUpU>
       <<<gu, 128, 0, st>>>(al, cs, fz_up, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
-  // down projection: one W2 row per warp, 4 column chunks in flight per lane
-  // (d rows only: R=4 left most SMs idle on Mixtral's 4096 x 14336 W2)
-  constexpr int RD = 1, UD = 4;
+  // down projection: one W2 row per warp (d rows only: more rows per warp
+  // left SMs idle on Mixtral's 4096 x 14336 W2)
+  constexpr int RD = kDnR, UD = kDnU;
   dim3 gd((d + WARPS * RD - 1) / (WARPS * RD), n_active);
   XAct<WT> xa{act, ff};
   CtrlSrc cs2 = cs;
@@ -988,40 +1012,19 @@ int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k,
 int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                      int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
-                     int max_rows, int d, int ff, int dtype, void* act, float* y, int* counter,
-                     float* h, float* xnext, const int32_t* inv, const float* wts, const float* ys,
-                     const float* gate_logit, int B, float eps) {
+                     int max_rows, int d, int ff, int dtype, void* act, float* y) {
   EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
   ActiveList al{};
   CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
-  FuseArgs fu{};
-  fu.hc = reinterpret_cast<volatile HostCtrl*>(hctrl_dev);
-  fu.dc = reinterpret_cast<DevCtrl*>(dctrl);
-  fu.dflag = dflag;
-  fu.seq = seq;
-  FuseArgs fd{};
-  if (counter) {
-    fd.counter = counter;
-    fd.h = h;
-    fd.x = xnext;
-    fd.y = y;
-    fd.inv = inv;
-    fd.wts = wts;
-    fd.ys = ys;
-    fd.gate_logit = gate_logit;
-    fd.B = B;
-    fd.d = d;
-    fd.k = k;
-    fd.eps = eps;
-    fd.stamp_combine = stats ? stats + 5 : nullptr;
-  }
+  FuseArgs fu{reinterpret_cast<volatile HostCtrl*>(hctrl_dev), reinterpret_cast<DevCtrl*>(dctrl),
+              dflag, seq};
   if (dtype == EF_BF16) {
     XGather<__nv_bfloat16> xg{x, perm, k, d, false, 0};
     launch_ffn<__nv_bfloat16>(st, al, cs, max_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y,
-                              fu, fd);
+                              fu);
   } else {
     XGather<float> xg{x, perm, k, d, false, 0};
-    launch_ffn<float>(st, al, cs, max_active, max_rows, d, ff, xg, (float*)act, y, fu, fd);
+    launch_ffn<float>(st, al, cs, max_active, max_rows, d, ff, xg, (float*)act, y, fu);
   }
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
@@ -1829,7 +1832,7 @@ extern "C" int ef_gather_rows_bf16(void* stream, const float* x, const int32_t* 
 }
 
 // ============================================================ (c) combine + norm
-__global__ void combine_kernel(float* __restrict__ h, float* __restrict__ x,
+__global__ void __launch_bounds__(256) combine_kernel(float* __restrict__ h, float* __restrict__ x,
                                const float* __restrict__ y, const int32_t* __restrict__ inv,
                                const float* __restrict__ wts, const float* __restrict__ ys,
                                const float* __restrict__ gate_logit, int d, int k, float eps,
@@ -1844,7 +1847,7 @@ int combine_stamped(cudaStream_t st, float* h, float* x, const float* y, const i
                     const float* wts, const float* ys, const float* gate_logit, int B, int d, int k,
                     float eps, unsigned long long* stamp) {
   if (B == 0) return EF_OK;
-  combine_kernel<<<B, 1024, 0, st>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps, stamp);
+  combine_kernel<<<B, 256, 0, st>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps, stamp);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -1855,7 +1858,7 @@ extern "C" int ef_combine(void* stream, float* h, float* x, const float* y, cons
                           int d, int k, float eps) {
   EF_CHECK_ARG(B >= 0 && d > 0 && k >= 1, "bad combine shape");
   if (B == 0) return EF_OK;
-  combine_kernel<<<B, 1024, 0, S(stream)>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps, nullptr);
+  combine_kernel<<<B, 256, 0, S(stream)>>>(h, x, y, inv, wts, ys, gate_logit, d, k, eps, nullptr);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -1889,14 +1892,14 @@ static void preload_dtype(int& n) {
   preload(ffn_stream_kernel<WT, 2>, n);
   preload(ffn_stream_kernel<WT, 4>, n);
   preload(ffn_stream_kernel<WT, 8>, n);
-  preload(ffn_gemv_kernel<WT, 1, 4, true, XGather<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 2, 4, true, XGather<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 4, 4, true, XGather<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 8, 4, true, XGather<WT>>, n);
-  preload(ffn_gemv_kernel<WT, 1, 1, false, XAct<WT>, 4>, n);
-  preload(ffn_gemv_kernel<WT, 2, 1, false, XAct<WT>, 4>, n);
-  preload(ffn_gemv_kernel<WT, 4, 1, false, XAct<WT>, 4>, n);
-  preload(ffn_gemv_kernel<WT, 8, 1, false, XAct<WT>, 4>, n);
+  preload(ffn_gemv_kernel<WT, 1, kUpR, true, XGather<WT>, kUpU>, n);
+  preload(ffn_gemv_kernel<WT, 2, kUpR, true, XGather<WT>, kUpU>, n);
+  preload(ffn_gemv_kernel<WT, 4, kUpR, true, XGather<WT>, kUpU>, n);
+  preload(ffn_gemv_kernel<WT, 8, kUpR, true, XGather<WT>, kUpU>, n);
+  preload(ffn_gemv_kernel<WT, 1, kDnR, false, XAct<WT>, kDnU>, n);
+  preload(ffn_gemv_kernel<WT, 2, kDnR, false, XAct<WT>, kDnU>, n);
+  preload(ffn_gemv_kernel<WT, 4, kDnR, false, XAct<WT>, kDnU>, n);
+  preload(ffn_gemv_kernel<WT, 8, kDnR, false, XAct<WT>, kDnU>, n);
 }
 
 int preload_pipeline_kernels() {

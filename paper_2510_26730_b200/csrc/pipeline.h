@@ -62,8 +62,8 @@ int combine_stamped(cudaStream_t st, float* h, float* x, const float* y, const i
                     const float* wts, const float* ys, const float* gate_logit, int B, int d, int k,
                     float eps, unsigned long long* stamp);
 // Fused decode pipeline (default for the split FFN): router + route in one
-// kernel (the last CTA routes), gate folded into the up kernel, combine +
-// next rmsnorm folded into the down kernel's last CTA when counter != null.
+// kernel (the last CTA routes; optionally the previous layer's combine +
+// rmsnorm first), gate folded into the up kernel.
 // The previous layer's combine, folded into router_route_fused (x is then
 // both the router input and, rewritten by the last CTA, the layer's x).
 struct CombineIn {
@@ -84,7 +84,5 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
 int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                      int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
-                     int max_rows, int d, int ff, int dtype, void* act, float* y, int* counter,
-                     float* h, float* xnext, const int32_t* inv, const float* wts, const float* ys,
-                     const float* gate_logit, int B, float eps);
+                     int max_rows, int d, int ff, int dtype, void* act, float* y);
 }  // namespace ef
