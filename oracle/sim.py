@@ -342,6 +342,9 @@ class OracleStepper:
             self.pre_layer_hook(0, set(self.cache.tier))
         if self.tokens_run == 0:
             self._start(tt)
+        # the reference's no-progress guard (:299) lives for one trace = one
+        # token; a multi-token decode run re-arms it per token
+        self.miss_guard = 0
         self.predicted: Dict[int, tuple] = {}
         self.horizons: List[_Horizon] = []
         self.horizon_by_expert: Dict[tuple, _Horizon] = {}

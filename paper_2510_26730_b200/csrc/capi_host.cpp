@@ -1,6 +1,7 @@
 // capi_host.cpp — extern "C" boundary for the host-side decision path
 // (include/expertflow.h).  Status codes instead of exceptions; a
 // thread-local message for ef_last_error().
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
@@ -112,8 +113,10 @@ extern "C" int ef_cache_admit(ef_cache* c, int32_t layer, int32_t expert, int ti
 extern "C" int ef_cache_reassign_tiers(ef_cache* c, const int32_t* pred, int n_pred,
                                        int64_t window, int64_t now) {
   EF_TRY({
-    std::set<uint64_t> s;
-    for (int i = 0; i < n_pred; ++i) s.insert(eid_key(pred[2 * i], pred[2 * i + 1]));
+    std::vector<uint64_t> s;
+    for (int i = 0; i < n_pred; ++i) s.push_back(eid_key(pred[2 * i], pred[2 * i + 1]));
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
     c->c.reassign_tiers(s, window, now);
   });
 }

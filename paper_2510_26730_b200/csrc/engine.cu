@@ -124,6 +124,18 @@ struct ef_engine {
   static constexpr uint32_t kSeqRing = 1u << 16;  // pinned sources of the ready-flag copies
   uint32_t* seq_ring = nullptr;
   std::vector<unsigned long long> stats_h;
+  // timing: each step's stats are copied asynchronously into a pinned buffer
+  // (double-buffered) and folded in one step later, so timing never adds a
+  // host sync at the end of a step
+  unsigned long long* stats_pin[2] = {nullptr, nullptr};
+  cudaEvent_t tev[2][3] = {};  // begin, end, stats copied
+  int stats_buf = 0, stats_pending = -1;
+  int64_t stats_copies[2] = {0, 0}, copies_at_step = 0;
+  void fold_stats(int i);
+  void flush_stats() {
+    if (stats_pending >= 0) fold_stats(stats_pending);
+    stats_pending = -1;
+  }
   std::vector<char*> store;  // per layer: M * stride bytes
   cudaStream_t copy_stream = nullptr, side_stream = nullptr;
   // slot table
@@ -312,6 +324,11 @@ void ef_engine::init_weights() {
 ef_engine::~ef_engine() {
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   cudaDeviceSynchronize();
+  for (int i = 0; i < 2; ++i) {
+    if (stats_pin[i]) cudaFreeHost(stats_pin[i]);
+    for (int j = 0; j < 3; ++j)
+      if (tev[i][j]) cudaEventDestroy(tev[i][j]);
+  }
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
@@ -372,7 +389,7 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
                              mask[1], sel_d, wts_d, counts_d, offsets_d, perm_d, inv_d, nullptr,
                              dev_of(out_sel(l)), dev_of(out_logits(l)),
                              const_cast<uint32_t*>(&dev_of(out(l))->done),
-                             stats_d + kStats * l + 6));
+                             stats_d + kStats * l + 6, R * B * M));
     ++launches;
   }
   if (cfg.shared_ff) {  // always resident: runs while the host decides the layer
@@ -467,11 +484,16 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
   if (B < 1 || B > cfg.max_batch) throw ValueError("batch size outside [1, max_batch]");
   std::vector<int64_t> tokens = tokens_in;
   if (tokens.empty()) tokens.push_back(-(int64_t)(steps + 1));  // unique prediction-cache key
-  cudaEvent_t t_begin = nullptr, t_end = nullptr;
   if (cfg.timing) {
-    CK(cudaEventCreate(&t_begin));
-    CK(cudaEventCreate(&t_end));
-    CK(cudaEventRecord(t_begin, stream));
+    if (!stats_pin[0]) {
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaHostAlloc(&stats_pin[i], sizeof(unsigned long long) * kStats * L,
+                         cudaHostAllocDefault));
+        for (int j = 0; j < 3; ++j) CK(cudaEventCreate(&tev[i][j]));
+      }
+    }
+    CK(cudaEventRecord(tev[stats_buf][0], stream));
+    copies_at_step = copies;
   }
   cur_h = h;
   CKS(launch_init_stats(stream, stats_d, L));
@@ -536,30 +558,16 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       }
       for (int e = 0; e < M; ++e)
         if (cnt[e]) r.actual.push_back(e);
-      bool fetched = false;
-      auto fetch_rows = [&]() {
-        if (fetched || R <= 1) return;
-        CK(cudaMemcpyAsync(logits_h + (int64_t)B * M, logits_d + (int64_t)B * M,
-                           (size_t)(R - 1) * B * M * sizeof(float), cudaMemcpyDeviceToHost,
-                           side_stream));
-        CK(cudaStreamSynchronize(side_stream));
-        d2h_bytes += (int64_t)(R - 1) * B * M * 4;
-        fetched = true;
-      };
-      hooks->pregate_fn = [&, R](int layer, int hz, double* o) {
+      // the route kernel published every scored row (pre-gate rows included)
+      d2h_bytes += (int64_t)(B * k + R * B * M) * 4;
+      hooks->pregate_fn = [&, R, lg0](int layer, int hz, double* o) {
         if (hz >= R) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
-        fetch_rows();
         uint64_t m[2];
         residency_mask(layer + hz, m);
-        batch_gate(logits_h + (int64_t)hz * B * M, B, M, cfg.routing_bias, m, o);
+        batch_gate(lg0 + (int64_t)hz * B * M, B, M, cfg.routing_bias, m, o);
       };
       if (cfg.record_routing) {
-        fetch_rows();
-        std::vector<float> lg((int64_t)R * B * M);
-        std::memcpy(lg.data(), lg0, sizeof(float) * B * M);
-        if (R > 1)
-          std::memcpy(lg.data() + (int64_t)B * M, logits_h + (int64_t)B * M,
-                      sizeof(float) * (R - 1) * B * M);
+        std::vector<float> lg(lg0, lg0 + (int64_t)R * B * M);
         rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(sel, sel + B * k), R, B,
                                   cur_mask[0], cur_mask[1]});
       }
@@ -615,43 +623,51 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
     st->end_token();
   } catch (...) {
     abort_pipeline(stream, l, enq);
-    if (t_begin) cudaEventDestroy(t_begin);
-    if (t_end) cudaEventDestroy(t_end);
     throw;
   }
   host_ms += host_acc;
   ++steps;
   if (cfg.timing) {
-    CK(cudaEventRecord(t_end, stream));
-    CK(cudaEventSynchronize(t_end));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, t_begin, t_end));
-    step_ms += ms;
-    CK(cudaMemcpy(stats_h.data(), stats_d, sizeof(unsigned long long) * kStats * L,
-                  cudaMemcpyDeviceToHost));
-    static const bool dump = getenv("EF_STATS_DUMP") != nullptr;
-    for (int j = 0; j < L; ++j) {
-      const unsigned long long* sj = &stats_h[kStats * j];
-      stall_ms += sj[2] * 1e-6;
-      if (sj[1] >= sj[0]) bubble_ms += (sj[1] - sj[0]) * 1e-6;
-      if (sj[3] != ~0ull && sj[4] > sj[3]) ffn_ms += (sj[4] - sj[3]) * 1e-6;
-      if (dump) {  // per-layer device timeline (us)
-        auto us = [](unsigned long long a, unsigned long long b) {
-          return ((double)b - (double)a) * 1e-3;
-        };
-        fprintf(stderr,
-                "layer %2d router %5.1f route %5.1f pub->gate %5.1f wait %6.1f gate %5.1f "
-                "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f\n",
-                j, us(sj[7], sj[6]), us(sj[6], sj[9]), us(sj[9], sj[0]), us(sj[0], sj[1]),
-                us(sj[1], sj[8]), sj[10] != ~0ull ? us(sj[8], sj[10]) : 0.0,
-                sj[3] != ~0ull && sj[10] != ~0ull ? us(sj[10], sj[3]) : 0.0,
-                sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0, sj[2] * 1e-3, us(sj[4], sj[5]),
-                j + 1 < L ? us(sj[7], stats_h[kStats * (j + 1) + 7]) : 0.0);
-      }
-    }
-    cudaEventDestroy(t_begin);
-    cudaEventDestroy(t_end);
+    const int i = stats_buf;
+    CK(cudaEventRecord(tev[i][1], stream));
+    CK(cudaMemcpyAsync(stats_pin[i], stats_d, sizeof(unsigned long long) * kStats * L,
+                       cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(tev[i][2], stream));
+    stats_copies[i] = copies - copies_at_step;
+    if (stats_pending >= 0) fold_stats(stats_pending);  // the previous step: long done
+    stats_pending = i;
+    stats_buf ^= 1;
   }
+}
+
+void ef_engine::fold_stats(int i) {
+  const int L = cfg.L;
+  CK(cudaEventSynchronize(tev[i][2]));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, tev[i][0], tev[i][1]));
+  step_ms += ms;
+  std::memcpy(stats_h.data(), stats_pin[i], sizeof(unsigned long long) * kStats * L);
+  static const bool dump = getenv("EF_STATS_DUMP") != nullptr;
+  for (int j = 0; j < L; ++j) {
+    const unsigned long long* sj = &stats_h[kStats * j];
+    stall_ms += sj[2] * 1e-6;
+    if (sj[1] >= sj[0]) bubble_ms += (sj[1] - sj[0]) * 1e-6;
+    if (sj[3] != ~0ull && sj[4] > sj[3]) ffn_ms += (sj[4] - sj[3]) * 1e-6;
+    if (dump) {  // per-layer device timeline (us)
+      auto us = [](unsigned long long a, unsigned long long b) {
+        return ((double)b - (double)a) * 1e-3;
+      };
+      fprintf(stderr,
+              "layer %2d router %5.1f route %5.1f pub->gate %5.1f wait %6.1f gate %5.1f "
+              "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f\n",
+              j, us(sj[7], sj[6]), us(sj[6], sj[9]), us(sj[9], sj[0]), us(sj[0], sj[1]),
+              us(sj[1], sj[8]), sj[10] != ~0ull ? us(sj[8], sj[10]) : 0.0,
+              sj[3] != ~0ull && sj[10] != ~0ull ? us(sj[10], sj[3]) : 0.0,
+              sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0, sj[2] * 1e-3, us(sj[4], sj[5]),
+              j + 1 < L ? us(sj[7], stats_h[kStats * (j + 1) + 7]) : 0.0);
+    }
+  }
+  if (dump) fprintf(stderr, "step device time %.3f ms copies %lld\n", ms, (long long)stats_copies[i]);
 }
 
 extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
@@ -723,7 +739,8 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     std::memset((void*)e->hctrl, 0, sizeof(HostCtrl) * L);
     CK(cudaHostGetDevicePointer((void**)&e->hctrl_dev, e->hctrl, 0));
     e->out_stride =
-        ((int64_t)sizeof(HostOut) + (int64_t)B * k * 4 + (int64_t)B * M * 4 + 127) / 128 * 128;
+        ((int64_t)sizeof(HostOut) + (int64_t)B * k * 4 + (int64_t)e->Rmax * B * M * 4 + 127) / 128 *
+        128;
     CK(cudaHostAlloc(&e->hout, e->out_stride * L, cudaHostAllocMapped));
     std::memset(e->hout, 0, e->out_stride * L);
     CK(cudaHostGetDevicePointer((void**)&e->hout_dev, e->hout, 0));
@@ -795,6 +812,7 @@ extern "C" int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len,
 
 extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   EF_TRY({
+    e->flush_stats();
     double v[16] = {(double)e->steps,         (double)e->copies,
                     (double)e->copy_bytes,    e->stall_ms,
                     (double)e->P,             (double)e->st->cache().capacity(),

@@ -312,7 +312,7 @@ __device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int 
                            int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
                            int32_t* __restrict__ perm, int32_t* __restrict__ inv,
                            const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
-                           volatile uint32_t* host_done, unsigned long long* stamp) {
+                           volatile uint32_t* host_done, unsigned long long* stamp, int n_pub) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (stamp && tid == 0) *stamp = gtimer();
   if (mask_src) {  // mask in mapped host memory: one PCIe read, broadcast through smem
@@ -447,10 +447,11 @@ __device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int 
   __syncthreads();
   for (int f = tid; f < N; f += blockDim.x) perm[inv[f]] = f;
   if (host_done && wid == 0) {
-    // publish the selection and row-0 logits to mapped host memory from one
+    // publish the selection and the logits rows (row 0 = this layer, rows
+    // 1.. = pre-gate scores of later layers) to mapped host memory from one
     // warp: a system-scope fence costs microseconds per warp that issues it
     for (int f = lane; f < N; f += 32) host_sel[f] = sel[f];
-    for (int i = lane; i < B * M; i += 32) host_logits[i] = logits[i];
+    for (int i = lane; i < n_pub; i += 32) host_logits[i] = __ldcg(logits + i);
     __threadfence_system();
     __syncwarp();
     if (lane == 0) {
@@ -465,10 +466,10 @@ __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
     uint64_t mhi, int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts,
     int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv,
     const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
-    volatile uint32_t* host_done, unsigned long long* stamp) {
+    volatile uint32_t* host_done, unsigned long long* stamp, int n_pub) {
   __shared__ RouteSmem sm;
   route_body(sm, logits, B, M, k, mode, bias, mlo, mhi, sel, wts, counts, offsets, perm, inv,
-             mask_src, host_sel, host_logits, host_done, stamp);
+             mask_src, host_sel, host_logits, host_done, stamp, n_pub);
 }
 
 // Engine decode path: router GEMV rows, then the last CTA to finish runs
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   }
   route_body(sm, logits, B, M, ra.k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.sel, ra.wts, ra.counts,
              ra.offsets, ra.perm, ra.inv, nullptr, ra.host_sel, ra.host_logits, ra.host_done,
-             ra.stamp_route);
+             ra.stamp_route, rows * B);
   if (threadIdx.x == 0) *ra.counter = 0;  // ready for the next launch
 }
 
@@ -659,7 +660,7 @@ extern "C" int ef_route_permute(void* stream, const float* logits, int B, int M,
   route_permute_kernel<<<1, kRouteThreads, 0, S(stream)>>>(logits, B, M, k, mode, bias, mlo, mhi,
                                                            sel, wts, counts, offsets, perm, inv,
                                                            nullptr, nullptr, nullptr, nullptr,
-                                                           nullptr);
+                                                           nullptr, 0);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -1785,11 +1786,11 @@ int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int
                          float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
                          int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                          const void* mask_src, int32_t* host_sel, float* host_logits,
-                         uint32_t* host_done, unsigned long long* stamp) {
+                         uint32_t* host_done, unsigned long long* stamp, int n_pub) {
   route_permute_kernel<<<1, kRouteThreads, 0, st>>>(
       logits, B, M, k, mode, bias, mlo, mhi, sel, wts, counts, offsets, perm, inv,
       reinterpret_cast<const volatile uint64_t*>(mask_src), host_sel, host_logits, host_done,
-      stamp);
+      stamp, n_pub);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }

@@ -55,7 +55,7 @@ int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int
                          float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
                          int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                          const void* mask_src, int32_t* host_sel, float* host_logits,
-                         uint32_t* host_done, unsigned long long* stamp);
+                         uint32_t* host_done, unsigned long long* stamp, int n_pub);
 int router_logits_stamped(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
                           int d, int M, float* logits, unsigned long long* stamp);
 int combine_stamped(cudaStream_t st, float* h, float* x, const float* y, const int32_t* inv,

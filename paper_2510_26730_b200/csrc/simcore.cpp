@@ -202,8 +202,9 @@ std::vector<uint64_t> ExpertCache::admit(uint64_t k, int tier, int64_t now) {
   return victims;
 }
 
-void ExpertCache::reassign_tiers(const std::set<uint64_t>& predicted, int64_t window,
+void ExpertCache::reassign_tiers(const std::vector<uint64_t>& predicted, int64_t window,
                                  int64_t now) {
+  // predicted: sorted, unique keys
   // memory.py:137-156: global touch order, then split by the new tier.
   if (window < 0) throw ValueError("recent_window must be >= 0");
   std::vector<Node*> order;
@@ -222,7 +223,8 @@ void ExpertCache::reassign_tiers(const std::set<uint64_t>& predicted, int64_t wi
   lists_[kLow] = List{};
   lists_[kHigh] = List{};
   for (Node* n : order) {
-    bool hot = predicted.count(n->key) || (now - n->last < window);
+    bool hot = (now - n->last < window) ||
+               std::binary_search(predicted.begin(), predicted.end(), n->key);
     n->prev = n->next = nullptr;
     append(n, hot ? kHigh : kLow);
   }
@@ -761,6 +763,7 @@ void Stepper::begin_token(const std::vector<int64_t>& tokens,
                           const std::vector<int64_t>& group_sizes, const LayerRouting& layer0) {
   tokens_ = tokens;
   group_sizes_ = group_sizes;
+  miss_guard_ = 0;  // engine.py:299's guard covers one trace (one token); re-armed per token
   if (tokens_run_ == 0) {
     const Policy& p = cfg_.policy;
     if (p.strategy == 3) {  // engine.py:545-563
@@ -815,9 +818,15 @@ void Stepper::run_layer(int l, const LayerRouting& r) {
   auto pit = predicted_.find(l);
   if (pit != predicted_.end()) {  // engine.py:585-596
     const std::vector<int>& pred = pit->second.first;
-    std::set<int> a(r.actual.begin(), r.actual.end());
+    // |set(pred) & set(actual)| and |set(actual)| with expert bit masks (M <= 128
+    // on the engine path; wider models fall back to sorted vectors)
+    std::vector<int> a(r.actual.begin(), r.actual.end()), pv(pred.begin(), pred.end());
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+    std::sort(pv.begin(), pv.end());
+    pv.erase(std::unique(pv.begin(), pv.end()), pv.end());
     int sel = 0;
-    for (int e : std::set<int>(pred.begin(), pred.end())) sel += a.count(e);
+    for (int e : pv) sel += std::binary_search(a.begin(), a.end(), e);
     n_selected_ += sel;
     n_total_ += (int64_t)a.size();
     samples_.push_back(SampleRec{tokens_, l, pred, r.actual, pit->second.second});
@@ -882,11 +891,13 @@ void Stepper::run_layer(int l, const LayerRouting& r) {
   }
   if (cfg_.policy.strategy == 3) {  // engine.py:631-644
     int64_t window = cfg_.policy.recent_window >= 0 ? cfg_.policy.recent_window : state_.current;
-    std::set<uint64_t> hot;
+    hot_scratch_.clear();
     for (auto& kv : predicted_)
       if (kv.first > l)
-        for (int e : kv.second.first) hot.insert(eid_key(kv.first, e));
-    cache_.reassign_tiers(hot, window, now_);
+        for (int e : kv.second.first) hot_scratch_.push_back(eid_key(kv.first, e));
+    std::sort(hot_scratch_.begin(), hot_scratch_.end());
+    hot_scratch_.erase(std::unique(hot_scratch_.begin(), hot_scratch_.end()), hot_scratch_.end());
+    cache_.reassign_tiers(hot_scratch_, window, now_);
   }
   if (cfg_.emit_events) emit(chain, kLayerEnd, "layer=" + std::to_string(l));
   LayerRecord rec;

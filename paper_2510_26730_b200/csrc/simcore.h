@@ -81,7 +81,7 @@ class ExpertCache {
   bool access(uint64_t k, int64_t now);
   // returns victims in eviction order
   std::vector<uint64_t> admit(uint64_t k, int tier, int64_t now);
-  void reassign_tiers(const std::set<uint64_t>& predicted, int64_t window, int64_t now);
+  void reassign_tiers(const std::vector<uint64_t>& predicted_sorted, int64_t window, int64_t now);
   int tier_of(uint64_t k) const;  // -1 absent
   int64_t last_access(uint64_t k) const;
   std::vector<uint64_t> resident_sorted() const;
@@ -312,6 +312,7 @@ class Stepper {
   int tokens_run() const { return tokens_run_; }
 
  private:
+  std::vector<uint64_t> hot_scratch_;
   struct Inflight {
     uint64_t key;
     int prio;
