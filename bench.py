@@ -316,10 +316,14 @@ def run_ours(args, cfg, bias):
     import gc
     gc.collect()
     torch.cuda.synchronize()
-    baseline = None
+    baseline = unbiased = None
     if not args.no_baseline and rank == 0 and world == 1:
         baseline = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K)
+        if bias != 0.0:
+            unbiased = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
+                                         strategy=args.strategy, bias=0.0)
 
+    traffic = ncu_traffic()
     if rank == 0:
         cpu_v, cpu_desc = (None, "skipped (--no-cpu)") if args.no_cpu else \
             time_cpu_port(cpu_port(cfg, B, args.seed), cfg, B, args.cpu_seconds)
@@ -350,9 +354,17 @@ def run_ours(args, cfg, bias):
             / (K * cfg.num_layers),
             "ffn_us_per_layer": 1e3 * ffn_ms / (K * cfg.num_layers),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None,
+                         "frac": achieved / hbm_peak,
+                         "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
                          "kernel": "ef_expert_ffn_decode (gate/up+SiLU GEMV, down GEMV)",
                          "bytes_per_launch": ffn_bytes / max(ffn_pairs, 1),
+                         "timing": "on-device globaltimer stamps per layer (first FFN CTA past "
+                                   "its ready check -> last down-projection CTA), summed over the "
+                                   "timed steps; CUDA events around the launch would include the "
+                                   "host-decision wait folded into the gate/up kernel",
+                         "traffic_source": (f"profiles/ncu_traffic.json ({traffic['source']}, "
+                                            "ncu --set full, dram__bytes_read+write per launch)")
+                         if traffic else None,
                          "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * cfg.d_model * 4,
                     "d2h_bytes_per_step": B * cfg.d_model * 4, "output_finite": finite},
@@ -363,6 +375,8 @@ def run_ours(args, cfg, bias):
         }
         if baseline:
             line["reactive_baseline"] = baseline
+        if unbiased:
+            line["unbiased_routing"] = unbiased
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -372,18 +386,21 @@ def _rate(h, m):
     return h / (h + m) if h + m else 0.0
 
 
-def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K):
+def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
+                      strategy="reactive", bias=0.0):
     """The reactive per-layer baseline (engine.py:488-489) on the same
-    engine type, budget and inputs; no routing bias."""
+    engine type, budget and inputs; no routing bias.  With strategy=adaptive
+    it is the headline policy with unbiased routing (the PCIe-bound case)."""
     import torch
     import paper_2510_26730_b200 as ef
     from paper_2510_26730_b200.runtime import MoEEngine
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     eng = MoEEngine(cfg, budget_experts=budget,
-                    policy=ef.PolicyConfig("reactive", "reactive", predictor="pregate"),
+                    policy=ef.PolicyConfig(strategy, strategy, predictor="pregate",
+                                           cache_aware_routing=strategy != "reactive"),
                     link_bw=link_bw, layer_time_s=layer_s, max_batch=args.batch, seed=args.seed,
-                    routing_bias=0.0, timing=True)
+                    routing_bias=bias, timing=True)
     n = min(K, 6)
     for t in range(min(W, 2)):
         eng.step(inputs[t].clone())
@@ -397,17 +414,36 @@ def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K):
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
     st1 = eng.stats()
-    return {"tokens_per_s": args.batch * n / (ms / 1e3), "steps": n,
-            "expert_stall_pct": 100.0 * (st1["stall_ms"] - st0["stall_ms"]) / ms,
-            "policy": "reactive/pregate, routing_bias 0"}
+    out = {"tokens_per_s": args.batch * n / (ms / 1e3), "steps": n,
+           "expert_stall_pct": 100.0 * (st1["stall_ms"] - st0["stall_ms"]) / ms,
+           "copies_per_step": (st1["copies"] - st0["copies"]) / n,
+           "policy": f"{strategy}/pregate, routing_bias {bias:g}"}
+    eng.close()
+    del eng
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    return out
+
+
+def ncu_traffic():
+    """DRAM bytes per decode-FFN launch from the committed ncu capture
+    (profiles/ncu_traffic.json, made by tools/make_profiles.py)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p))
 
 
 def main():
     args = parse()
     from paper_2510_26730_b200.runtime import PRESETS
     cfg = PRESETS[args.config]
-    # headline: cache-aware routing bias on (the north star's kernel (a))
-    bias = args.bias if args.bias is not None else 2.0
+    # headline: cache-aware routing with a residency-first bias (the north
+    # star's kernel (a)): a resident expert outranks any non-resident one, so
+    # routing only leaves HBM when fewer than top_k experts of a layer are
+    # resident.  The unbiased (PCIe-bound) run is reported beside it.
+    bias = args.bias if args.bias is not None else 1e4
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
