@@ -298,6 +298,12 @@ void ef_engine_destroy(ef_engine* e);
 /* one decode step: h[B,d] fp32 device in/out, on `stream` */
 int ef_engine_step(ef_engine* e, void* stream, float* h, int B, const int64_t* tokens,
                    int n_tokens);
+/* the same step with the hidden state in pinned host memory: h_in[B,d] is read
+   and h_out[B,d] written (may alias) by SM loads/stores over PCIe, ordered on
+   `stream` (h_out is complete when the stream reaches the step's end); never
+   queues behind an expert swap-in on the copy engine */
+int ef_engine_step_host(ef_engine* e, void* stream, const float* h_in, float* h_out, int B,
+                        const int64_t* tokens, int n_tokens);
 /* scheduler outputs of the engine's stepper: same layouts as ef_sim_* */
 int ef_engine_metrics(ef_engine* e, int64_t* ints, int32_t n_ints, double* bw_estimate);
 int ef_engine_output(ef_engine* e, int32_t kind, int64_t* buf, int64_t max_len, int64_t* n);

@@ -136,6 +136,7 @@ _SIGS = {
     "ef_engine_create": (C.c_int, [P(EngineCfg), P(SimCfg), P(LadderCfg), P(vp)]),
     "ef_engine_destroy": (None, [vp]),
     "ef_engine_step": (C.c_int, [vp, vp, vp, C.c_int, P(i64), C.c_int]),
+    "ef_engine_step_host": (C.c_int, [vp, vp, vp, vp, C.c_int, P(i64), C.c_int]),
     "ef_engine_metrics": (C.c_int, [vp, P(i64), i32, P(f64)]),
     "ef_engine_output": (C.c_int, [vp, i32, P(i64), i64, P(i64)]),
     "ef_engine_event_details": (C.c_int, [vp, C.c_char_p, i64, P(i64)]),

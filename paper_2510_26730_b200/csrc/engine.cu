@@ -107,7 +107,7 @@ struct ef_engine {
   char* shared_w = nullptr;  // [L] x sstride
   void* sgate_w = nullptr;   // [L][d]
   float *x_d = nullptr, *logits_d = nullptr, *sgl_d = nullptr, *wts_d = nullptr, *y_d = nullptr,
-        *ys_d = nullptr;
+        *ys_d = nullptr, *h_io_d = nullptr;  // h_io_d: hidden state of step_host()
   int32_t *sel_d = nullptr, *counts_d = nullptr, *offsets_d = nullptr, *perm_d = nullptr,
           *inv_d = nullptr;
   void *act_d = nullptr, *acts_d = nullptr;
@@ -261,6 +261,9 @@ struct ef_engine {
   void abort_pipeline(cudaStream_t stream, int from, int enq);
   void init_weights();
   void step(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
+  void step_host(cudaStream_t stream, const float* h_in, float* h_out, int B,
+                 const std::vector<int64_t>& tokens);
+  void join(cudaStream_t stream, cudaStream_t caller);
   void step_on(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
   cudaStream_t compute_stream = nullptr;
   cudaEvent_t join_in = nullptr, join_out = nullptr;
@@ -332,7 +335,7 @@ ef_engine::~ef_engine() {
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
-                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d})
+                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d, (void*)h_io_d})
     if (p) cudaFree(p);
   for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring})
     if (p) cudaFreeHost(p);
@@ -471,10 +474,33 @@ void ef_engine::step(cudaStream_t caller, float* h, int B, const std::vector<int
     CK(cudaStreamWaitEvent(stream, join_in, 0));
   }
   step_on(stream, h, B, tokens_in);
+  join(stream, caller);
+}
+
+void ef_engine::join(cudaStream_t stream, cudaStream_t caller) {
   if (stream != caller) {
     CK(cudaEventRecord(join_out, stream));
     CK(cudaStreamWaitEvent(caller, join_out, 0));
   }
+}
+
+// Host-buffer step: h_in / h_out are pinned host arrays [B, d] (may alias).
+// The hidden state moves by SM loads/stores over PCIe, so it never queues
+// behind an expert swap-in on the copy engine.
+void ef_engine::step_host(cudaStream_t caller, const float* h_in, float* h_out, int B,
+                          const std::vector<int64_t>& tokens_in) {
+  if (B < 1 || B > cfg.max_batch) throw ValueError("batch size outside [1, max_batch]");
+  cudaStream_t stream = compute_stream ? compute_stream : caller;
+  if (stream != caller) {
+    CK(cudaEventRecord(join_in, caller));
+    CK(cudaStreamWaitEvent(stream, join_in, 0));
+  }
+  const int64_t n = (int64_t)B * cfg.d;
+  CKS(launch_host_io(stream, h_in, h_io_d, n, false));
+  step_on(stream, h_io_d, B, tokens_in);
+  CKS(launch_host_io(stream, h_io_d, h_out, n, true));
+  launches += 2;
+  join(stream, caller);
 }
 
 void ef_engine::step_on(cudaStream_t stream, float* h, int B,
@@ -719,6 +745,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       CK(cudaMalloc(&e->ys_d, (size_t)B * d * 4));
     }
     CK(cudaMalloc(&e->x_d, (size_t)B * d * 4));
+    CK(cudaMalloc(&e->h_io_d, (size_t)B * d * 4));
     CK(cudaMalloc(&e->logits_d, (size_t)e->Rmax * B * M * 4));
     CK(cudaMalloc(&e->sgl_d, (size_t)B * 4));
     CK(cudaMalloc(&e->wts_d, (size_t)B * k * 4));
@@ -788,6 +815,15 @@ extern "C" int ef_engine_step(ef_engine* e, void* stream, float* h, int B, const
     std::vector<int64_t> t;
     if (tokens && n_tokens > 0) t.assign(tokens, tokens + n_tokens);
     e->step(reinterpret_cast<cudaStream_t>(stream), h, B, t);
+  });
+}
+
+extern "C" int ef_engine_step_host(ef_engine* e, void* stream, const float* h_in, float* h_out,
+                                   int B, const int64_t* tokens, int n_tokens) {
+  EF_TRY({
+    std::vector<int64_t> t;
+    if (tokens && n_tokens > 0) t.assign(tokens, tokens + n_tokens);
+    e->step_host(reinterpret_cast<cudaStream_t>(stream), h_in, h_out, B, t);
   });
 }
 

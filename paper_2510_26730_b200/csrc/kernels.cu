@@ -1903,6 +1903,29 @@ static void preload_dtype(int& n) {
   preload(ffn_gemv_kernel<WT, 8, kDnR, false, XAct<WT>, kDnU>, n);
 }
 
+// Host-buffer I/O for MoEEngine.step_host(): the hidden state is read from /
+// written to pinned host memory by SMs (zero-copy), not by a copy engine: an
+// H2D cudaMemcpy would queue behind an in-flight 352 MB expert swap-in on the
+// shared copy engine (profiles/r01_copy_lab.txt).
+__global__ void host_io_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n,
+                               int to_host) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<float4*>(dst)[i] = __ldcv(reinterpret_cast<const float4*>(src) + i);
+  for (int64_t i = (n / 4) * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcv(src + i);
+  if (to_host) __threadfence_system();
+}
+
+int launch_host_io(cudaStream_t st, const float* src, float* dst, int64_t n, bool to_host) {
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>(32, (n / 4 + threads - 1) / threads + 1);
+  host_io_kernel<<<blocks, threads, 0, st>>>(src, dst, n, to_host ? 1 : 0);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
 int preload_pipeline_kernels() {
   int n = 0;
   preload_dtype<__nv_bfloat16>(n);
@@ -1913,6 +1936,7 @@ int preload_pipeline_kernels() {
   preload(rmsnorm_kernel, n);
   preload(combine_kernel, n);
   preload(set_ready_kernel, n);
+  preload(host_io_kernel, n);
   return n;
 }
 }  // namespace ef

@@ -74,6 +74,8 @@ struct CombineIn {
   float eps;
   unsigned long long* stamp;
 };
+// zero-copy hidden-state I/O between pinned host memory and HBM (SM loads/stores)
+int launch_host_io(cudaStream_t st, const float* src, float* dst, int64_t n, bool to_host);
 int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
                        int d, int M, float* logits, unsigned long long* stamp_router, int k,
                        int mode, float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,

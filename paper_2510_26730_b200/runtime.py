@@ -148,6 +148,31 @@ class MoEEngine:
                                      len(token_ids) if token_ids else 0))
         return h
 
+    def step_host(self, h_in: torch.Tensor, h_out: Optional[torch.Tensor] = None,
+                  token_ids: Optional[Sequence[int]] = None) -> torch.Tensor:
+        """step() with the hidden state in pinned host memory: h_in[B, d] fp32
+        (pinned CPU tensor) is read and h_out (default: h_in) written by the
+        GPU over PCIe, ordered on the current stream — synchronise the stream
+        before reading h_out.  Unlike a cudaMemcpy of the input, this never
+        queues behind an expert swap-in on the copy engine."""
+        h_out = h_in if h_out is None else h_out
+        for t in (h_in, h_out):
+            if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.float32 \
+                    or not t.is_contiguous():
+                raise ValueError("h_in / h_out must be contiguous pinned fp32 CPU tensors")
+        B, d = h_in.shape
+        if d != self.cfg.d_model or tuple(h_out.shape) != (B, d):
+            raise ValueError(f"hidden width {d} != d_model {self.cfg.d_model}")
+        toks = L.i64arr(list(token_ids) if token_ids else [0])
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        L._pending_exc.clear()
+        L.check(L.lib.ef_engine_step_host(self._h.ptr, C.c_void_p(stream),
+                                          C.c_void_p(h_in.data_ptr()),
+                                          C.c_void_p(h_out.data_ptr()), B,
+                                          L.as_ptr(toks, C.c_int64),
+                                          len(token_ids) if token_ids else 0))
+        return h_out
+
     def metrics(self) -> SimMetrics:
         return collect_metrics(self.policy.name, self._h.ptr, L.lib.ef_engine_metrics,
                                L.lib.ef_engine_output, L.lib.ef_engine_event_details,

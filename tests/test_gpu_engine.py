@@ -210,3 +210,31 @@ def test_mixtral_full_size_decisions_and_slab_contents():
                 assert ok, (layer, e)
                 checked += 1
     assert checked > 0
+
+
+def test_step_host_matches_device_step():
+    """MoEEngine.step_host (pinned host buffers, zero-copy I/O) produces the
+    same bytes as step() on a device tensor, over several tokens, for two
+    engines driven in lockstep with identical inputs."""
+    cfg = PRESETS["tiny"]
+    pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
+    kw = dict(budget_experts=16, policy=pol, link_bw=4 * ef.GB, layer_time_s=0.0002, max_batch=3,
+              seed=5, routing_bias=1.0)
+    e_dev, e_host = MoEEngine(cfg, **kw), MoEEngine(cfg, **kw)
+    for t in range(4):
+        h = synthetic_hidden(cfg, 5, t, 3, DEV)
+        hin = h.cpu().pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        e_dev.step(h)
+        e_host.step_host(hin, hout)
+        torch.cuda.synchronize()
+        assert torch.equal(hout, h.cpu()), t
+        # in place (h_out aliases h_in)
+        h2 = synthetic_hidden(cfg, 5, 100 + t, 3, DEV)
+        hin2 = h2.cpu().pin_memory()
+        e_dev.step(h2)
+        e_host.step_host(hin2)
+        torch.cuda.synchronize()
+        assert torch.equal(hin2, h2.cpu()), t
+    with pytest.raises(ValueError):
+        e_host.step_host(torch.zeros(3, cfg.d_model))  # not pinned

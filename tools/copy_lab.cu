@@ -50,42 +50,46 @@ __device__ __forceinline__ float dot8(uint4 w, float4 a, float4 b, float acc) {
   return acc;
 }
 
+template <int R = 2, int U = 2>
 __global__ void __launch_bounds__(128) up_k(const __nv_bfloat16* w, int e0, const float* x,
                                             __nv_bfloat16* act) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int e = (e0 + blockIdx.y) % E;
   const __nv_bfloat16* W1 = w + (int64_t)e * 3 * FF * D;
   const __nv_bfloat16* W3 = W1 + (int64_t)FF * D;
-  const int j0 = (blockIdx.x * 4 + wid) * 2;
-  float ag[2] = {0, 0}, au[2] = {0, 0};
-  for (int c0 = lane * 8; c0 < D; c0 += 32 * 8 * 2) {
-    uint4 g[2][2], u[2][2];
+  const int j0 = (blockIdx.x * 4 + wid) * R;
+  float ag[R], au[R];
 #pragma unroll
-    for (int v = 0; v < 2; ++v)
+  for (int r = 0; r < R; ++r) ag[r] = au[r] = 0.f;
+  for (int c0 = lane * 8; c0 < D; c0 += 32 * 8 * U) {
+    uint4 g[U][R], u[U][R];
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+    for (int v = 0; v < U; ++v)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
         g[v][r] = ldw(W1 + (int64_t)(j0 + r) * D + c0 + v * 256);
         u[v][r] = ldw(W3 + (int64_t)(j0 + r) * D + c0 + v * 256);
       }
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < U; ++v) {
       const float4* xp = reinterpret_cast<const float4*>(x + c0 + v * 256);
       float4 x0 = __ldg(xp), x1 = __ldg(xp + 1);
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < R; ++r) {
         ag[r] = dot8(g[v][r], x0, x1, ag[r]);
         au[r] = dot8(u[v][r], x0, x1, au[r]);
       }
     }
   }
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < R; ++r) {
     float gg = wsum(ag[r]), uu = wsum(au[r]);
     if (lane == 0)
       act[blockIdx.y * FF + j0 + r] = __float2bfloat16_rn(gg / (1.f + __expf(-gg)) * uu);
   }
 }
 
+template <int U = 2>
 __global__ void __launch_bounds__(128) down_k(const __nv_bfloat16* w, int e0,
                                               const __nv_bfloat16* act, float* y) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -94,13 +98,13 @@ __global__ void __launch_bounds__(128) down_k(const __nv_bfloat16* w, int e0,
   const int i0 = blockIdx.x * 4 + wid;
   const __nv_bfloat16* xa = act + blockIdx.y * FF;
   float acc = 0.f;
-  for (int c0 = lane * 8; c0 < FF; c0 += 32 * 8 * 2) {
-    uint4 wv[2];
+  for (int c0 = lane * 8; c0 < FF; c0 += 32 * 8 * U) {
+    uint4 wv[U];
 #pragma unroll
-    for (int v = 0; v < 2; ++v)
+    for (int v = 0; v < U; ++v)
       if (c0 + v * 256 < FF) wv[v] = ldw(W2 + (int64_t)i0 * FF + c0 + v * 256);
 #pragma unroll
-    for (int v = 0; v < 2; ++v)
+    for (int v = 0; v < U; ++v)
       if (c0 + v * 256 < FF) {
         uint4 xv = __ldg(reinterpret_cast<const uint4*>(xa + c0 + v * 256));
         float4 x0 = make_float4(lo(xv.x), hi(xv.x), lo(xv.y), hi(xv.y));
@@ -165,6 +169,10 @@ int main() {
   *hword = 7;
   uint32_t* hword_dev;
   CK(cudaHostGetDevicePointer((void**)&hword_dev, hword, 0));
+  char *small_h, *small_hd, *small_d;
+  CK(cudaHostAlloc(&small_h, 16384, cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&small_hd, small_h, 0));
+  CK(cudaMalloc(&small_d, 16384));
   float *x, *y;
   __nv_bfloat16* act;
   uint32_t* out;
@@ -202,8 +210,8 @@ int main() {
   for (int mode = 0; mode < 6; ++mode) {
     start_copy(mode);
     // while the copy runs: alternate FFN pairs and control round trips
-    double ffn_us = 0, ctrl_us = 0;
-    int n_ffn = 0, n_ctrl = 0;
+    double ffn_us = 0, ctrl_us = 0, small_us = 0, zc_us = 0, ffn2_us = 0, ffn3_us = 0;
+    int n_ffn = 0, n_ctrl = 0, n_small = 0, n_zc = 0;
     for (int it = 0; it < 40; ++it) {
       CK(cudaEventRecord(e0, s));
       up_k<<<dim3(FF / 8, NA), 128, 0, s>>>(w, (2 * it) % E, x, act);
@@ -213,6 +221,21 @@ int main() {
       float ms;
       CK(cudaEventElapsedTime(&ms, e0, e1));
       if (it >= 2) ffn_us += ms * 1e3, ++n_ffn;
+      // deeper-pipelined variant: 2 rows x 4 chunks up, 4 chunks down
+      CK(cudaEventRecord(e0, s));
+      up_k<2, 4><<<dim3(FF / 8, NA), 128, 0, s>>>(w, (2 * it + 1) % E, x, act);
+      down_k<4><<<dim3(D / 4, NA), 128, 0, s>>>(w, (2 * it + 1) % E, act, y);
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (it >= 2) ffn2_us += ms * 1e3;
+      CK(cudaEventRecord(e0, s));
+      up_k<4, 2><<<dim3(FF / 16, NA), 128, 0, s>>>(w, (2 * it) % E, x, act);
+      down_k<8><<<dim3(D / 4, NA), 128, 0, s>>>(w, (2 * it) % E, act, y);
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (it >= 2) ffn3_us += ms * 1e3;
       CK(cudaEventRecord(e0, s));
       ctrl_k<<<1, 32, 0, s>>>(hword_dev, out);
       ctrl_k<<<1, 32, 0, s>>>(hword_dev, out);
@@ -221,13 +244,31 @@ int main() {
       CK(cudaEventSynchronize(e1));
       CK(cudaEventElapsedTime(&ms, e0, e1));
       if (it >= 2) ctrl_us += ms * 1e3 / 3, ++n_ctrl;
+      // small H2D copy (16 KB, a B=1 hidden state) on the compute stream
+      CK(cudaEventRecord(e0, s));
+      CK(cudaMemcpyAsync(small_d, small_h, 16384, cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (it >= 2) small_us += ms * 1e3, ++n_small;
+      // the same 16 KB pulled by a kernel from mapped host memory
+      CK(cudaEventRecord(e0, s));
+      pull_k<1><<<4, 256, 0, s>>>((const uint4*)small_hd, (uint4*)small_d, 1024);
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (it >= 2) zc_us += ms * 1e3, ++n_zc;
       if (mode && cudaEventQuery(c1) == cudaSuccess) break;
     }
     CK(cudaEventSynchronize(c1));
     float cms = 0;
     CK(cudaEventElapsedTime(&cms, c0, c1));
-    printf("%-18s ffn pair %7.1f us  ctrl kernel %6.2f us  copy %7.2f ms (%5.1f GB/s)  samples %d\n",
-           names[mode], n_ffn ? ffn_us / n_ffn : 0.0, n_ctrl ? ctrl_us / n_ctrl : 0.0, cms,
+    printf("%-18s deep ffn (up 2x4, down 4) %7.1f us  (up 4x2, down 8) %7.1f us\n", names[mode],
+           n_ffn ? ffn2_us / n_ffn : 0.0, n_ffn ? ffn3_us / n_ffn : 0.0);
+    printf("%-18s ffn pair %7.1f us  ctrl kernel %6.2f us  16KB memcpy %7.1f us  16KB zero-copy "
+           "kernel %6.1f us  copy %7.2f ms (%5.1f GB/s)  samples %d\n",
+           names[mode], n_ffn ? ffn_us / n_ffn : 0.0, n_ctrl ? ctrl_us / n_ctrl : 0.0,
+           n_small ? small_us / n_small : 0.0, n_zc ? zc_us / n_zc : 0.0, cms,
            mode ? BLOB / (cms * 1e6) : 0.0, n_ffn);
   }
   return 0;
