@@ -311,7 +311,9 @@ int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len, int64_t* n
 /* physical counters, in order: steps, copies, copy_bytes, stall_ms, phys_slots,
    logical_capacity, staging_slots, kernel_launches, host_decision_ms, ffn_ms, step_ms,
    preload_copies, d2h_bytes, ffn_bytes (routed expert weight bytes streamed), ffn_launches,
-   gate_wait_ms (GPU time spent waiting for the host's per-layer decision) */
+   gate_wait_ms (GPU time spent waiting for the host's per-layer decision),
+   fast_layers (layers whose routed FFN started from the device-side slot table,
+   without waiting for the host) */
 int ef_engine_stats(ef_engine* e, double* out, int n);
 /* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
    6 perm, 7 inv, 8 y, 9 x */

@@ -165,12 +165,12 @@ struct ef_engine {
     void on_transfer_start(uint64_t key, int) override { e->issue_copy(key, false); }
     void on_admit(uint64_t key) override {
       if (e->inflight_slot < 0) throw RuntimeErr("admit without a landed transfer");
-      e->phys_of[e->idx(key)] = e->inflight_slot;
+      e->set_phys(e->idx(key), e->inflight_slot);
       e->inflight_slot = -1;
     }
     void on_evict(uint64_t key) override {
       int s = e->phys_of[e->idx(key)];
-      e->phys_of[e->idx(key)] = -1;
+      e->set_phys(e->idx(key), -1);
       if (s < 0) return;
       if (e->pinned[s])
         e->deferred_free.push_back(s);
@@ -227,7 +227,7 @@ struct ef_engine {
     copy_bytes += stride;
     if (preload) {
       ++preload_copies;
-      phys_of[idx(key)] = s;
+      set_phys(idx(key), s);
     } else {
       inflight_slot = s;
     }
@@ -249,9 +249,26 @@ struct ef_engine {
   int* counters_d = nullptr;
   // EF_FUSE bit mask: 1 router+route in one kernel, 2 gate folded into the
   // up kernel, 8 combine(l-1) + rmsnorm folded into router_route(l)
-  int fuse = 11;
+  int fuse = 27;
   int* fuse_d = nullptr;  // [0] route counter [2] gate flag
   unsigned gate_seq = 0;
+  std::vector<unsigned> layer_seq;  // gate sequence of each layer's current launch
+  // EF_FUSE bit 16: device-side slot resolution.  The host mirrors phys_of +
+  // fill seq into a mapped table; the fused gate warp of layer l copies row
+  // l+1 into device memory once the host has decided layer l; route(l+1)
+  // resolves its experts from it and, if all are resident, starts FFN(l+1)
+  // without waiting for the host (whose decision still runs, pinning those
+  // slots until FFN(l+1) has finished).
+  int2* host_tab = nullptr;      // [L*M] {slot, fill seq}, mapped pinned
+  int2* host_tab_dev = nullptr;  // device alias
+  int2* dev_tab = nullptr;       // [L*M] device copy, refreshed row by row
+  unsigned* fast_words = nullptr;  // [L]
+  int64_t fast_layers = 0;
+  bool fast_path() const { return (fuse & 16) && (fuse & 3) == 3 && ffn_mode == 2 && !debug; }
+  void set_phys(int64_t i, int s) {
+    phys_of[i] = s;
+    host_tab[i] = make_int2(s, s >= 0 ? (int)slot_seq[s] : 0);
+  }
   float* cur_h = nullptr;  // the step's hidden state (combine-in-router writes it)
   // EF_FUSE bit 8: combine(l-1) folded into router_route(l), small batches
   bool comb_in_router(int l, int B) const {
@@ -335,9 +352,10 @@ ef_engine::~ef_engine() {
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
-                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d, (void*)h_io_d})
+                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d, (void*)h_io_d, (void*)dev_tab,
+                  (void*)fast_words})
     if (p) cudaFree(p);
-  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring})
+  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring, (void*)host_tab})
     if (p) cudaFreeHost(p);
   for (char* p : store)
     if (p) cudaFreeHost(p);
@@ -363,16 +381,19 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
   R = std::max(1, std::min(R, cfg.L - l));
   layer_R[l] = R;
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
+  layer_seq[l] = ++gate_seq;
   if ((fuse & 1) && M <= 128) {
     CombineIn ci{cur_h, y_d, cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, 1e-6f,
                  l > 0 ? stats_d + kStats * (l - 1) + 5 : nullptr};
+    const bool fp = fast_path();
+    RouteFast rf{dev_tab + (int64_t)l * M, &dctrl[l], fast_words + l, layer_seq[l]};
     CKS(router_route_fused(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
                            B, d, M, logits_d, stats_d + kStats * l + 7, k, cfg.route_mode,
                            cfg.routing_bias, mask[0], mask[1], sel_d, wts_d, counts_d, offsets_d,
                            perm_d, inv_d, dev_of(out_sel(l)), dev_of(out_logits(l)),
-                           const_cast<uint32_t*>(&dev_of(out(l))->done),
+                           fp ? nullptr : const_cast<uint32_t*>(&dev_of(out(l))->done),
                            stats_d + kStats * l + 6, fuse_d,
-                           comb_in_router(l, B) ? &ci : nullptr));
+                           comb_in_router(l, B) ? &ci : nullptr, fp ? &rf : nullptr));
     ++launches;
     if (sgate) {
       CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
@@ -409,11 +430,18 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
   const bool comb_next = comb_in_router(l + 1, B);
   if ((fuse & 2) && ffn_mode == 2) {
-    ++gate_seq;
+    GateIO io{};
+    if (fast_path()) {
+      const int nl = (l + 1) % cfg.L;
+      io = GateIO{fast_words + l, sel_d, logits_d, B * k, layer_R[l] * B * M,
+                  dev_of(out_sel(l)), dev_of(out_logits(l)),
+                  const_cast<uint32_t*>(&dev_of(out(l))->done), host_tab_dev + (int64_t)nl * M,
+                  dev_tab + (int64_t)nl * M, M};
+    }
     CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
-                         reinterpret_cast<volatile unsigned*>(fuse_d + 2), gate_seq, ready,
+                         reinterpret_cast<volatile unsigned*>(fuse_d + 2), layer_seq[l], ready,
                          stats_d + kStats * l, std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d,
-                         y_d));
+                         y_d, &io));
     launches += 2;
     if (!comb_next) {
       CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
@@ -462,6 +490,10 @@ void ef_engine::abort_pipeline(cudaStream_t stream, int from, int enq) {
   pinned_list.clear();
   for (int s : deferred_free) free_slots.push_back(s);
   deferred_free.clear();
+  // the device table may now lag the host's: no fast path until refreshed
+  cudaMemsetAsync(dev_tab, 0xff, sizeof(int2) * cfg.L * cfg.M, stream);
+  cudaMemsetAsync(fast_words, 0, sizeof(unsigned) * cfg.L, stream);
+  cudaStreamSynchronize(stream);
 }
 
 void ef_engine::step(cudaStream_t caller, float* h, int B, const std::vector<int64_t>& tokens_in) {
@@ -597,6 +629,17 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
         rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(sel, sel + B * k), R, B,
                                   cur_mask[0], cur_mask[1]});
       }
+      // the route kernel may have started FFN(l) on the slots of its table
+      // row (fast path): keep them until FFN(l) is done, whatever this
+      // decision evicts
+      for (int e = 0; e < M; ++e) {
+        if (!cnt[e]) continue;
+        const int s = phys_of[(int64_t)l * M + e];
+        if (s >= 0 && !pinned[s]) {
+          pinned[s] = 1;
+          pinned_list.push_back(s);
+        }
+      }
       if (l == 0) st->begin_token(tokens, gsizes, r);
       std::fill(layer_use.begin(), layer_use.end(), -1);
       st->begin_layer(l);
@@ -679,18 +722,20 @@ void ef_engine::fold_stats(int i) {
     stall_ms += sj[2] * 1e-6;
     if (sj[1] >= sj[0]) bubble_ms += (sj[1] - sj[0]) * 1e-6;
     if (sj[3] != ~0ull && sj[4] > sj[3]) ffn_ms += (sj[4] - sj[3]) * 1e-6;
+    fast_layers += sj[11] ? 1 : 0;
     if (dump) {  // per-layer device timeline (us)
       auto us = [](unsigned long long a, unsigned long long b) {
         return ((double)b - (double)a) * 1e-3;
       };
       fprintf(stderr,
               "layer %2d router %5.1f route %5.1f pub->gate %5.1f wait %6.1f gate %5.1f "
-              "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f\n",
+              "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f%s\n",
               j, us(sj[7], sj[6]), us(sj[6], sj[9]), us(sj[9], sj[0]), us(sj[0], sj[1]),
               us(sj[1], sj[8]), sj[10] != ~0ull ? us(sj[8], sj[10]) : 0.0,
               sj[3] != ~0ull && sj[10] != ~0ull ? us(sj[10], sj[3]) : 0.0,
               sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0, sj[2] * 1e-3, us(sj[4], sj[5]),
-              j + 1 < L ? us(sj[7], stats_h[kStats * (j + 1) + 7]) : 0.0);
+              j + 1 < L ? us(sj[7], stats_h[kStats * (j + 1) + 7]) : 0.0,
+              sj[11] ? " fast" : "");
     }
   }
   if (dump) fprintf(stderr, "step device time %.3f ms copies %lld\n", ms, (long long)stats_copies[i]);
@@ -799,8 +844,18 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     if (ffn && std::string(ffn) == "persistent") e->ffn_mode = 1;
     if (ffn && std::string(ffn) == "stream") e->ffn_mode = 0;
     CK(cudaMalloc(&e->counters_d, sizeof(int) * (kMaxActive + 1)));
+    CK(cudaHostAlloc(&e->host_tab, sizeof(int2) * L * M, cudaHostAllocMapped));
+    for (int64_t i = 0; i < (int64_t)L * M; ++i) e->host_tab[i] = make_int2(-1, 0);
+    CK(cudaHostGetDevicePointer((void**)&e->host_tab_dev, e->host_tab, 0));
+    CK(cudaMalloc(&e->dev_tab, sizeof(int2) * L * M));
+    CK(cudaMemset(e->dev_tab, 0xff, sizeof(int2) * L * M));
+    CK(cudaMalloc(&e->fast_words, sizeof(unsigned) * L));
+    CK(cudaMemset(e->fast_words, 0, sizeof(unsigned) * L));
+    e->layer_seq.assign(L, 0);
     CK(cudaMalloc(&e->fuse_d, sizeof(int) * 4));
     CK(cudaMemset(e->fuse_d, 0, sizeof(int) * 4));
+    const char* pdl = getenv("EF_PDL");
+    ef::g_use_pdl = !(pdl && pdl[0] == '0');
     const char* fz = getenv("EF_FUSE");
     if (fz) e->fuse = atoi(fz);
     *out = e.release();
@@ -849,15 +904,16 @@ extern "C" int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len,
 extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   EF_TRY({
     e->flush_stats();
-    double v[16] = {(double)e->steps,         (double)e->copies,
+    double v[17] = {(double)e->steps,         (double)e->copies,
                     (double)e->copy_bytes,    e->stall_ms,
                     (double)e->P,             (double)e->st->cache().capacity(),
                     (double)e->cfg.staging_slots, (double)e->launches,
                     e->host_ms,               e->ffn_ms,
                     e->step_ms,               (double)e->preload_copies,
                     (double)e->d2h_bytes,     (double)e->ffn_bytes,
-                    (double)e->ffn_launches,  e->bubble_ms};
-    for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
+                    (double)e->ffn_launches,  e->bubble_ms,
+                    (double)e->fast_layers};
+    for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];
   });
 }
 

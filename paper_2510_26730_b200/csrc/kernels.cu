@@ -17,10 +17,39 @@
 #include <cstddef>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/expertflow.h"
 #include "kernels.cuh"
 #include "pipeline.h"
+
+// Programmatic dependent launch (PDL): the decode kernels start with
+// griddepcontrol.wait (a no-op without a PDL primary), so a kernel launched
+// with programmatic stream serialisation may be scheduled while its
+// predecessor drains and only its launch latency overlaps — results are the
+// same as with plain stream order.
+namespace ef {
+bool g_use_pdl = false;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... K, typename... A>
+static cudaError_t launch_k(void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t c{};
+  c.gridDim = grid;
+  c.blockDim = block;
+  c.dynamicSmemBytes = smem;
+  c.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = at;
+  c.numAttrs = ef::g_use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&c, kern, std::forward<A>(args)...);
+}
 
 namespace ef {
 extern thread_local std::string g_last_error;
@@ -481,10 +510,47 @@ struct RouteArgs {
   uint64_t mlo, mhi;
   int32_t *sel, *counts, *offsets, *perm, *inv, *host_sel;
   float *wts, *host_logits;
-  uint32_t* host_done;
+  uint32_t* host_done;  // null: the fused gate warp publishes instead
   unsigned long long* stamp_route;
   int* counter;
+  ef::RouteFast rf;  // device-side slot resolution (rf.dc null: off)
 };
+
+__device__ __forceinline__ int2 ld_volatile_v2(const void* p) {
+  int2 v;
+  asm volatile("ld.volatile.global.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// Device-side slot resolution (one warp): if every routed expert of this
+// layer is in the device copy of the slot table, write the FFN's decision
+// block {slot, row offset, rows, fill seq} straight into DevCtrl and mark the
+// layer fast — the routed FFN then starts without the host round trip (the
+// host still decides the layer; its slots are pinned until FFN(l) is done).
+__device__ void resolve_fast(const ef::RouteFast& rf, const int32_t* counts,
+                             const int32_t* offsets, int M, unsigned long long* stamp_fast) {
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  bool ok = true;
+  for (int e0 = 0; e0 < M; e0 += 32) {
+    const int e = e0 + lane;
+    const int c = e < M ? __ldcg(counts + e) : 0;
+    int2 t = make_int2(-1, 0);
+    if (c > 0) t = ld_volatile_v2(rf.tab_row + e);
+    ok = ok && !__any_sync(0xffffffffu, c > 0 && t.x < 0);
+    const unsigned m = __ballot_sync(0xffffffffu, c > 0);
+    const int pos = base + __popc(m & ((1u << lane) - 1u));
+    if (c > 0 && pos < ef::kMaxActive) rf.dc->ent[pos] = make_int4(t.x, __ldcg(offsets + e), c, t.y);
+    base += __popc(m);
+  }
+  ok = ok && base <= ef::kMaxActive;
+  if (lane == 0) {
+    if (ok) rf.dc->n_active = base;
+    __threadfence();
+    *rf.fast_word = ok ? rf.seq : 0u;
+    if (stamp_fast) *stamp_fast = ok ? 1ull : 0ull;
+  }
+}
 
 // Previous layer's combine folded into the router (small batches): every CTA
 // recomputes h + sum_r w*y (+ g*ys) and the rmsnorm scale for its tokens into
@@ -513,6 +579,8 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   const int B = ra.B, M = ra.M;
   const int t0 = blockIdx.y * MAXB;
   const int nb = min(MAXB, B - t0);
+  pdl_wait();
+  pdl_trigger();  // a tiny grid: let the FFN's CTAs be scheduled behind it
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = gtimer();
   extern __shared__ float hs[];  // [nb][d] combined, un-normalised rows (cb.h only)
   __shared__ float invn_s[MAXB];
@@ -606,6 +674,8 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   route_body(sm, logits, B, M, ra.k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.sel, ra.wts, ra.counts,
              ra.offsets, ra.perm, ra.inv, nullptr, ra.host_sel, ra.host_logits, ra.host_done,
              ra.stamp_route, rows * B);
+  if (ra.rf.dc && (threadIdx.x >> 5) == 0)
+    resolve_fast(ra.rf, ra.counts, ra.offsets, M, ra.stamp_route ? ra.stamp_route + 5 : nullptr);
   if (threadIdx.x == 0) *ra.counter = 0;  // ready for the next launch
 }
 
@@ -615,10 +685,11 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
                        int mode, float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
                        int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                        int32_t* host_sel, float* host_logits, uint32_t* host_done,
-                       unsigned long long* stamp_route, int* counter, const CombineIn* ci) {
+                       unsigned long long* stamp_route, int* counter, const CombineIn* ci,
+                       const RouteFast* rf) {
   EF_CHECK_ARG(M <= 128 && k <= 16 && B >= 1, "bad fused route shape");
   RouteArgs ra{B, M, k, mode, bias, mlo, mhi, sel, counts, offsets, perm, inv, host_sel, wts,
-               host_logits, host_done, stamp_route, counter};
+               host_logits, host_done, stamp_route, counter, rf ? *rf : RouteFast{}};
   CombArgs cb{};
   size_t smem = 0;
   if (ci) {
@@ -634,18 +705,18 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
   const int blocks = (rows * 32 + threads - 1) / threads;
   if (dtype == EF_BF16) {
     if (B == 1)
-      router_route_kernel<__nv_bfloat16, 1><<<dim3(blocks, 1), threads, smem, st>>>(
-          x, (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb);
+      EF_CUDA_RET(launch_k(router_route_kernel<__nv_bfloat16, 1>, dim3(blocks, 1), dim3(threads), smem, st, x,
+                           (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb));
     else
-      router_route_kernel<__nv_bfloat16, 8><<<dim3(blocks, (B + 7) / 8), threads, smem, st>>>(
-          x, (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb);
+      EF_CUDA_RET(launch_k(router_route_kernel<__nv_bfloat16, 8>, dim3(blocks, (B + 7) / 8), dim3(threads), smem, st, x,
+                           (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb));
   } else {
     if (B == 1)
-      router_route_kernel<float, 1><<<dim3(blocks, 1), threads, smem, st>>>(
-          x, (const float*)w, rows, d, logits, stamp_router, ra, cb);
+      EF_CUDA_RET(launch_k(router_route_kernel<float, 1>, dim3(blocks, 1), dim3(threads), smem, st, x,
+                           (const float*)w, rows, d, logits, stamp_router, ra, cb));
     else
-      router_route_kernel<float, 8><<<dim3(blocks, (B + 7) / 8), threads, smem, st>>>(
-          x, (const float*)w, rows, d, logits, stamp_router, ra, cb);
+      EF_CUDA_RET(launch_k(router_route_kernel<float, 8>, dim3(blocks, (B + 7) / 8), dim3(threads), smem, st, x,
+                           (const float*)w, rows, d, logits, stamp_router, ra, cb));
   }
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
@@ -749,6 +820,7 @@ struct FuseArgs {
   DevCtrl* dc;
   volatile unsigned* dflag;
   unsigned seq;
+  ef::GateIO io;
 };
 
 __device__ __forceinline__ uint2 ld_acquire_sys_v2_(const volatile void* p) {
@@ -772,13 +844,26 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const volatile unsigned* p) {
   return v;
 }
 
-// One full warp: wait for go, copy the decision, publish it on the device.
+// One full warp: publish the route to the host, wait for go, copy the
+// decision (unless the route kernel resolved every slot on the device), then
+// copy the next layer's slot-table row for that kernel's fast path.
 __device__ void gate_duty(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats,
-                          volatile unsigned* dflag, unsigned seq) {
+                          volatile unsigned* dflag, unsigned seq, const ef::GateIO& io) {
   const int lane = threadIdx.x & 31;
+  if (stats && lane == 0) stats[0] = globaltimer();
+  if (io.host_done) {  // selection + every scored logits row -> mapped host memory
+    for (int f = lane; f < io.n_sel; f += 32) io.host_sel[f] = __ldcg(io.sel_src + f);
+    for (int i = lane; i < io.n_pub; i += 32) io.host_logits[i] = __ldcg(io.logits_src + i);
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) {
+      *reinterpret_cast<volatile uint32_t*>(io.host_done) = 1u;
+      if (stats) stats[9] = globaltimer();
+    }
+  }
+  const bool fast = io.fast_word && *reinterpret_cast<const volatile unsigned*>(io.fast_word) == seq;
   uint2 gn = make_uint2(0, 0);
   if (lane == 0) {
-    if (stats) stats[0] = globaltimer();
     const long long c0 = clock64();
     for (;;) {
       gn = ld_acquire_sys_v2_(&hc->go);
@@ -788,13 +873,22 @@ __device__ void gate_duty(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long
     }
     if (stats) stats[1] = globaltimer();
   }
-  const int n = __shfl_sync(0xffffffffu, (int)gn.y, 0);
-  for (int i = lane; i < n; i += 32) dc->ent[i] = ld_volatile_v4_(&hc->ent[i]);
+  if (!fast) {
+    const int n = __shfl_sync(0xffffffffu, (int)gn.y, 0);
+    for (int i = lane; i < n; i += 32) dc->ent[i] = ld_volatile_v4_(&hc->ent[i]);
+    __syncwarp();
+    if (lane == 0) {
+      dc->n_active = n;
+      __threadfence();
+      if (dflag) *dflag = seq;
+    }
+  }
+  __syncwarp();
+  if (io.tab_dst)  // the host's decision of this layer is final: refresh the next row
+    for (int e = lane; e < io.M; e += 32)
+      io.tab_dst[e] = ld_volatile_v2(io.tab_src + e);
   __syncwarp();
   if (lane == 0) {
-    dc->n_active = n;
-    __threadfence();
-    if (dflag) *dflag = seq;
     hc->go = 0u;
     if (stats) stats[8] = globaltimer();
   }
@@ -812,12 +906,19 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int n_all, p0;
   const char* wbase;
+  pdl_wait();
+  // down projection: the next kernel is the small router grid, schedule it early;
+  // gate/up: trigger only at the end (down CTAs must not take the slots of the
+  // second wave of gate/up CTAs)
+  if (!DUAL) pdl_trigger();
   if (fz.hc) {  // fused gate (up kernel)
     if (blockIdx.x == 0 && blockIdx.y == 0) {
-      if (wid == 0) gate_duty(fz.hc, fz.dc, cs.stats, fz.dflag, fz.seq);
+      if (wid == 0) gate_duty(fz.hc, fz.dc, cs.stats, fz.dflag, fz.seq, fz.io);
     } else if (threadIdx.x == 0) {
+      const bool fast = fz.io.fast_word &&
+                        *reinterpret_cast<const volatile unsigned*>(fz.io.fast_word) == fz.seq;
       const long long c0 = clock64();
-      while (ld_acquire_gpu(fz.dflag) < fz.seq) {
+      while (!fast && ld_acquire_gpu(fz.dflag) < fz.seq) {
         __nanosleep(64);
         if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
       }
@@ -937,6 +1038,7 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
     }
   }
   if (work && cs.ctrl && !DUAL && cs.stats && lane == 0) atomicMax(&cs.stats[4], globaltimer());
+  if (DUAL) pdl_trigger();
 }
 
 // Decode GEMV tilings (tools/ffn_lab.cu sweep on B200, Mixtral shapes):
@@ -952,8 +1054,8 @@ static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& 
   constexpr int R = kUpR, WARPS = 4;
   const int64_t es = sizeof(WT);
   dim3 gu((ff + WARPS * R - 1) / (WARPS * R), n_active);
-  ffn_gemv_kernel<WT, NT, R, true, XGather<WT>, kUpU>
-      <<<gu, 128, 0, st>>>(al, cs, fz_up, 0, (int64_t)ff * d * es, ff, d, xg, act, nullptr, ff);
+  launch_k(ffn_gemv_kernel<WT, NT, R, true, XGather<WT>, kUpU>, gu, dim3(128), 0, st, al, cs,
+           fz_up, (int64_t)0, (int64_t)ff * d * es, ff, d, xg, act, (float*)nullptr, ff);
   // down projection: one W2 row per warp (d rows only: more rows per warp
   // left SMs idle on Mixtral's 4096 x 14336 W2)
   constexpr int RD = kDnR, UD = kDnU;
@@ -961,8 +1063,8 @@ static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& 
   XAct<WT> xa{act, ff};
   CtrlSrc cs2 = cs;
   cs2.wait_ready = false;
-  ffn_gemv_kernel<WT, NT, RD, false, XAct<WT>, UD>
-      <<<gd, 128, 0, st>>>(al, cs2, fz_dn, 2 * (int64_t)ff * d * es, 0, d, ff, xa, nullptr, y, d);
+  launch_k(ffn_gemv_kernel<WT, NT, RD, false, XAct<WT>, UD>, gd, dim3(128), 0, st, al, cs2, fz_dn,
+           2 * (int64_t)ff * d * es, (int64_t)0, d, ff, xa, (WT*)nullptr, y, d);
 }
 
 template <typename WT>
@@ -1013,12 +1115,13 @@ int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k,
 int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                      int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
-                     int max_rows, int d, int ff, int dtype, void* act, float* y) {
+                     int max_rows, int d, int ff, int dtype, void* act, float* y,
+                     const GateIO* io) {
   EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
   ActiveList al{};
   CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
   FuseArgs fu{reinterpret_cast<volatile HostCtrl*>(hctrl_dev), reinterpret_cast<DevCtrl*>(dctrl),
-              dflag, seq};
+              dflag, seq, io ? *io : GateIO{}};
   if (dtype == EF_BF16) {
     XGather<__nv_bfloat16> xg{x, perm, k, d, false, 0};
     launch_ffn<__nv_bfloat16>(st, al, cs, max_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y,

@@ -12,6 +12,7 @@
 
 namespace ef {
 constexpr int kMaxActive = 80;
+extern bool g_use_pdl;  // launch decode kernels with programmatic dependent launch
 constexpr int kStats = 16;  // per-layer device timeline slots (see engine.cu dump)
 
 struct HostCtrl {
@@ -26,6 +27,26 @@ struct DevCtrl {
   int4 ent[kMaxActive];
 };
 
+// Device-side slot resolution by the route kernel (see resolve_fast).
+struct RouteFast {
+  const int2* tab_row;  // device copy of this layer's slot table: {slot, fill seq}, slot -1
+  DevCtrl* dc;          // this layer's decision block
+  unsigned* fast_word;  // set to seq when every routed expert resolved, else 0
+  unsigned seq;
+};
+// Extra duties of the fused gate warp (up kernel CTA 0, warp 0).
+struct GateIO {
+  const unsigned* fast_word;  // == seq: decision already on the device, do not overwrite
+  const int32_t* sel_src;     // publish sel[n_sel] and logits rows[n_pub] to the host
+  const float* logits_src;
+  int n_sel, n_pub;
+  int32_t* host_sel;
+  float* host_logits;
+  uint32_t* host_done;
+  const int2* tab_src;  // host slot-table row of the next layer (mapped) -> tab_dst
+  int2* tab_dst;
+  int M;
+};
 struct HostOut {  // followed by sel[B*k] int32 and logits[B*M] f32
   volatile uint32_t done;
   uint32_t pad[15];
@@ -82,9 +103,10 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
                        int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                        int32_t* host_sel, float* host_logits, uint32_t* host_done,
                        unsigned long long* stamp_route, int* counter,
-                       const CombineIn* comb = nullptr);
+                       const CombineIn* comb = nullptr, const RouteFast* rf = nullptr);
 int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                      int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
-                     int max_rows, int d, int ff, int dtype, void* act, float* y);
+                     int max_rows, int d, int ff, int dtype, void* act, float* y,
+                     const GateIO* io = nullptr);
 }  // namespace ef

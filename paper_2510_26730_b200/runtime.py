@@ -189,7 +189,8 @@ class MoEEngine:
     def stats(self) -> dict:
         keys = ["steps", "copies", "copy_bytes", "stall_ms", "phys_slots", "logical_capacity",
                 "staging_slots", "kernel_launches", "host_decision_ms", "ffn_ms", "step_ms",
-                "preload_copies", "d2h_bytes", "ffn_bytes", "ffn_launches", "gate_wait_ms"]
+                "preload_copies", "d2h_bytes", "ffn_bytes", "ffn_launches", "gate_wait_ms",
+                "fast_layers"]
         out = (C.c_double * len(keys))()
         L.check(L.lib.ef_engine_stats(self._h.ptr, out, len(keys)))
         return dict(zip(keys, list(out)))
