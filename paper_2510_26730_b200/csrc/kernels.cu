@@ -333,6 +333,87 @@ struct RouteSmem {
   uint64_t mask[2];
 };
 
+// Top-k of one token's logits by one warp (M <= 128), keyed on
+// logit + bias for resident experts (value desc, index asc — SURVEY H6), and
+// the routing weights from the raw logits.  sel/wts written by lane 0;
+// sel_sh (optional) gets a shared-memory copy.
+__device__ void topk_token(const float* __restrict__ lg, int M, int k, int mode, float bias,
+                           uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts, int32_t* sel_sh) {
+  const int lane = threadIdx.x & 31;
+  float v[4], key[4];
+  bool taken[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < M ? lg[e] : -INFINITY;
+    const bool res = e < 64 ? ((mlo >> e) & 1ull) : ((mhi >> (e - 64)) & 1ull);
+    key[i] = (e < M && res && bias != 0.f) ? __fadd_rn(v[i], bias) : v[i];
+    taken[i] = e >= M;
+  }
+  float mx_all = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx_all = fmaxf(mx_all, __shfl_xor_sync(0xffffffffu, mx_all, o));
+  float chosen_v[16];
+  int chosen_e[16];
+  for (int r = 0; r < k; ++r) {
+    float bk = 0.f;
+    int be = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = lane + 32 * i;
+      if (!taken[i] && (be == 0x7fffffff || key[i] > bk)) {
+        bk = key[i];
+        be = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      const bool other_better =
+          oe != 0x7fffffff && (be == 0x7fffffff || ok > bk || (ok == bk && oe < be));
+      if (other_better) {
+        bk = ok;
+        be = oe;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i == be) taken[i] = true;
+    chosen_e[r] = be;
+    // raw logit of the winner (weights ignore the bias), from its owning lane
+    const int bi = be >> 5;
+    const float mine = bi == 0 ? v[0] : bi == 1 ? v[1] : bi == 2 ? v[2] : v[3];
+    chosen_v[r] = __shfl_sync(0xffffffffu, mine, be & 31);
+  }
+  if (lane == 0) {
+    for (int r = 0; r < k; ++r) {
+      sel[r] = chosen_e[r];
+      if (sel_sh) sel_sh[r] = chosen_e[r];
+    }
+  }
+  if (mode == EF_ROUTE_MIXTRAL) {
+    if (lane == 0) {
+      float mx = -INFINITY;
+      for (int r = 0; r < k; ++r) mx = fmaxf(mx, chosen_v[r]);
+      float ev[16], sum = 0.f;
+      for (int r = 0; r < k; ++r) {
+        ev[r] = expf(chosen_v[r] - mx);
+        sum += ev[r];
+      }
+      for (int r = 0; r < k; ++r) wts[r] = ev[r] / sum;
+    }
+  } else {
+    float part = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < M) part += expf(v[i] - mx_all);
+    const float sum = warp_sum(part);
+    if (lane == 0)
+      for (int r = 0; r < k; ++r) wts[r] = expf(chosen_v[r] - mx_all) / sum;
+  }
+}
+
 // Route body, usable by any block size (the standalone kernel runs it with
 // 1024 threads, the fused router kernel with the last router CTA).
 __device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int B, int M, int k,
@@ -356,75 +437,9 @@ __device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int 
 
   // ---- top-k and weights: one warp per token, logits in registers (M <= 128),
   // k rounds of a warp arg-max keyed (value desc, index asc) — SURVEY H6
-  for (int t = wid; t < B; t += blockDim.x / 32) {
-    const float* lg = logits + (int64_t)t * M;
-    float v[4], key[4];
-    bool taken[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = lane + 32 * i;
-      v[i] = e < M ? lg[e] : -INFINITY;
-      const bool res = e < 64 ? ((mlo >> e) & 1ull) : ((mhi >> (e - 64)) & 1ull);
-      key[i] = (e < M && res && bias != 0.f) ? __fadd_rn(v[i], bias) : v[i];
-      taken[i] = e >= M;
-    }
-    float mx_all = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx_all = fmaxf(mx_all, __shfl_xor_sync(0xffffffffu, mx_all, o));
-    float chosen_v[16];
-    int chosen_e[16];
-    for (int r = 0; r < k; ++r) {
-      float bk = 0.f;
-      int be = 0x7fffffff;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = lane + 32 * i;
-        if (!taken[i] && (be == 0x7fffffff || key[i] > bk)) {
-          bk = key[i];
-          be = e;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-        const bool other_better =
-            oe != 0x7fffffff && (be == 0x7fffffff || ok > bk || (ok == bk && oe < be));
-        if (other_better) {
-          bk = ok;
-          be = oe;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (lane + 32 * i == be) taken[i] = true;
-      chosen_e[r] = be;
-      chosen_v[r] = lg[be];  // raw logit (weights ignore the bias)
-    }
-    if (lane == 0) {
-      for (int r = 0; r < k; ++r) sel[t * k + r] = chosen_e[r];
-    }
-    if (mode == EF_ROUTE_MIXTRAL) {
-      if (lane == 0) {
-        float mx = -INFINITY;
-        for (int r = 0; r < k; ++r) mx = fmaxf(mx, chosen_v[r]);
-        float ev[16], sum = 0.f;
-        for (int r = 0; r < k; ++r) {
-          ev[r] = expf(chosen_v[r] - mx);
-          sum += ev[r];
-        }
-        for (int r = 0; r < k; ++r) wts[t * k + r] = ev[r] / sum;
-      }
-    } else {
-      float part = 0.f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (lane + 32 * i < M) part += expf(v[i] - mx_all);
-      const float sum = warp_sum(part);
-      if (lane == 0)
-        for (int r = 0; r < k; ++r) wts[t * k + r] = expf(chosen_v[r] - mx_all) / sum;
-    }
-  }
+  for (int t = wid; t < B; t += blockDim.x / 32)
+    topk_token(logits + (int64_t)t * M, M, k, mode, bias, mlo, mhi, sel + t * k, wts + t * k,
+               nullptr);
   __syncthreads();
 
   // ---- stable counting sort by expert over flat slots f = t*k + r
@@ -552,6 +567,87 @@ __device__ void resolve_fast(const ef::RouteFast& rf, const int32_t* counts,
   }
 }
 
+// Small-batch route (B*k <= 32, one warp per token): top-k into shared
+// memory, then warp 0 does the stable sort of the <= 32 (token, rank) slots
+// with shuffles only, writes sel/wts/counts/offsets/perm/inv, and — with the
+// slot-table row preloaded in registers — resolves the layer's decision
+// block on the device.  No dependent global-memory round trips.
+__device__ void route_small(const float* __restrict__ logits, const RouteArgs& ra,
+                            const int2 (&tabv)[4], unsigned long long* stamp) {
+  __shared__ int32_t sel_sh[32];
+  const int B = ra.B, M = ra.M, k = ra.k, N = B * k;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (stamp && threadIdx.x == 0) *stamp = gtimer();
+  if (wid < B)
+    topk_token(logits + (int64_t)wid * M, M, k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.sel + wid * k,
+               ra.wts + wid * k, sel_sh + wid * k);
+  __syncthreads();
+  if (wid != 0) return;
+  const int e = lane < N ? sel_sh[lane] : 0x7fffffff;
+  // rank within the expert (stable in f) and number of slots with a smaller expert
+  const unsigned same = __match_any_sync(0xffffffffu, e);
+  const int rank = __popc(same & ((1u << lane) - 1u));
+  int below = 0;
+  for (int j = 0; j < N; ++j) below += __shfl_sync(0xffffffffu, e, j) < e;
+  if (lane < N) {
+    const int pos = below + rank;
+    ra.inv[lane] = pos;
+    ra.perm[pos] = lane;
+  }
+  // per-expert counts / offsets (lane owns experts lane + 32 i)
+  int cnt[4], off[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) cnt[i] = off[i] = 0;
+  for (int j = 0; j < N; ++j) {
+    const int ej = __shfl_sync(0xffffffffu, e, j);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      cnt[i] += ej == lane + 32 * i;
+      off[i] += ej < lane + 32 * i;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int x = lane + 32 * i;
+    if (x < M) {
+      ra.counts[x] = cnt[i];
+      ra.offsets[x] = off[i];
+    }
+  }
+  if (lane == 0) ra.offsets[M] = N;
+  if (ra.rf.dc) {  // device-side slot resolution, experts in ascending order
+    int base = 0;
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x = lane + 32 * i;
+      const bool act = x < M && cnt[i] > 0;
+      ok = ok && !__any_sync(0xffffffffu, act && tabv[i].x < 0);
+      const unsigned m = __ballot_sync(0xffffffffu, act);
+      const int pos = base + __popc(m & ((1u << lane) - 1u));
+      if (act && pos < ef::kMaxActive) ra.rf.dc->ent[pos] = make_int4(tabv[i].x, off[i], cnt[i], tabv[i].y);
+      base += __popc(m);
+    }
+    ok = ok && base <= ef::kMaxActive;
+    if (lane == 0) {
+      if (ok) ra.rf.dc->n_active = base;
+      __threadfence();
+      *ra.rf.fast_word = ok ? ra.rf.seq : 0u;
+      if (stamp) stamp[5] = ok ? 1ull : 0ull;
+    }
+  }
+  if (ra.host_done) {  // publish (non-fast configurations)
+    if (lane < N) ra.host_sel[lane] = e;
+    for (int i = lane; i < B * M; i += 32) ra.host_logits[i] = __ldcg(logits + i);
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) {
+      *reinterpret_cast<volatile uint32_t*>(ra.host_done) = 1u;
+      if (stamp) stamp[3] = gtimer();
+    }
+  }
+}
+
 // Previous layer's combine folded into the router (small batches): every CTA
 // recomputes h + sum_r w*y (+ g*ys) and the rmsnorm scale for its tokens into
 // shared memory; the last CTA writes h and x back once all CTAs have read h.
@@ -579,6 +675,29 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   const int B = ra.B, M = ra.M;
   const int t0 = blockIdx.y * MAXB;
   const int nb = min(MAXB, B - t0);
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  // UN 16-byte chunks in flight per lane (a 4096-wide bf16 row in one round trip at B=1)
+  constexpr int UN = MAXB == 1 ? 16 : 8;
+  // the router weights are constant: the first chunk group of this warp's row
+  // is loaded before waiting on the previous kernel, so its HBM latency
+  // overlaps the tail of the previous layer's FFN
+  uint4 wv0[UN];
+  if (warp < rows) {
+#pragma unroll
+    for (int u = 0; u < UN; ++u)
+      if (lane * V + u * 32 * V < d) wv0[u] = ld_stream16(w + (int64_t)warp * d + lane * V + u * 32 * V);
+  }
+  // this layer's slot-table row is final once the previous kernel has started
+  // (written by the previous layer's gate warp, two kernels back)
+  int2 tabv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tabv[i] = make_int2(-1, 0);
+  if (ra.rf.dc && threadIdx.x < 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < M) tabv[i] = ld_volatile_v2(ra.rf.tab_row + lane + 32 * i);
+  }
   pdl_wait();
   pdl_trigger();  // a tiny grid: let the FFN's CTAs be scheduled behind it
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = gtimer();
@@ -594,20 +713,20 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     }
     __syncthreads();
   }
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   if (warp < rows) {
     const WT* wr = w + (int64_t)warp * d;
     float acc[MAXB];
 #pragma unroll
     for (int t = 0; t < MAXB; ++t) acc[t] = 0.f;
-    // UN 16-byte chunks in flight per lane (a 4096-wide bf16 row in one round trip at B=1)
-    constexpr int UN = MAXB == 1 ? 16 : 8;
     for (int c0 = lane * V; c0 < d; c0 += UN * 32 * V) {
       uint4 wv[UN];
 #pragma unroll
-      for (int u = 0; u < UN; ++u)
-        if (c0 + u * 32 * V < d) wv[u] = ld_stream16(wr + c0 + u * 32 * V);
+      for (int u = 0; u < UN; ++u) {
+        if (c0 == lane * V)
+          wv[u] = wv0[u];
+        else if (c0 + u * 32 * V < d)
+          wv[u] = ld_stream16(wr + c0 + u * 32 * V);
+      }
 #pragma unroll
       for (int u = 0; u < UN; ++u) {
         const int c = c0 + u * 32 * V;
@@ -671,12 +790,16 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     }
     if (cb.stamp && threadIdx.x == 0) *cb.stamp = gtimer();
   }
+  if (threadIdx.x == 0) *ra.counter = 0;  // ready for the next launch
+  if (B * ra.k <= 32 && B <= (int)(blockDim.x >> 5) && (!ra.host_done || rows == M)) {
+    route_small(logits, ra, tabv, ra.stamp_route);
+    return;
+  }
   route_body(sm, logits, B, M, ra.k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.sel, ra.wts, ra.counts,
              ra.offsets, ra.perm, ra.inv, nullptr, ra.host_sel, ra.host_logits, ra.host_done,
              ra.stamp_route, rows * B);
   if (ra.rf.dc && (threadIdx.x >> 5) == 0)
     resolve_fast(ra.rf, ra.counts, ra.offsets, M, ra.stamp_route ? ra.stamp_route + 5 : nullptr);
-  if (threadIdx.x == 0) *ra.counter = 0;  // ready for the next launch
 }
 
 namespace ef {
