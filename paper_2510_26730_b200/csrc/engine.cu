@@ -433,10 +433,14 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
     GateIO io{};
     if (fast_path()) {
       const int nl = (l + 1) % cfg.L;
+      // rows the next router will most likely read: its layer plus up to 3
+      // pre-gate layers (the horizon is decided later)
+      const int64_t rrows = (int64_t)std::min(4, cfg.L - nl) * M;
       io = GateIO{fast_words + l, sel_d, logits_d, B * k, layer_R[l] * B * M,
                   dev_of(out_sel(l)), dev_of(out_logits(l)),
                   const_cast<uint32_t*>(&dev_of(out(l))->done), host_tab_dev + (int64_t)nl * M,
-                  dev_tab + (int64_t)nl * M, M};
+                  dev_tab + (int64_t)nl * M, M,
+                  (const char*)router_w + (int64_t)nl * M * d * esz, rrows * d * esz};
     }
     CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
                          reinterpret_cast<volatile unsigned*>(fuse_d + 2), layer_seq[l], ready,
@@ -582,6 +586,12 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       enqueue_layer(stream, 0, B, h, Rmax, cur_mask);
     }
     enq = 1;
+    // the previous step's stats, now that this step's first layer is queued
+    // (keeps host bookkeeping off the step boundary)
+    if (stats_pending >= 0) {
+      fold_stats(stats_pending);
+      stats_pending = -1;
+    }
     for (l = 0; l < L; ++l) {
       // ---- wait for route(l) to publish its selection
       HostOut* ho = out(l);
@@ -703,7 +713,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
                        cudaMemcpyDeviceToHost, stream));
     CK(cudaEventRecord(tev[i][2], stream));
     stats_copies[i] = copies - copies_at_step;
-    if (stats_pending >= 0) fold_stats(stats_pending);  // the previous step: long done
+    if (stats_pending >= 0) fold_stats(stats_pending);  // (folded at step start normally)
     stats_pending = i;
     stats_buf ^= 1;
   }
@@ -738,7 +748,20 @@ void ef_engine::fold_stats(int i) {
               sj[11] ? " fast" : "");
     }
   }
-  if (dump) fprintf(stderr, "step device time %.3f ms copies %lld\n", ms, (long long)stats_copies[i]);
+  if (dump) {
+    double a = 0, b = 0, c = 0;
+    for (int j = 1; j < L; ++j) {
+      const unsigned long long* sj = &stats_h[kStats * j];
+      a += ((double)sj[14] - (double)sj[15]);
+      b += ((double)sj[12] - (double)sj[14]);
+      c += ((double)sj[13] - (double)sj[12]);
+    }
+    fprintf(stderr,
+            "router phases (SM cycles, mean over layers 1..): weights-ready %.0f combine %.0f "
+            "gemv %.0f\n",
+            a / (L - 1), b / (L - 1), c / (L - 1));
+    fprintf(stderr, "step device time %.3f ms copies %lld\n", ms, (long long)stats_copies[i]);
+  }
 }
 
 extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,

@@ -46,6 +46,8 @@ struct GateIO {
   const int2* tab_src;  // host slot-table row of the next layer (mapped) -> tab_dst
   int2* tab_dst;
   int M;
+  const char* router_next;  // next layer's router weight rows, prefetched into L2
+  int64_t router_bytes;
 };
 struct HostOut {  // followed by sel[B*k] int32 and logits[B*M] f32
   volatile uint32_t done;
