@@ -132,9 +132,14 @@ struct ef_engine {
   int stats_buf = 0, stats_pending = -1;
   int64_t stats_copies[2] = {0, 0}, copies_at_step = 0;
   void fold_stats(int i);
+  std::string dump_text;  // EF_STATS_DUMP timeline, printed on flush (not mid-step)
   void flush_stats() {
     if (stats_pending >= 0) fold_stats(stats_pending);
     stats_pending = -1;
+    if (!dump_text.empty()) {
+      fputs(dump_text.c_str(), stderr);
+      dump_text.clear();
+    }
   }
   std::vector<char*> store;  // per layer: M * stride bytes
   cudaStream_t copy_stream = nullptr, side_stream = nullptr;
@@ -737,7 +742,8 @@ void ef_engine::fold_stats(int i) {
       auto us = [](unsigned long long a, unsigned long long b) {
         return ((double)b - (double)a) * 1e-3;
       };
-      fprintf(stderr,
+      char line[320];
+      snprintf(line, sizeof line,
               "layer %2d router %5.1f route %5.1f pub->gate %5.1f wait %6.1f gate %5.1f "
               "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f%s\n",
               j, us(sj[7], sj[6]), us(sj[6], sj[9]), us(sj[9], sj[0]), us(sj[0], sj[1]),
@@ -746,6 +752,7 @@ void ef_engine::fold_stats(int i) {
               sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0, sj[2] * 1e-3, us(sj[4], sj[5]),
               j + 1 < L ? us(sj[7], stats_h[kStats * (j + 1) + 7]) : 0.0,
               sj[11] ? " fast" : "");
+      dump_text += line;
     }
   }
   if (dump) {
@@ -756,11 +763,12 @@ void ef_engine::fold_stats(int i) {
       b += ((double)sj[12] - (double)sj[14]);
       c += ((double)sj[13] - (double)sj[12]);
     }
-    fprintf(stderr,
-            "router phases (SM cycles, mean over layers 1..): weights-ready %.0f combine %.0f "
-            "gemv %.0f\n",
-            a / (L - 1), b / (L - 1), c / (L - 1));
-    fprintf(stderr, "step device time %.3f ms copies %lld\n", ms, (long long)stats_copies[i]);
+    char line[320];
+    snprintf(line, sizeof line,
+             "router phases (SM cycles, mean over layers 1..): weights-ready %.0f combine %.0f "
+             "gemv %.0f\nstep device time %.3f ms copies %lld\n",
+             a / (L - 1), b / (L - 1), c / (L - 1), ms, (long long)stats_copies[i]);
+    dump_text += line;
   }
 }
 

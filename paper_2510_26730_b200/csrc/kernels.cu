@@ -1094,10 +1094,12 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
   // gate/up: trigger only at the end (down CTAs must not take the slots of the
   // second wave of gate/up CTAs)
   if (!DUAL) pdl_trigger();
-  if (fz.hc) {  // fused gate (up kernel)
-    if (blockIdx.x == 0 && blockIdx.y == 0) {
-      if (wid == 0) gate_duty(fz.hc, fz.dc, cs.stats, fz.dflag, fz.seq, fz.io);
-    } else if (threadIdx.x == 0) {
+  if (fz.hc) {  // fused gate (up kernel): column 0 of the grid is the gate, not FFN work
+    if (blockIdx.x == 0) {
+      if (blockIdx.y == 0 && wid == 0) gate_duty(fz.hc, fz.dc, cs.stats, fz.dflag, fz.seq, fz.io);
+      return;
+    }
+    if (threadIdx.x == 0) {
       const bool fast = fz.io.fast_word &&
                         *reinterpret_cast<const volatile unsigned*>(fz.io.fast_word) == fz.seq;
       const long long c0 = clock64();
@@ -1111,7 +1113,11 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
   if (cs.ctrl) {
     __shared__ int4 e_sh;
     if (threadIdx.x == 0) {
-      if (cs.wait_ready && cs.stats) atomicMin(&cs.stats[10], globaltimer());
+      // timeline stamps: the earliest CTAs of the grid define the start, one
+      // atomic per CTA for the end (thousands of same-address atomics per
+      // launch would serialise in L2)
+      const bool early = blockIdx.x < 3;
+      if (cs.wait_ready && cs.stats && early) atomicMin(&cs.stats[10], globaltimer());
       int4 e = make_int4(0, 0, 0, 0);
       if (a < __ldcg(&cs.ctrl->n_active)) e = __ldcg(&cs.ctrl->ent[a]);
       if (cs.wait_ready && e.z > 0) {
@@ -1126,7 +1132,7 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
           unsigned long long t1 = globaltimer();
           if (t1 > t0) atomicMax(&cs.stats[2], t1 - t0);
         }
-        atomicMin(&cs.stats[3], globaltimer());
+        if (early) atomicMin(&cs.stats[3], globaltimer());
       }
       e_sh = e;
     }
@@ -1140,7 +1146,7 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
     p0 = al.p0[a];
     wbase = al.w[a];
   }
-  const int j0 = (blockIdx.x * WARPS + wid) * R;
+  const int j0 = ((blockIdx.x - (fz.hc ? 1 : 0)) * WARPS + wid) * R;
   // no early return: the fused combine counts every CTA of the grid
   const bool work = n_all > 0 && j0 < rows;
   const WT* A = reinterpret_cast<const WT*>(wbase + offA);
@@ -1221,7 +1227,8 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
       }
     }
   }
-  if (work && cs.ctrl && !DUAL && cs.stats && lane == 0) atomicMax(&cs.stats[4], globaltimer());
+  if (work && cs.ctrl && !DUAL && cs.stats && threadIdx.x == 0)
+    atomicMax(&cs.stats[4], globaltimer());
   if (DUAL) pdl_trigger();
 }
 
@@ -1237,7 +1244,7 @@ static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& 
                           const FuseArgs& fz_up, const FuseArgs& fz_dn) {
   constexpr int R = kUpR, WARPS = 4;
   const int64_t es = sizeof(WT);
-  dim3 gu((ff + WARPS * R - 1) / (WARPS * R), n_active);
+  dim3 gu((ff + WARPS * R - 1) / (WARPS * R) + (fz_up.hc ? 1 : 0), n_active);
   launch_k(ffn_gemv_kernel<WT, NT, R, true, XGather<WT>, kUpU>, gu, dim3(128), 0, st, al, cs,
            fz_up, (int64_t)0, (int64_t)ff * d * es, ff, d, xg, act, (float*)nullptr, ff);
   // down projection: one W2 row per warp (d rows only: more rows per warp
