@@ -97,10 +97,13 @@ def launch_list(path, rnd):
     all_ns = sum(tot.values())
     md = [f"# {rnd}: kernel share of the decode steps (ncu launch list)", "",
           "Command: `EF_PIPE_DEBUG=1 EF_FUSE=1 ncu --metrics gpu__time_duration.sum "
-          "--clock-control none python tools/profile_decode.py --layers 2 --steps 3` "
-          "(Mixtral-8x7B layer shape, 2 layers, B=1; EF_PIPE_DEBUG serialises the host "
-          "pipeline so ncu can replay each kernel; EF_FUSE=1 keeps the gate in its own "
-          "kernel because ncu cannot replay a kernel that consumes a host flag).", "",
+          "--clock-control none python tools/profile_decode.py --layers 32 --steps 3 "
+          "--policy adaptive --budget-frac 0.4 --bias 10000` (Mixtral-8x7B shape, 32 layers, "
+          "B=1, the bench's policy and budget).  ncu makes every launch synchronous, so the "
+          "run-ahead pipeline (whose fused gate waits on the host) cannot run under it: "
+          "EF_PIPE_DEBUG=1 decides each layer before enqueueing its FFN and EF_FUSE=1 keeps "
+          "the gate in its own kernel.  The default pipeline has no gate_kernel launch, no "
+          "combine_kernel launch (folded into the next router) and no host wait.", "",
           "Per-launch times are cold-cache and serialised: compare shares, not absolutes.", "",
           "| kernel | launches | total us | mean us | share |", "|---|---:|---:|---:|---:|"]
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
@@ -117,13 +120,25 @@ def main():
     ap.add_argument("--ffn")
     ap.add_argument("--router")
     ap.add_argument("--gemm")
+    ap.add_argument("--up", help="separate capture of the gate/up GEMV (merged into decode_ffn)")
+    ap.add_argument("--down", help="separate capture of the down GEMV (merged into decode_ffn)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
         launch_list(a.launches, a.round)
     traffic = {}
-    if a.ffn:
+    if a.up and a.down:
+        ku = summarise(a.up, "decode_ffn_up", a.round)
+        kd = summarise(a.down, "decode_ffn_down", a.round)
+        a.ffn = None
+        ks = ku + kd
+        src = f"{os.path.basename(a.up)} + {os.path.basename(a.down)}"
+    elif a.ffn:
         ks = summarise(a.ffn, "decode_ffn", a.round)
+        src = os.path.basename(a.ffn)
+    else:
+        ks = []
+    if ks:
         up = [k for k in ks if "XGather" in k["kernel"]]
         dn = [k for k in ks if "XAct" in k["kernel"]]
         if up and dn:
@@ -136,7 +151,7 @@ def main():
                 "dram_bytes_up": dram(up[0]), "dram_bytes_down": dram(dn[0]),
                 "dram_bytes_per_launch": dram(up[0]) + dram(dn[0]),
                 "algorithmic_bytes_per_launch": 2 * 3 * 4096 * 14336 * 2,
-                "source": os.path.basename(a.ffn), "round": a.round,
+                "source": src, "round": a.round,
             }
             with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
                 json.dump(traffic, f, indent=1)
