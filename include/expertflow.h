@@ -291,6 +291,7 @@ typedef struct ef_engine_cfg {
   int32_t device;
   int32_t timing; /* record per-layer stall events (physical stall %) */
   int32_t record_routing; /* keep every layer's logits / selection for parity checks */
+  int32_t max_prefill;    /* > 0: allocate prefill buffers for up to this many tokens (bf16) */
 } ef_engine_cfg;
 int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim, const ef_ladder_cfg* ladder,
                      ef_engine** out);
@@ -298,6 +299,11 @@ void ef_engine_destroy(ef_engine* e);
 /* one decode step: h[B,d] fp32 device in/out, on `stream` */
 int ef_engine_step(ef_engine* e, void* stream, float* h, int B, const int64_t* tokens,
                    int n_tokens);
+/* prefill: T <= max_prefill tokens h[T,d] (fp32 device, in place) through every
+   layer as one scheduler step (one routing group per token); the expert FFNs run
+   on the tcgen05/TMA grouped GEMM (ef_grouped_gemm_bf16), synchronously per layer */
+int ef_engine_prefill(ef_engine* e, void* stream, float* h, int T, const int64_t* tokens,
+                      int n_tokens);
 /* the same step with the hidden state in pinned host memory: h_in[B,d] is read
    and h_out[B,d] written (may alias) by SM loads/stores over PCIe, ordered on
    `stream` (h_out is complete when the stream reaches the step's end); never

@@ -62,7 +62,7 @@ class EngineCfg(C.Structure):
                 ("route_mode", i32), ("max_batch", i32), ("shared_ff", i32),
                 ("shared_gate", i32), ("budget_slots", i64), ("staging_slots", i32),
                 ("routing_bias", f32), ("seed", u64), ("device", i32), ("timing", i32),
-                ("record_routing", i32)]
+                ("record_routing", i32), ("max_prefill", i32)]
 
 
 _SIGS = {
@@ -137,6 +137,7 @@ _SIGS = {
     "ef_engine_destroy": (None, [vp]),
     "ef_engine_step": (C.c_int, [vp, vp, vp, C.c_int, P(i64), C.c_int]),
     "ef_engine_step_host": (C.c_int, [vp, vp, vp, vp, C.c_int, P(i64), C.c_int]),
+    "ef_engine_prefill": (C.c_int, [vp, vp, vp, C.c_int, P(i64), C.c_int]),
     "ef_engine_metrics": (C.c_int, [vp, P(i64), i32, P(f64)]),
     "ef_engine_output": (C.c_int, [vp, i32, P(i64), i64, P(i64)]),
     "ef_engine_event_details": (C.c_int, [vp, C.c_char_p, i64, P(i64)]),

@@ -287,6 +287,22 @@ struct ef_engine {
                  const std::vector<int64_t>& tokens);
   void join(cudaStream_t stream, cudaStream_t caller);
   void step_on(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
+  // ---- prefill (config C4): T tokens through every layer as one scheduler
+  // step, expert FFNs on the tcgen05/TMA grouped GEMM; synchronous per layer
+  // (the host decides each layer from its copied logits, then the GEMMs run)
+  int max_prefill = 0;
+  float *px_d = nullptr, *plogits_d = nullptr, *pwts_d = nullptr, *py_d = nullptr,
+        *pys_d = nullptr, *psgl_d = nullptr, *plogits_h = nullptr;
+  int32_t *psel_d = nullptr, *pcounts_d = nullptr, *poffsets_d = nullptr, *pperm_d = nullptr,
+          *pinv_d = nullptr, *piota_d = nullptr, *psel_h = nullptr;
+  void *pA_d = nullptr, *pact_d = nullptr, *pacts_d = nullptr;
+  int4 *ptiles_h = nullptr, *ptiles_hdev = nullptr, *ptiles_d = nullptr;
+  int64_t ptiles_cap = 0;  // int4 entries per region (4 regions)
+  cudaEvent_t copy_mark = nullptr;
+  int64_t prefills = 0, prefill_tokens = 0;
+  double prefill_gemm_flop = 0;
+  void prefill(cudaStream_t stream, float* h, int T, const std::vector<int64_t>& tokens);
+  void prefill_on(cudaStream_t stream, float* h, int T, const std::vector<int64_t>& tokens);
   cudaStream_t compute_stream = nullptr;
   cudaEvent_t join_in = nullptr, join_out = nullptr;
   ~ef_engine();
@@ -358,9 +374,14 @@ ef_engine::~ef_engine() {
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
                   (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d, (void*)h_io_d, (void*)dev_tab,
-                  (void*)fast_words})
+                  (void*)fast_words, (void*)px_d, (void*)plogits_d, (void*)pwts_d, (void*)py_d,
+                  (void*)pys_d, (void*)psgl_d, (void*)psel_d, (void*)pcounts_d, (void*)poffsets_d,
+                  (void*)pperm_d, (void*)pinv_d, (void*)piota_d, pA_d, pact_d, pacts_d,
+                  (void*)ptiles_d})
     if (p) cudaFree(p);
-  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring, (void*)host_tab})
+  if (copy_mark) cudaEventDestroy(copy_mark);
+  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring, (void*)host_tab,
+                  (void*)plogits_h, (void*)psel_h, (void*)ptiles_h})
     if (p) cudaFreeHost(p);
   for (char* p : store)
     if (p) cudaFreeHost(p);
@@ -772,6 +793,163 @@ void ef_engine::fold_stats(int i) {
   }
 }
 
+void ef_engine::prefill(cudaStream_t caller, float* h, int T,
+                        const std::vector<int64_t>& tokens_in) {
+  cudaStream_t stream = compute_stream ? compute_stream : caller;
+  if (stream != caller) {
+    CK(cudaEventRecord(join_in, caller));
+    CK(cudaStreamWaitEvent(stream, join_in, 0));
+  }
+  prefill_on(stream, h, T, tokens_in);
+  join(stream, caller);
+}
+
+void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
+                           const std::vector<int64_t>& tokens_in) {
+  const int L = cfg.L, M = cfg.M, k = cfg.top_k, d = cfg.d, ff = cfg.ff;
+  if (max_prefill < 1) throw ValueError("engine created without prefill buffers (max_prefill)");
+  if (T < 1 || T > max_prefill) throw ValueError("prefill length outside [1, max_prefill]");
+  std::vector<int64_t> tokens = tokens_in;
+  if (tokens.empty()) tokens.push_back(-(steps + prefills + 1));
+  const bool sgate = cfg.shared_ff && cfg.shared_gate;
+  const int sff = cfg.shared_ff;
+  std::vector<int64_t> gsizes(T, 1);
+  CKS(ef_rmsnorm(stream, h, px_d, T, d, 1e-6f));
+  ++launches;
+  residency_mask(0, cur_mask);
+  int R = Rmax;
+  for (int l = 0; l < L; ++l) {
+    R = std::max(1, std::min(R, L - l));
+    // ---- router (layer l + pre-gate rows) and route; the host copies what it needs
+    CKS(ef_router_logits(stream, px_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R, T,
+                         d, M, plogits_d));
+    CKS(launch_route_publish(stream, plogits_d, T, M, k, cfg.route_mode, cfg.routing_bias,
+                             cur_mask[0], cur_mask[1], psel_d, pwts_d, pcounts_d, poffsets_d,
+                             pperm_d, pinv_d, nullptr, nullptr, nullptr, nullptr, nullptr, 0));
+    launches += 2;
+    CK(cudaMemcpyAsync(plogits_h, plogits_d, sizeof(float) * R * T * M, cudaMemcpyDeviceToHost,
+                       stream));
+    CK(cudaMemcpyAsync(psel_h, psel_d, sizeof(int32_t) * T * k, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    d2h_bytes += (int64_t)(T * k + R * T * M) * 4;
+    // ---- decision (same contract as the decode loop, one group per token)
+    LayerRouting r;
+    r.gate.resize(M);
+    batch_gate(plogits_h, T, M, cfg.routing_bias, cur_mask, r.gate.data());
+    std::vector<int> cnt(M, 0);
+    r.group_actual.resize(T);
+    for (int t = 0; t < T; ++t) {
+      std::vector<int> g(psel_h + t * k, psel_h + (t + 1) * k);
+      for (int e : g) {
+        if (e < 0 || e >= M) throw RuntimeErr("route kernel produced an invalid expert id");
+        cnt[e]++;
+      }
+      std::sort(g.begin(), g.end());
+      r.group_actual[t] = std::move(g);
+    }
+    for (int e = 0; e < M; ++e)
+      if (cnt[e]) r.actual.push_back(e);
+    const float* lg0 = plogits_h;
+    hooks->pregate_fn = [&, R, lg0](int layer, int hz, double* o) {
+      if (hz >= R) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
+      uint64_t m[2];
+      residency_mask(layer + hz, m);
+      batch_gate(lg0 + (int64_t)hz * T * M, T, M, cfg.routing_bias, m, o);
+    };
+    if (cfg.record_routing) {
+      std::vector<float> lg(lg0, lg0 + (int64_t)R * T * M);
+      rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(psel_h, psel_h + T * k), R, T,
+                                cur_mask[0], cur_mask[1]});
+    }
+    if (l == 0) st->begin_token(tokens, gsizes, r);
+    std::fill(layer_use.begin(), layer_use.end(), -1);
+    st->begin_layer(l);
+    st->run_layer(l, r);
+    // every copy issued so far has to land (the link is serial: the layer's
+    // demand transfers are the last ones the decision waited for)
+    CK(cudaEventRecord(copy_mark, copy_stream));
+    CK(cudaStreamWaitEvent(stream, copy_mark, 0));
+    // ---- tiles {a_row0, b_row0, m_valid, n0}: 128-row m-tiles x 128-column n-tiles
+    int4* tu = ptiles_h;
+    int4* td = ptiles_h + ptiles_cap;
+    int nu = 0, nd = 0, run = 0, n_act = 0;
+    for (int e = 0; e < M; ++e) {
+      if (!cnt[e]) continue;
+      const int sl = layer_use[e];
+      if (sl < 0) throw RuntimeErr("routed expert has no resolved slot");
+      for (int n0 = 0; n0 < ff; n0 += 128)
+        for (int m0 = 0; m0 < cnt[e]; m0 += 128)
+          tu[nu++] = make_int4(run + m0, sl * 3 * ff, std::min(128, cnt[e] - m0), n0);
+      for (int n0 = 0; n0 < d; n0 += 128)
+        for (int m0 = 0; m0 < cnt[e]; m0 += 128)
+          td[nd++] = make_int4(run + m0, sl * 3 * d + 2 * d, std::min(128, cnt[e] - m0), n0);
+      run += cnt[e];
+      ++n_act;
+    }
+    if (nu > ptiles_cap || nd > ptiles_cap) throw RuntimeErr("prefill tile list overflow");
+    int nsu = 0, nsd = 0;
+    int4* tsu = ptiles_h + 2 * ptiles_cap;
+    int4* tsd = ptiles_h + 3 * ptiles_cap;
+    if (sff) {
+      for (int n0 = 0; n0 < sff; n0 += 128)
+        for (int m0 = 0; m0 < T; m0 += 128) tsu[nsu++] = make_int4(m0, 0, std::min(128, T - m0), n0);
+      for (int n0 = 0; n0 < d; n0 += 128)
+        for (int m0 = 0; m0 < T; m0 += 128)
+          tsd[nsd++] = make_int4(m0, 2 * d, std::min(128, T - m0), n0);
+      if (nsu > ptiles_cap || nsd > ptiles_cap) throw RuntimeErr("prefill tile list overflow");
+    }
+    // tile lists to device memory by SM loads (no copy-engine queueing)
+    CKS(launch_host_io(stream, reinterpret_cast<const float*>(ptiles_hdev),
+                       reinterpret_cast<float*>(ptiles_d), 4 * 4 * ptiles_cap, false));
+    ffn_bytes += (int64_t)n_act * stride;
+    ffn_launches += 2;
+    prefill_gemm_flop += 2.0 * T * k * (double)d * 3 * ff;
+    // ---- routed experts on the tensor cores: gather, gate/up (+SiLU*up), down
+    const int64_t rows = (int64_t)T * k;
+    CKS(ef_gather_rows_bf16(stream, px_d, pperm_d, k, d, (int)rows, pA_d));
+    CKS(ef_grouped_gemm_bf16(stream, pA_d, rows, d, slab, (int64_t)P * 3 * ff, d, ptiles_d, nu, 1, ff,
+                             pact_d, ff));
+    CKS(ef_grouped_gemm_bf16(stream, pact_d, rows, ff, slab, (int64_t)P * 3 * d, ff,
+                             ptiles_d + ptiles_cap, nd, 0, 0, py_d, d));
+    launches += 4;
+    if (sff) {  // shared expert(s): same GEMMs over all T tokens in order
+      const char* sw = shared_w + (int64_t)l * sstride;
+      CKS(ef_gather_rows_bf16(stream, px_d, piota_d, 1, d, T, pA_d));
+      CKS(ef_grouped_gemm_bf16(stream, pA_d, T, d, sw, 3LL * sff, d, ptiles_d + 2 * ptiles_cap,
+                               nsu, 1, sff, pacts_d, sff));
+      CKS(ef_grouped_gemm_bf16(stream, pacts_d, T, sff, sw, 3LL * d, sff, ptiles_d + 3 * ptiles_cap,
+                               nsd, 0, 0, pys_d, d));
+      launches += 3;
+      prefill_gemm_flop += 2.0 * T * (double)d * 3 * sff;
+      if (sgate) {
+        CKS(ef_router_logits(stream, px_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, T, d,
+                             1, psgl_d));
+        ++launches;
+      }
+    }
+    CKS(combine_stamped(stream, h, px_d, py_d, pinv_d, pwts_d, sff ? pys_d : nullptr,
+                        sgate ? psgl_d : nullptr, T, d, k, 1e-6f, nullptr));
+    ++launches;
+    // slots read by this layer's GEMMs are free again once the next layer's
+    // route has been synchronised (stream order)
+    for (int s2 : pinned_list) pinned[s2] = 0;
+    pinned_list.clear();
+    for (int s2 : deferred_free) free_slots.push_back(s2);
+    deferred_free.clear();
+    if (l + 1 < L) {
+      residency_mask(l + 1, cur_mask);
+      R = 1 + st->planned_horizon(l + 1);
+    }
+  }
+  st->end_token();
+  ++prefills;
+  prefill_tokens += T;
+  // the decode fast path's device slot table lags the host mirror now
+  CKS(launch_host_io(stream, reinterpret_cast<const float*>(host_tab_dev),
+                     reinterpret_cast<float*>(dev_tab), (int64_t)L * M * 2, false));
+  ++launches;
+}
+
 extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
                                 const ef_ladder_cfg* ladder, ef_engine** out) {
   EF_TRY({
@@ -822,6 +1000,41 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     }
     CK(cudaMalloc(&e->x_d, (size_t)B * d * 4));
     CK(cudaMalloc(&e->h_io_d, (size_t)B * d * 4));
+    e->max_prefill = c.max_prefill;
+    if (c.max_prefill > 0) {
+      const int64_t T = c.max_prefill, sff = c.shared_ff;
+      if (c.dtype != EF_BF16) throw ValueError("prefill needs bf16 weights (tcgen05 grouped GEMM)");
+      if (d % 128 || c.ff % 128 || sff % 128)
+        throw ValueError("prefill needs d, ff and shared_ff multiples of 128");
+      CK(cudaMalloc(&e->px_d, T * d * 4));
+      CK(cudaMalloc(&e->plogits_d, (size_t)e->Rmax * T * M * 4));
+      CK(cudaMalloc(&e->pwts_d, T * k * 4));
+      CK(cudaMalloc(&e->py_d, T * k * d * 4));
+      CK(cudaMalloc(&e->psel_d, T * k * 4));
+      CK(cudaMalloc(&e->pcounts_d, (M + 1) * 4));
+      CK(cudaMalloc(&e->poffsets_d, (M + 1) * 4));
+      CK(cudaMalloc(&e->pperm_d, T * k * 4));
+      CK(cudaMalloc(&e->pinv_d, T * k * 4));
+      CK(cudaMalloc(&e->pA_d, T * std::max<int64_t>(k, 1) * d * 2));
+      CK(cudaMalloc(&e->pact_d, T * k * c.ff * 2));
+      if (sff) {
+        CK(cudaMalloc(&e->pys_d, T * d * 4));
+        CK(cudaMalloc(&e->pacts_d, T * sff * 2));
+        CK(cudaMalloc(&e->psgl_d, T * 4));
+      }
+      std::vector<int32_t> iota(T);
+      for (int64_t i = 0; i < T; ++i) iota[i] = (int32_t)i;
+      CK(cudaMalloc(&e->piota_d, T * 4));
+      CK(cudaMemcpy(e->piota_d, iota.data(), T * 4, cudaMemcpyHostToDevice));
+      CK(cudaHostAlloc(&e->plogits_h, (size_t)e->Rmax * T * M * 4, cudaHostAllocDefault));
+      CK(cudaHostAlloc(&e->psel_h, T * k * 4, cudaHostAllocDefault));
+      const int64_t widest = std::max<int64_t>({(int64_t)c.ff, (int64_t)d, sff});
+      e->ptiles_cap = ((T * k + 127) / 128 + M + 1) * ((widest + 127) / 128);
+      CK(cudaHostAlloc(&e->ptiles_h, sizeof(int4) * 4 * e->ptiles_cap, cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer((void**)&e->ptiles_hdev, e->ptiles_h, 0));
+      CK(cudaMalloc(&e->ptiles_d, sizeof(int4) * 4 * e->ptiles_cap));
+      CK(cudaEventCreateWithFlags(&e->copy_mark, cudaEventDisableTiming));
+    }
     CK(cudaMalloc(&e->logits_d, (size_t)e->Rmax * B * M * 4));
     CK(cudaMalloc(&e->sgl_d, (size_t)B * 4));
     CK(cudaMalloc(&e->wts_d, (size_t)B * k * 4));
@@ -910,6 +1123,15 @@ extern "C" int ef_engine_step_host(ef_engine* e, void* stream, const float* h_in
     std::vector<int64_t> t;
     if (tokens && n_tokens > 0) t.assign(tokens, tokens + n_tokens);
     e->step_host(reinterpret_cast<cudaStream_t>(stream), h_in, h_out, B, t);
+  });
+}
+
+extern "C" int ef_engine_prefill(ef_engine* e, void* stream, float* h, int T,
+                                 const int64_t* tokens, int n_tokens) {
+  EF_TRY({
+    std::vector<int64_t> t;
+    if (tokens && n_tokens > 0) t.assign(tokens, tokens + n_tokens);
+    e->prefill(reinterpret_cast<cudaStream_t>(stream), h, T, t);
   });
 }
 

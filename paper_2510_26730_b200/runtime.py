@@ -87,11 +87,12 @@ class MoEEngine:
                  routing_bias: float = 0.0, staging_slots: Optional[int] = None,
                  forest: Optional[ForestModel] = None, table: Optional[EmbeddingTable] = None,
                  emit_events: bool = False, timing: bool = False, record_routing: bool = False,
-                 device: int = 0):
+                 device: int = 0, max_prefill: int = 0):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
         self.max_batch = max_batch
+        self.max_prefill = max_prefill
         self.emit_events = emit_events
         self.device = torch.device("cuda", device)
         model = cfg.model_spec()
@@ -116,12 +117,14 @@ class MoEEngine:
         ec.budget_slots = budget_experts
         # landing slot for the one in-flight transfer + slots pinned by the
         # current layer after an in-layer eviction
-        ec.staging_slots = staging_slots or (2 + min(max_batch * cfg.top_k, cfg.num_experts))
+        ec.staging_slots = staging_slots or (
+            2 + min(max(max_batch, max_prefill) * cfg.top_k, cfg.num_experts))
         ec.routing_bias = routing_bias
         ec.seed = seed
         ec.device = device
         ec.timing = int(timing)
         ec.record_routing = int(record_routing)
+        ec.max_prefill = int(max_prefill)
         torch.cuda.set_device(device)
         torch.cuda.init()
         h = L.vp()
@@ -146,6 +149,24 @@ class MoEEngine:
         L.check(L.lib.ef_engine_step(self._h.ptr, C.c_void_p(stream), C.c_void_p(h.data_ptr()),
                                      B, L.as_ptr(toks, C.c_int64),
                                      len(token_ids) if token_ids else 0))
+        return h
+
+    def prefill(self, h: torch.Tensor, token_ids: Optional[Sequence[int]] = None) -> torch.Tensor:
+        """Prefill T <= max_prefill tokens: h[T, d] (fp32, on this device) <- MoE
+        stack(h), in place.  One scheduler step with one routing group per
+        token; the expert FFNs run on the tcgen05/TMA grouped GEMM (bf16
+        engines only).  Later step() calls continue from the same cache."""
+        if h.device != self.device or h.dtype != torch.float32 or not h.is_contiguous():
+            raise ValueError("h must be a contiguous fp32 tensor on the engine's device")
+        T, d = h.shape
+        if d != self.cfg.d_model:
+            raise ValueError(f"hidden width {d} != d_model {self.cfg.d_model}")
+        toks = L.i64arr(list(token_ids) if token_ids else [0])
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        L._pending_exc.clear()
+        L.check(L.lib.ef_engine_prefill(self._h.ptr, C.c_void_p(stream), C.c_void_p(h.data_ptr()),
+                                        T, L.as_ptr(toks, C.c_int64),
+                                        len(token_ids) if token_ids else 0))
         return h
 
     def step_host(self, h_in: torch.Tensor, h_out: Optional[torch.Tensor] = None,
@@ -203,10 +224,12 @@ class MoEEngine:
                                             C.byref(B), C.byref(lo), C.byref(hi), C.byref(n)))
         out = []
         M, k = self.cfg.num_experts, self.cfg.top_k
-        Rmax = self.cfg.num_layers
         for i in range(n.value):
-            lg = np.empty(Rmax * self.max_batch * M, dtype=np.float32)
-            sel = np.empty(self.max_batch * k, dtype=np.int32)
+            L.check(L.lib.ef_engine_routing_log(self._h.ptr, i, None, 0, None, 0, C.byref(R),
+                                                C.byref(B), C.byref(lo), C.byref(hi),
+                                                C.byref(n)))
+            lg = np.empty(max(1, R.value * B.value * M), dtype=np.float32)
+            sel = np.empty(max(1, B.value * k), dtype=np.int32)
             L.check(L.lib.ef_engine_routing_log(self._h.ptr, i, L.as_ptr(lg, C.c_float), lg.size,
                                                 L.as_ptr(sel, C.c_int32), sel.size, C.byref(R),
                                                 C.byref(B), C.byref(lo), C.byref(hi),

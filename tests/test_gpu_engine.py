@@ -238,3 +238,48 @@ def test_step_host_matches_device_step():
         assert torch.equal(hin2, h2.cpu()), t
     with pytest.raises(ValueError):
         e_host.step_host(torch.zeros(3, cfg.d_model))  # not pinned
+
+
+@pytest.mark.parametrize("shape", ["tiny", "qwen"])
+def test_prefill_then_decode_parity(shape):
+    """Prefill (tcgen05/TMA grouped GEMM path) of T tokens as one scheduler
+    step, then decode steps from the same cache: every decision bit-exact
+    with the oracle replay, every output within the bf16 tolerance."""
+    if shape == "tiny":
+        cfg, T, B, budget = PRESETS["tiny-bf16"], 96, 2, 12
+    else:
+        cfg = MoEConfig("qwen-2l", 2, 60, 4, 2048, 1408, dtype="bf16", route_mode="softmax_topk",
+                        shared_ff=5632, shared_gate=True)
+        T, B, budget = 160, 4, 80
+    pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
+    link_bw, layer_s, seed = 4 * ef.GB, 2e-4, 3
+    eng = MoEEngine(cfg, budget_experts=budget, policy=pol, link_bw=link_bw, layer_time_s=layer_s,
+                    max_batch=B, seed=seed, record_routing=True, emit_events=True, max_prefill=T)
+    hs_in, hs_out, toks = [], [], []
+    h = synthetic_hidden(cfg, seed, 0, T, DEV)
+    hs_in.append(h.cpu().numpy())
+    eng.prefill(h, list(range(T)))
+    torch.cuda.synchronize()
+    hs_out.append(h.cpu().numpy())
+    toks.append(tuple(range(T)))
+    for t in range(1, 3):
+        h = synthetic_hidden(cfg, seed, t, B, DEV)
+        hs_in.append(h.cpu().numpy())
+        eng.step(h, [1000 + t])
+        torch.cuda.synchronize()
+        hs_out.append(h.cpu().numpy())
+        toks.append((1000 + t,))
+    log = eng.routing_log()
+    assert len(log) == 3 * cfg.num_layers
+    assert log[0][1].shape == (T, cfg.top_k)
+    st, mask_bad, sel_bad = _replay(log, cfg, budget, link_bw, layer_s, pol, toks, 0.0, None, None)
+    assert not mask_bad and not sel_bad
+    got = R.product_metrics_dict(eng.metrics(), eng.cache_events())
+    assert R.diff_dicts(got, R.oracle_metrics_dict(st)) == []
+    w = N.ModelWeights(L=cfg.num_layers, M=cfg.num_experts, d=cfg.d_model, ff=cfg.d_ff,
+                       dtype=cfg.dtype, seed=seed, shared_ff=cfg.shared_ff,
+                       shared_gate=cfg.shared_gate)
+    for t in range(3):
+        ref = R.forward_step(hs_in[t], log, t, w, cfg.num_layers, cfg.top_k, cfg.route_mode)
+        assert R.rel_err(hs_out[t], ref) < 2e-2, t
+    assert eng.stats()["steps"] == 2
