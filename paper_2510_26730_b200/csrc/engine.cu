@@ -259,17 +259,23 @@ struct ef_engine {
   unsigned gate_seq = 0;
   std::vector<unsigned> layer_seq;  // gate sequence of each layer's current launch
   // EF_FUSE bit 16: device-side slot resolution.  The host mirrors phys_of +
-  // fill seq into a mapped table; the fused gate warp of layer l copies row
-  // l+1 into device memory once the host has decided layer l; route(l+1)
-  // resolves its experts from it and, if all are resident, starts FFN(l+1)
-  // without waiting for the host (whose decision still runs, pinning those
-  // slots until FFN(l+1) has finished).
-  int2* host_tab = nullptr;      // [L*M] {slot, fill seq}, mapped pinned
-  int2* host_tab_dev = nullptr;  // device alias
-  int2* dev_tab = nullptr;       // [L*M] device copy, refreshed row by row
+  // fill seq into a table; when it enqueues layer l (after deciding layer
+  // l-1) it passes row l by value in the router launch; route(l) resolves its
+  // experts from it and, if all are resident, FFN(l) starts without waiting
+  // for the host (whose decision still runs, pinning those slots until FFN(l)
+  // has finished) — no PCIe read on the critical path.
+  int2* host_tab = nullptr;      // [L*M] {slot, fill seq} host mirror of phys_of
+  int2* host_tab_dev = nullptr;  // device alias (unused by the kernels)
   unsigned* fast_words = nullptr;  // [L]
   int64_t fast_layers = 0;
+  // EF_ROUTER_PREFETCH=1: the gate warp bulk-prefetches the next router's rows
+  // into L2.  Off by default: one SM's bulk prefetches are slow (~0.3 TB/s)
+  // and the gate CTA, on the critical path of its kernel, waits for them.
+  bool router_prefetch = false;
   bool fast_path() const { return (fuse & 16) && (fuse & 3) == 3 && ffn_mode == 2 && !debug; }
+  // the gate folded into the up kernel waits for go >= its launch sequence
+  // number (monotonic); the separate gate kernel uses a 0/1 flag it resets
+  bool fused_gate() const { return (fuse & 2) && ffn_mode == 2; }
   void set_phys(int64_t i, int s) {
     phys_of[i] = s;
     host_tab[i] = make_int2(s, s >= 0 ? (int)slot_seq[s] : 0);
@@ -373,7 +379,7 @@ ef_engine::~ef_engine() {
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
-                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d, (void*)h_io_d, (void*)dev_tab,
+                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d, (void*)h_io_d,
                   (void*)fast_words, (void*)px_d, (void*)plogits_d, (void*)pwts_d, (void*)py_d,
                   (void*)pys_d, (void*)psgl_d, (void*)psel_d, (void*)pcounts_d, (void*)poffsets_d,
                   (void*)pperm_d, (void*)pinv_d, (void*)piota_d, pA_d, pact_d, pacts_d,
@@ -412,7 +418,9 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
     CombineIn ci{cur_h, y_d, cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, 1e-6f,
                  l > 0 ? stats_d + kStats * (l - 1) + 5 : nullptr};
     const bool fp = fast_path();
-    RouteFast rf{dev_tab + (int64_t)l * M, &dctrl[l], fast_words + l, layer_seq[l]};
+    RouteFast rf{&dctrl[l], fast_words + l, layer_seq[l], {}};
+    if (fp)
+      for (int e = 0; e < M; ++e) rf.tab[e] = host_tab[(int64_t)l * M + e];
     CKS(router_route_fused(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
                            B, d, M, logits_d, stats_d + kStats * l + 7, k, cfg.route_mode,
                            cfg.routing_bias, mask[0], mask[1], sel_d, wts_d, counts_d, offsets_d,
@@ -464,9 +472,9 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
       const int64_t rrows = (int64_t)std::min(4, cfg.L - nl) * M;
       io = GateIO{fast_words + l, sel_d, logits_d, B * k, layer_R[l] * B * M,
                   dev_of(out_sel(l)), dev_of(out_logits(l)),
-                  const_cast<uint32_t*>(&dev_of(out(l))->done), host_tab_dev + (int64_t)nl * M,
-                  dev_tab + (int64_t)nl * M, M,
-                  (const char*)router_w + (int64_t)nl * M * d * esz, rrows * d * esz};
+                  const_cast<uint32_t*>(&dev_of(out(l))->done), M,
+                  router_prefetch ? (const char*)router_w + (int64_t)nl * M * d * esz : nullptr,
+                  rrows * d * esz};
     }
     CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
                          reinterpret_cast<volatile unsigned*>(fuse_d + 2), layer_seq[l], ready,
@@ -508,7 +516,7 @@ void ef_engine::abort_pipeline(cudaStream_t stream, int from, int enq) {
   for (int j = from; j < enq; ++j) {
     hctrl[j].n_active = 0;
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    hctrl[j].go = 1u;
+    hctrl[j].go = fused_gate() ? layer_seq[j] : 1u;
   }
   cudaStreamSynchronize(stream);
   cudaStreamSynchronize(copy_stream);
@@ -520,8 +528,6 @@ void ef_engine::abort_pipeline(cudaStream_t stream, int from, int enq) {
   pinned_list.clear();
   for (int s : deferred_free) free_slots.push_back(s);
   deferred_free.clear();
-  // the device table may now lag the host's: no fast path until refreshed
-  cudaMemsetAsync(dev_tab, 0xff, sizeof(int2) * cfg.L * cfg.M, stream);
   cudaMemsetAsync(fast_words, 0, sizeof(unsigned) * cfg.L, stream);
   cudaStreamSynchronize(stream);
 }
@@ -697,7 +703,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       ffn_launches += 2;
       std::atomic_thread_fence(std::memory_order_seq_cst);
       _mm_sfence();
-      hc.go = 1u;
+      hc.go = fused_gate() ? layer_seq[l] : 1u;
       host_acc += std::chrono::duration<double, std::milli>(clk::now() - h0).count();
       // enqueue layer l+1 while FFN(l) runs: its horizon and bias mask are final now
       if (l + 1 < L) {
@@ -944,10 +950,6 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
   st->end_token();
   ++prefills;
   prefill_tokens += T;
-  // the decode fast path's device slot table lags the host mirror now
-  CKS(launch_host_io(stream, reinterpret_cast<const float*>(host_tab_dev),
-                     reinterpret_cast<float*>(dev_tab), (int64_t)L * M * 2, false));
-  ++launches;
 }
 
 extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
@@ -1091,13 +1093,13 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     CK(cudaHostAlloc(&e->host_tab, sizeof(int2) * L * M, cudaHostAllocMapped));
     for (int64_t i = 0; i < (int64_t)L * M; ++i) e->host_tab[i] = make_int2(-1, 0);
     CK(cudaHostGetDevicePointer((void**)&e->host_tab_dev, e->host_tab, 0));
-    CK(cudaMalloc(&e->dev_tab, sizeof(int2) * L * M));
-    CK(cudaMemset(e->dev_tab, 0xff, sizeof(int2) * L * M));
     CK(cudaMalloc(&e->fast_words, sizeof(unsigned) * L));
     CK(cudaMemset(e->fast_words, 0, sizeof(unsigned) * L));
     e->layer_seq.assign(L, 0);
     CK(cudaMalloc(&e->fuse_d, sizeof(int) * 4));
     CK(cudaMemset(e->fuse_d, 0, sizeof(int) * 4));
+    const char* rpf = getenv("EF_ROUTER_PREFETCH");
+    e->router_prefetch = rpf && rpf[0] == '1';
     const char* pdl = getenv("EF_PDL");
     ef::g_use_pdl = !(pdl && pdl[0] == '0');
     const char* fz = getenv("EF_FUSE");

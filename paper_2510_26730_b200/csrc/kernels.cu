@@ -577,7 +577,7 @@ __device__ void resolve_fast(const ef::RouteFast& rf, const int32_t* counts,
     const int e = e0 + lane;
     const int c = e < M ? __ldcg(counts + e) : 0;
     int2 t = make_int2(-1, 0);
-    if (c > 0) t = ld_volatile_v2(rf.tab_row + e);
+    if (c > 0) t = rf.tab[e];
     ok = ok && !__any_sync(0xffffffffu, c > 0 && t.x < 0);
     const unsigned m = __ballot_sync(0xffffffffu, c > 0);
     const int pos = base + __popc(m & ((1u << lane) - 1u));
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   if (ra.rf.dc && threadIdx.x < 32) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (lane + 32 * i < M) tabv[i] = ld_volatile_v2(ra.rf.tab_row + lane + 32 * i);
+      if (lane + 32 * i < M) tabv[i] = ra.rf.tab[lane + 32 * i];
   }
   pdl_wait();
   pdl_trigger();  // a tiny grid: let the FFN's CTAs be scheduled behind it
@@ -1040,39 +1040,31 @@ __device__ void gate_duty(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long
     }
   }
   const bool fast = io.fast_word && *reinterpret_cast<const volatile unsigned*>(io.fast_word) == seq;
+  if (fast) {  // the route kernel resolved every slot: nothing to wait for
+    if (stats && lane == 0) stats[1] = stats[8] = globaltimer();
+    __syncwarp();
+    return;
+  }
+  // slow path: the host's decision; go carries the layer's launch sequence
+  // number (monotonic), so no reset is needed
   uint2 gn = make_uint2(0, 0);
   if (lane == 0) {
     const long long c0 = clock64();
     for (;;) {
       gn = ld_acquire_sys_v2_(&hc->go);
-      if (gn.x != 0u) break;
+      if ((int)(gn.x - seq) >= 0) break;
       __nanosleep(64);
       if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
     }
     if (stats) stats[1] = globaltimer();
   }
-  if (!fast) {
-    const int n = __shfl_sync(0xffffffffu, (int)gn.y, 0);
-    for (int i = lane; i < n; i += 32) dc->ent[i] = ld_volatile_v4_(&hc->ent[i]);
-    __syncwarp();
-    if (lane == 0) {
-      dc->n_active = n;
-      __threadfence();
-      if (dflag) *dflag = seq;
-    }
-  }
-  __syncwarp();
-  if (io.tab_dst)  // the host's decision of this layer is final: refresh the next row
-    for (int e = lane; e < io.M; e += 32)
-      io.tab_dst[e] = ld_volatile_v2(io.tab_src + e);
-  if (io.router_next && lane == 0) {  // next router's weight rows: keep them in L2
-    const uint64_t pl = l2_evict_last_policy();
-    for (int64_t o = 0; o < io.router_bytes; o += 65536)
-      prefetch_l2_bulk(io.router_next + o, (uint32_t)(io.router_bytes - o < 65536 ? io.router_bytes - o : 65536), pl);
-  }
+  const int n = __shfl_sync(0xffffffffu, (int)gn.y, 0);
+  for (int i = lane; i < n; i += 32) dc->ent[i] = ld_volatile_v4_(&hc->ent[i]);
   __syncwarp();
   if (lane == 0) {
-    hc->go = 0u;
+    dc->n_active = n;
+    __threadfence();
+    if (dflag) *dflag = seq;
     if (stats) stats[8] = globaltimer();
   }
   __syncwarp();

@@ -28,23 +28,26 @@ struct DevCtrl {
 };
 
 // Device-side slot resolution by the route kernel (see resolve_fast).
+constexpr int kMaxTab = 128;
 struct RouteFast {
-  const int2* tab_row;  // device copy of this layer's slot table: {slot, fill seq}, slot -1
   DevCtrl* dc;          // this layer's decision block
   unsigned* fast_word;  // set to seq when every routed expert resolved, else 0
   unsigned seq;
+  // this layer's slot table row {slot, fill seq} (slot -1: not resident),
+  // passed by value in the launch: the host enqueues the router after it has
+  // decided the previous layer, so the row is final and needs no PCIe read
+  int2 tab[kMaxTab];
 };
 // Extra duties of the fused gate warp (up kernel CTA 0, warp 0).
 struct GateIO {
-  const unsigned* fast_word;  // == seq: decision already on the device, do not overwrite
+  const unsigned* fast_word;  // == seq: decision already on the device; the gate neither
+                              // waits for the host nor copies its decision
   const int32_t* sel_src;     // publish sel[n_sel] and logits rows[n_pub] to the host
   const float* logits_src;
   int n_sel, n_pub;
   int32_t* host_sel;
   float* host_logits;
   uint32_t* host_done;
-  const int2* tab_src;  // host slot-table row of the next layer (mapped) -> tab_dst
-  int2* tab_dst;
   int M;
   const char* router_next;  // next layer's router weight rows, prefetched into L2
   int64_t router_bytes;

@@ -22,7 +22,11 @@
     }                                                                                   \
   } while (0)
 
+#ifdef QWEN  // Qwen1.5-MoE / DeepSeek-V2-Lite expert shape, 4 routed experts (top-4 at B=1)
+constexpr int D = 2048, FF = 1408, E = 64, NA = 4;
+#else
 constexpr int D = 4096, FF = 14336, E = 16, NA = 2;
+#endif
 
 __device__ __forceinline__ uint4 ldw(const void* p) {
   uint4 r;
@@ -260,6 +264,18 @@ int main() {
     return ms * 1e3 / IT;  // us per iteration
   };
 
+#ifdef QWEN
+  std::vector<Up> ups = {
+      mk_up<2, 2, 4, false>("up R2 U2 W4 (engine)"), mk_up<1, 4, 4, false>("up R1 U4 W4"),
+      mk_up<1, 2, 4, false>("up R1 U2 W4"),          mk_up<1, 4, 2, false>("up R1 U4 W2"),
+      mk_up<1, 8, 4, false>("up R1 U8 W4"),          mk_up<1, 2, 2, false>("up R1 U2 W2"),
+  };
+  std::vector<Up> dns = {
+      mk_dn<1, 2, 4, false, true>("down R1 U2 W4 ldg (engine)"), mk_dn<1, 1, 4, false, true>("down R1 U1 W4 ldg"),
+      mk_dn<1, 4, 4, false, true>("down R1 U4 W4 ldg"),          mk_dn<1, 2, 2, false, true>("down R1 U2 W2 ldg"),
+      mk_dn<1, 1, 2, false, true>("down R1 U1 W2 ldg"),          mk_dn<2, 1, 4, false, true>("down R2 U1 W4 ldg"),
+  };
+#else
   std::vector<Up> ups = {
       mk_up<4, 1, 4, false>("up R4 U1 W4 (engine)"), mk_up<2, 2, 4, false>("up R2 U2 W4"),
       mk_up<2, 2, 2, false>("up R2 U2 W2"),          mk_up<2, 2, 8, false>("up R2 U2 W8"),
@@ -276,6 +292,7 @@ int main() {
       mk_sk<2, 4, 8>("down splitK2 U4 W8 smem"),          mk_sk<4, 1, 16>("down splitK4 U1 W16 smem"),
       mk_sk<7, 1, 14>("down splitK7 U1 W14 smem"),        mk_sk<2, 2, 16>("down splitK2 U2 W16 smem"),
   };
+#endif
   for (auto& u : ups) {
     float t = time_it([&](int i) {
       launch(u.fn, FF, u.rows_per_cta, u.threads, Args{w, (2 * i) % E, x, act, y}, s, false);
@@ -294,12 +311,20 @@ int main() {
     Up u, d;
     bool pdl;
   };
+#ifdef QWEN
+  std::vector<Pair> pairs = {
+      {"pair engine", mk_up<2, 2, 4, false>(""), mk_dn<1, 2, 4, false, true>(""), false},
+      {"pair R1U4 + R1U2", mk_up<1, 4, 4, false>(""), mk_dn<1, 2, 4, false, true>(""), false},
+      {"pair R1U4W2 + R1U1W2", mk_up<1, 4, 2, false>(""), mk_dn<1, 1, 2, false, true>(""), false},
+  };
+#else
   std::vector<Pair> pairs = {
       {"pair engine", mk_up<4, 1, 4, false>(""), mk_dn<1, 4, 4, false>(""), false},
       {"pair R2U2 + R1U2ldg", mk_up<2, 2, 4, false>(""), mk_dn<1, 2, 4, false, true>(""), false},
       {"pair R2U2 + sk2U2W8", mk_up<2, 2, 4, false>(""), mk_sk<2, 2, 8>(""), false},
       {"pair R2U2 + sk4U2W8", mk_up<2, 2, 4, false>(""), mk_sk<4, 2, 8>(""), false},
   };
+#endif
   for (auto& p : pairs) {
     float t = time_it([&](int i) {
       Args a{w, (2 * i) % E, x, act, y};
