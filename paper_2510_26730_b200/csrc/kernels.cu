@@ -1234,11 +1234,20 @@ template <typename WT, int NT>
 static void launch_ffn_nt(cudaStream_t st, const ActiveList& al, const CtrlSrc& cs, int n_active,
                           int d, int ff, const XGather<WT>& xg, WT* act, float* y,
                           const FuseArgs& fz_up, const FuseArgs& fz_dn) {
-  constexpr int R = kUpR, WARPS = 4;
+  constexpr int WARPS = 4;
   const int64_t es = sizeof(WT);
-  dim3 gu((ff + WARPS * R - 1) / (WARPS * R) + (fz_up.hc ? 1 : 0), n_active);
-  launch_k(ffn_gemv_kernel<WT, NT, R, true, XGather<WT>, kUpU>, gu, dim3(128), 0, st, al, cs,
-           fz_up, (int64_t)0, (int64_t)ff * d * es, ff, d, xg, act, (float*)nullptr, ff);
+  if (d <= 2048 && NT == 1) {
+    // short rows (Qwen / DeepSeek experts, d = 2048): one row x 4 chunks per
+    // warp keeps more warps streaming (tools/ffn_lab.cu -DQWEN: 4.47 vs 3.73 TB/s)
+    dim3 gu((ff + WARPS - 1) / WARPS + (fz_up.hc ? 1 : 0), n_active);
+    launch_k(ffn_gemv_kernel<WT, NT, 1, true, XGather<WT>, 4>, gu, dim3(128), 0, st, al, cs, fz_up,
+             (int64_t)0, (int64_t)ff * d * es, ff, d, xg, act, (float*)nullptr, ff);
+  } else {
+    constexpr int R = kUpR;
+    dim3 gu((ff + WARPS * R - 1) / (WARPS * R) + (fz_up.hc ? 1 : 0), n_active);
+    launch_k(ffn_gemv_kernel<WT, NT, R, true, XGather<WT>, kUpU>, gu, dim3(128), 0, st, al, cs,
+             fz_up, (int64_t)0, (int64_t)ff * d * es, ff, d, xg, act, (float*)nullptr, ff);
+  }
   // down projection: one W2 row per warp (d rows only: more rows per warp
   // left SMs idle on Mixtral's 4096 x 14336 W2)
   constexpr int RD = kDnR, UD = kDnU;
@@ -2180,6 +2189,7 @@ static void preload_dtype(int& n) {
   preload(ffn_stream_kernel<WT, 4>, n);
   preload(ffn_stream_kernel<WT, 8>, n);
   preload(ffn_gemv_kernel<WT, 1, kUpR, true, XGather<WT>, kUpU>, n);
+  preload(ffn_gemv_kernel<WT, 1, 1, true, XGather<WT>, 4>, n);
   preload(ffn_gemv_kernel<WT, 2, kUpR, true, XGather<WT>, kUpU>, n);
   preload(ffn_gemv_kernel<WT, 4, kUpR, true, XGather<WT>, kUpU>, n);
   preload(ffn_gemv_kernel<WT, 8, kUpR, true, XGather<WT>, kUpU>, n);
