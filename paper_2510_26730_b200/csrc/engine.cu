@@ -416,7 +416,7 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
   layer_seq[l] = ++gate_seq;
   if ((fuse & 1) && M <= 128) {
     CombineIn ci{cur_h, y_d, cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, 1e-6f,
-                 l > 0 ? stats_d + kStats * (l - 1) + 5 : nullptr};
+                 l > 0 ? stats_d + kStats * (l - 1) + 5 : nullptr, fused_gate()};
     const bool fp = fast_path();
     RouteFast rf{&dctrl[l], fast_words + l, layer_seq[l], {}};
     if (fp)
@@ -481,8 +481,8 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
                          stats_d + kStats * l, std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d,
                          y_d, &io));
     launches += 2;
-    if (!comb_next) {
-      CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
+    if (!comb_next) {  // y is in slot order after the fused FFN: no inv
+      CKS(combine_stamped(stream, h, x_d, y_d, nullptr, wts_d, cfg.shared_ff ? ys_d : nullptr,
                           sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
       ++launches;
     }

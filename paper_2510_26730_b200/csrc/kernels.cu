@@ -140,11 +140,11 @@ __global__ void rmsnorm_kernel(const float* __restrict__ h, float* __restrict__ 
 // vout (may alias h[t]); returns the block-wide sum of v^2.  float4 lanes with
 // P passes in flight so the L2 round trips overlap (d % 4 == 0).  Any block
 // size; all threads of the block must call it.
+template <int P = 4>
 __device__ float combine_row(int t, const float* h, float* vout, const float* __restrict__ y,
                              const int32_t* __restrict__ inv, const float* __restrict__ wts,
                              const float* __restrict__ ys, const float* __restrict__ gate_logit,
                              int d, int k, float* red) {
-  constexpr int P = 4;
   const float g = gate_logit ? 1.0f / (1.0f + expf(-gate_logit[t])) : 1.f;
   const float* hr = h + (int64_t)t * d;
   const int step = blockDim.x * 4;
@@ -156,7 +156,7 @@ __device__ float combine_row(int t, const float* h, float* vout, const float* __
   for (int r = 0; r < 16; ++r)
     if (r < k) {
       wr_s[r] = __ldcg(wts + t * k + r);
-      ir_s[r] = __ldcg(inv + t * k + r);
+      ir_s[r] = inv ? __ldcg(inv + t * k + r) : t * k + r;  // inv null: y in slot order
     }
   for (int base = threadIdx.x * 4; base < d; base += step * P) {
     float4 hv[P], sv[P], acc[P];
@@ -857,6 +857,111 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     resolve_fast(ra.rf, ra.counts, ra.offsets, M, ra.stamp_route ? ra.stamp_route + 5 : nullptr);
 }
 
+// B = 1 variant: one CTA per router row, its 4 warps splitting the row, so
+// each SM reads the hidden vector once (the warp-per-row kernel is bound by
+// shared-memory bandwidth at B = 1: 8 warps x 16 KB per SM, tools/router_lab.cu)
+// and the rows spread over R*M SMs.  Same ticket / route / combine contract.
+template <typename WT>
+__global__ void __launch_bounds__(128) router_route_row_kernel(const float* __restrict__ x,
+                                                               const WT* __restrict__ w, int rows,
+                                                               int d, float* __restrict__ logits,
+                                                               unsigned long long* stamp,
+                                                               RouteArgs ra, CombArgs cb) {
+  constexpr int V = WTraits<WT>::kPer16;
+  constexpr int UQ = 8;  // 16-byte chunks per lane in flight
+  const int M = ra.M;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int row = blockIdx.x;
+  const int span = d / 4;
+  const int cb0 = wid * span + lane * V;
+  const WT* wr = w + (int64_t)row * d;
+  uint4 wv0[UQ];
+#pragma unroll
+  for (int u = 0; u < UQ; ++u)
+    wv0[u] = u * 32 * V < span ? ld_stream16(wr + cb0 + u * 32 * V) : make_uint4(0, 0, 0, 0);
+  int2 tabv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tabv[i] = make_int2(-1, 0);
+  if (ra.rf.dc && threadIdx.x < 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < M) tabv[i] = ra.rf.tab[lane + 32 * i];
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) {
+    *stamp = gtimer();
+    stamp[8] = clock64();
+    stamp[7] = clock64();
+  }
+  extern __shared__ float hs[];
+  __shared__ float red[32], part[4];
+  __shared__ float invn_s;
+  __shared__ int last;
+  const bool comb = cb.h != nullptr;
+  if (comb) {
+    // 128 threads x 8 float4 passes: a 4096-wide row in one round of loads
+    const float ss = combine_row<8>(0, cb.h, hs, cb.y, cb.inv, cb.wts, cb.ys, cb.gate_logit, d,
+                                    cb.k, red);
+    if (threadIdx.x == 0) invn_s = 1.0f / sqrtf(ss / (float)d + cb.eps);
+    __syncthreads();
+  }
+  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) stamp[5] = clock64();
+  const float sc = comb ? invn_s : 1.f;
+  float p[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int c0 = 0; c0 < span; c0 += UQ * 32 * V) {
+#pragma unroll
+    for (int u = 0; u < UQ; ++u) {
+      const int cc = c0 + u * 32 * V;
+      if (cc < span) {
+        const uint4 wq = c0 == 0 ? wv0[u] : ld_stream16(wr + cb0 + cc);
+        float f[V];
+        WTraits<WT>::unpack(wq, f);
+        const int c = cb0 + cc;
+#pragma unroll
+        for (int q = 0; q < V / 4; ++q) {
+          float4 xv;
+          if (comb) {
+            xv = reinterpret_cast<const float4*>(hs + c)[q];
+            xv.x *= sc;
+            xv.y *= sc;
+            xv.z *= sc;
+            xv.w *= sc;
+          } else {
+            xv = __ldg(reinterpret_cast<const float4*>(x + c) + q);
+          }
+          p[u & 3] = fmaf(f[4 * q + 0], xv.x, p[u & 3]);
+          p[u & 3] = fmaf(f[4 * q + 1], xv.y, p[u & 3]);
+          p[u & 3] = fmaf(f[4 * q + 2], xv.z, p[u & 3]);
+          p[u & 3] = fmaf(f[4 * q + 3], xv.w, p[u & 3]);
+        }
+      }
+    }
+  }
+  float acc = warp_sum((p[0] + p[1]) + (p[2] + p[3]));
+  if (lane == 0) part[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    logits[row] = (part[0] + part[1]) + (part[2] + part[3]);  // B = 1: [r][0][m] = row
+    if (stamp && blockIdx.x == 0) stamp[6] = clock64();
+    __threadfence();
+    last = atomicAdd(ra.counter, 1) == (int)gridDim.x - 1;
+    if (last) __threadfence();
+  }
+  __syncthreads();
+  if (!last) return;
+  if (comb) {  // every CTA has read h: publish h and x for the rest of the layer
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      const float v = hs[i];
+      cb.h[i] = v;
+      cb.x_out[i] = v * invn_s;
+    }
+    if (cb.stamp && threadIdx.x == 0) *cb.stamp = gtimer();
+  }
+  if (threadIdx.x == 0) *ra.counter = 0;
+  route_small(logits, ra, tabv, ra.stamp_route);
+}
+
 namespace ef {
 int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
                        int d, int M, float* logits, unsigned long long* stamp_router, int k,
@@ -875,12 +980,22 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
                  "combine-in-router needs B*d*4 <= 128 KiB");
     // the previous layer's y / inv / wts are read before route_body of this
     // layer overwrites inv / wts (only the last CTA routes)
-    cb = CombArgs{ci->h, const_cast<float*>(x), ci->y, inv, wts, ci->ys, ci->gate_logit, k,
-                  ci->eps, ci->stamp};
+    cb = CombArgs{ci->h, const_cast<float*>(x), ci->y, ci->y_slot_order ? nullptr : inv, wts,
+                  ci->ys, ci->gate_logit, k, ci->eps, ci->stamp};
     smem = (size_t)B * d * 4;
   }
   const int rows = R * M, threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
+  const int vq = dtype == EF_BF16 ? 8 : 4;
+  if (B == 1 && d % (4 * 32 * vq) == 0 && k <= 32 && (!host_done || R == 1)) {
+    if (dtype == EF_BF16)
+      EF_CUDA_RET(launch_k(router_route_row_kernel<__nv_bfloat16>, dim3(rows), dim3(128), smem, st,
+                           x, (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb));
+    else
+      EF_CUDA_RET(launch_k(router_route_row_kernel<float>, dim3(rows), dim3(128), smem, st, x,
+                           (const float*)w, rows, d, logits, stamp_router, ra, cb));
+    return EF_OK;
+  }
   if (dtype == EF_BF16) {
     if (B == 1)
       EF_CUDA_RET(launch_k(router_route_kernel<__nv_bfloat16, 1>, dim3(blocks, 1), dim3(threads), smem, st, x,
@@ -999,6 +1114,9 @@ struct FuseArgs {
   volatile unsigned* dflag;
   unsigned seq;
   ef::GateIO io;
+  // down kernel: write y in (token, rank) slot order, y[perm[p]], so the
+  // combine needs no inverse-permutation lookup before loading y
+  const int32_t* y_perm;
 };
 
 __device__ __forceinline__ uint2 ld_acquire_sys_v2_(const volatile void* p) {
@@ -1212,7 +1330,7 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
               float s = g / (1.0f + expf(-g));
               WTraits<WT>::store(act_out + row * out_ld + j, s * u);
             } else {
-              y_out[row * out_ld + j] = g;
+              y_out[(fz.y_perm ? (int64_t)__ldg(fz.y_perm + row) : row) * out_ld + j] = g;
             }
           }
         }
@@ -1313,14 +1431,16 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
   ActiveList al{};
   CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
   FuseArgs fu{reinterpret_cast<volatile HostCtrl*>(hctrl_dev), reinterpret_cast<DevCtrl*>(dctrl),
-              dflag, seq, io ? *io : GateIO{}};
+              dflag, seq, io ? *io : GateIO{}, nullptr};
+  FuseArgs fd{};
+  fd.y_perm = perm;  // y in slot order (the engine's combine reads it without inv)
   if (dtype == EF_BF16) {
     XGather<__nv_bfloat16> xg{x, perm, k, d, false, 0};
     launch_ffn<__nv_bfloat16>(st, al, cs, max_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y,
-                              fu);
+                              fu, fd);
   } else {
     XGather<float> xg{x, perm, k, d, false, 0};
-    launch_ffn<float>(st, al, cs, max_active, max_rows, d, ff, xg, (float*)act, y, fu);
+    launch_ffn<float>(st, al, cs, max_active, max_rows, d, ff, xg, (float*)act, y, fu, fd);
   }
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
@@ -2176,6 +2296,9 @@ static void preload_dtype(int& n) {
   preload(router_kernel<WT, 8>, n);
   preload(router_route_kernel<WT, 1>, n);
   preload(router_route_kernel<WT, 8>, n);
+  preload(router_route_row_kernel<WT>, n);
+  cudaFuncSetAttribute(router_route_row_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kCombSmemMax);
   cudaFuncSetAttribute(router_route_kernel<WT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kCombSmemMax);
   cudaFuncSetAttribute(router_route_kernel<WT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -99,6 +99,7 @@ struct CombineIn {
   const float* gate_logit;
   float eps;
   unsigned long long* stamp;
+  bool y_slot_order;  // y rows indexed by (token, rank) slot (fused FFN), not by inv
 };
 // zero-copy hidden-state I/O between pinned host memory and HBM (SM loads/stores)
 int launch_host_io(cudaStream_t st, const float* src, float* dst, int64_t n, bool to_host);
