@@ -283,3 +283,15 @@ def test_prefill_then_decode_parity(shape):
         ref = R.forward_step(hs_in[t], log, t, w, cfg.num_layers, cfg.top_k, cfg.route_mode)
         assert R.rel_err(hs_out[t], ref) < 2e-2, t
     assert eng.stats()["steps"] == 2
+
+
+@pytest.mark.parametrize("fuse,pdl", [("0", "1"), ("1", "1"), ("3", "1"), ("11", "0"), ("27", "0"),
+                                      ("19", "1")])
+def test_pipeline_variants_parity(monkeypatch, fuse, pdl):
+    """Every EF_FUSE / EF_PDL combination of the decode pipeline (separate or
+    fused router+route, gate, combine-in-router, device-side slot resolution,
+    programmatic dependent launch) gives the oracle's decisions and outputs."""
+    monkeypatch.setenv("EF_FUSE", fuse)
+    monkeypatch.setenv("EF_PDL", pdl)
+    run_and_check(PRESETS["tiny"], ef.PolicyConfig("a", "adaptive", predictor="pregate"), B=2,
+                  steps=3, budget=12, link_bw=2 * ef.GB, layer_s=0.0002, bias=1e4)
