@@ -188,6 +188,101 @@ __global__ void __launch_bounds__(WARPS * 32) down_sk(Args a) {
   }
 }
 
+// Persistent fused FFN: one launch, CTAs claim tiles from a counter in the
+// order [up tiles of every expert][down tiles of every expert]; a down tile of
+// expert e waits until all of e's up tiles have published their act rows.
+struct PArgs {
+  const __nv_bfloat16* w;
+  int e0;
+  const float* x;
+  __nv_bfloat16* act;
+  float* y;
+  int* ctr;  // [0] tile ticket, [1 + e] finished up tiles of expert e
+};
+template <int UPR, int UPU, int DNU>
+__global__ void __launch_bounds__(128, 8) persist_k(PArgs a) {
+  constexpr int WARPS = 4;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int up_rows_per_tile = WARPS * UPR, dn_rows_per_tile = WARPS;
+  constexpr int up_tiles = FF / up_rows_per_tile, dn_tiles = D / dn_rows_per_tile;
+  constexpr int total = NA * (up_tiles + dn_tiles);
+  __shared__ int tile_s;
+  for (;;) {
+    if (threadIdx.x == 0) tile_s = atomicAdd(&a.ctr[0], 1);
+    __syncthreads();
+    const int tile = tile_s;
+    __syncthreads();
+    if (tile >= total) break;
+    if (tile < NA * up_tiles) {
+      const int ea = tile / up_tiles, tb = tile % up_tiles;
+      const int e = (a.e0 + ea) % E;
+      const __nv_bfloat16* W1 = a.w + (int64_t)e * 3 * FF * D;
+      const __nv_bfloat16* W3 = W1 + (int64_t)FF * D;
+      const int j0 = (tb * WARPS + wid) * UPR;
+      float ag[UPR], au[UPR];
+#pragma unroll
+      for (int r = 0; r < UPR; ++r) ag[r] = au[r] = 0.f;
+      for (int c0 = lane * 8; c0 < D; c0 += 32 * 8 * UPU) {
+        uint4 g[UPU][UPR], u[UPU][UPR];
+#pragma unroll
+        for (int v = 0; v < UPU; ++v)
+#pragma unroll
+          for (int r = 0; r < UPR; ++r) {
+            g[v][r] = ldw(W1 + (int64_t)(j0 + r) * D + c0 + v * 256);
+            u[v][r] = ldw(W3 + (int64_t)(j0 + r) * D + c0 + v * 256);
+          }
+#pragma unroll
+        for (int v = 0; v < UPU; ++v) {
+          const float4* xp = reinterpret_cast<const float4*>(a.x + c0 + v * 256);
+          float4 x0 = __ldg(xp), x1 = __ldg(xp + 1);
+#pragma unroll
+          for (int r = 0; r < UPR; ++r) {
+            ag[r] = dot8(g[v][r], x0, x1, ag[r]);
+            au[r] = dot8(u[v][r], x0, x1, au[r]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < UPR; ++r) {
+        float gg = wsum(ag[r]), uu = wsum(au[r]);
+        if (lane == 0)
+          a.act[ea * FF + j0 + r] = __float2bfloat16_rn(gg / (1.f + __expf(-gg)) * uu);
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(&a.ctr[1 + ea], 1);
+    } else {
+      const int t2 = tile - NA * up_tiles;
+      const int ea = t2 / dn_tiles, tb = t2 % dn_tiles;
+      if (threadIdx.x == 0) {
+        while (atomicAdd(&a.ctr[1 + ea], 0) < up_tiles) __nanosleep(100);
+      }
+      __syncthreads();
+      const int e = (a.e0 + ea) % E;
+      const __nv_bfloat16* W2 = a.w + (int64_t)e * 3 * FF * D + 2LL * FF * D;
+      const int i0 = tb * WARPS + wid;
+      const __nv_bfloat16* xa = a.act + ea * FF;
+      float acc = 0.f;
+      for (int c0 = lane * 8; c0 < FF; c0 += 32 * 8 * DNU) {
+        uint4 wv[DNU];
+#pragma unroll
+        for (int v = 0; v < DNU; ++v)
+          if (c0 + v * 256 < FF) wv[v] = ldw(W2 + (int64_t)i0 * FF + c0 + v * 256);
+#pragma unroll
+        for (int v = 0; v < DNU; ++v)
+          if (c0 + v * 256 < FF) {
+            uint4 xv = __ldcg(reinterpret_cast<const uint4*>(xa + c0 + v * 256));
+            float4 x0 = make_float4(lo(xv.x), hi(xv.x), lo(xv.y), hi(xv.y));
+            float4 x1 = make_float4(lo(xv.z), hi(xv.z), lo(xv.w), hi(xv.w));
+            acc = dot8(wv[v], x0, x1, acc);
+          }
+      }
+      acc = wsum(acc);
+      if (lane == 0) a.y[ea * D + i0] = acc;
+    }
+  }
+}
+
 __global__ void fill_k(__nv_bfloat16* w, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -333,6 +428,26 @@ int main() {
     });
     printf("%-28s %8.1f us %7.0f GB/s\n", p.name, t, (up_bytes + dn_bytes) / t * 1e-3);
   }
+  // persistent fused variant
+  int* ctr;
+  CK(cudaMalloc(&ctr, 64 * sizeof(int)));
+  int sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  auto persist_time = [&](auto kern, const char* name, int per_sm) {
+    float t = time_it([&](int i) {
+      CK(cudaMemsetAsync(ctr, 0, 64 * sizeof(int), s));
+      kern<<<sms * per_sm, 128, 0, s>>>(PArgs{w, (2 * i) % E, x, act, y, ctr});
+    });
+    printf("%-28s %8.1f us %7.0f GB/s\n", name, t, (up_bytes + dn_bytes) / t * 1e-3);
+  };
+#ifndef QWEN
+  persist_time(persist_k<2, 2, 2>, "persist 8/SM up2x2 dn2", 8);
+  persist_time(persist_k<2, 2, 2>, "persist 6/SM up2x2 dn2", 6);
+  persist_time(persist_k<2, 2, 4>, "persist 8/SM up2x2 dn4", 8);
+  persist_time(persist_k<1, 4, 2>, "persist 8/SM up1x4 dn2", 8);
+#else
+  persist_time(persist_k<1, 4, 2>, "persist 8/SM up1x4 dn2", 8);
+#endif
   // isolated pair (sync between iterations, as in the engine where each layer
   // is gated by the host): launch latency and ramp included
   for (auto& p : pairs) {
