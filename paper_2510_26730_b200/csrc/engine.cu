@@ -264,14 +264,9 @@ struct ef_engine {
   // experts from it and, if all are resident, FFN(l) starts without waiting
   // for the host (whose decision still runs, pinning those slots until FFN(l)
   // has finished) — no PCIe read on the critical path.
-  int2* host_tab = nullptr;      // [L*M] {slot, fill seq} host mirror of phys_of
-  int2* host_tab_dev = nullptr;  // device alias (unused by the kernels)
+  int2* host_tab = nullptr;  // [L*M] {slot, fill seq} host mirror of phys_of
   unsigned* fast_words = nullptr;  // [L]
   int64_t fast_layers = 0;
-  // EF_ROUTER_PREFETCH=1: the gate warp bulk-prefetches the next router's rows
-  // into L2.  Off by default: one SM's bulk prefetches are slow (~0.3 TB/s)
-  // and the gate CTA, on the critical path of its kernel, waits for them.
-  bool router_prefetch = false;
   bool fast_path() const { return (fuse & 16) && (fuse & 3) == 3 && ffn_mode == 2 && !debug; }
   // the gate folded into the up kernel waits for go >= its launch sequence
   // number (monotonic); the separate gate kernel uses a 0/1 flag it resets
@@ -466,15 +461,9 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   if ((fuse & 2) && ffn_mode == 2) {
     GateIO io{};
     if (fast_path()) {
-      const int nl = (l + 1) % cfg.L;
-      // rows the next router will most likely read: its layer plus up to 3
-      // pre-gate layers (the horizon is decided later)
-      const int64_t rrows = (int64_t)std::min(4, cfg.L - nl) * M;
       io = GateIO{fast_words + l, sel_d, logits_d, B * k, layer_R[l] * B * M,
                   dev_of(out_sel(l)), dev_of(out_logits(l)),
-                  const_cast<uint32_t*>(&dev_of(out(l))->done), M,
-                  router_prefetch ? (const char*)router_w + (int64_t)nl * M * d * esz : nullptr,
-                  rrows * d * esz};
+                  const_cast<uint32_t*>(&dev_of(out(l))->done), M};
     }
     CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
                          reinterpret_cast<volatile unsigned*>(fuse_d + 2), layer_seq[l], ready,
@@ -1090,16 +1079,13 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     if (ffn && std::string(ffn) == "persistent") e->ffn_mode = 1;
     if (ffn && std::string(ffn) == "stream") e->ffn_mode = 0;
     CK(cudaMalloc(&e->counters_d, sizeof(int) * (kMaxActive + 1)));
-    CK(cudaHostAlloc(&e->host_tab, sizeof(int2) * L * M, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&e->host_tab, sizeof(int2) * L * M, cudaHostAllocDefault));
     for (int64_t i = 0; i < (int64_t)L * M; ++i) e->host_tab[i] = make_int2(-1, 0);
-    CK(cudaHostGetDevicePointer((void**)&e->host_tab_dev, e->host_tab, 0));
     CK(cudaMalloc(&e->fast_words, sizeof(unsigned) * L));
     CK(cudaMemset(e->fast_words, 0, sizeof(unsigned) * L));
     e->layer_seq.assign(L, 0);
     CK(cudaMalloc(&e->fuse_d, sizeof(int) * 4));
     CK(cudaMemset(e->fuse_d, 0, sizeof(int) * 4));
-    const char* rpf = getenv("EF_ROUTER_PREFETCH");
-    e->router_prefetch = rpf && rpf[0] == '1';
     const char* pdl = getenv("EF_PDL");
     ef::g_use_pdl = !(pdl && pdl[0] == '0');
     const char* fz = getenv("EF_FUSE");

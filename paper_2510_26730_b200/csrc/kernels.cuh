@@ -25,11 +25,6 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ uint4 ld_stream16_ef(const void* p, uint64_t pol) {
   uint4 r;
   asm volatile(
@@ -38,13 +33,6 @@ __device__ __forceinline__ uint4 ld_stream16_ef(const void* p, uint64_t pol) {
       : "l"(p), "l"(pol));
   return r;
 }
-// bulk prefetch of [p, p+bytes) into L2 with a cache policy (bytes % 16 == 0)
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes),
-               "l"(pol)
-               : "memory");
-}
-
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"

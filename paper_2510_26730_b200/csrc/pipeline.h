@@ -49,8 +49,6 @@ struct GateIO {
   float* host_logits;
   uint32_t* host_done;
   int M;
-  const char* router_next;  // next layer's router weight rows, prefetched into L2
-  int64_t router_bytes;
 };
 struct HostOut {  // followed by sel[B*k] int32 and logits[B*M] f32
   volatile uint32_t done;
