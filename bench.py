@@ -238,9 +238,21 @@ def run_ours(args, cfg, bias):
                              predictor=args.predictor if args.strategy != "static" else "none",
                              cache_aware_routing=True)
     t_init = time.perf_counter()
-    eng = MoEEngine(cfg, budget_experts=budget, policy=policy, link_bw=link_bw,
-                    layer_time_s=layer_s, max_batch=B, seed=args.seed, routing_bias=bias,
-                    timing=True, device=local)
+    kw = dict(budget_experts=budget, policy=policy, link_bw=link_bw, layer_time_s=layer_s,
+              max_batch=B, seed=args.seed, routing_bias=bias, timing=True, device=local)
+    if world > 1:
+        # replicas share one pinned host expert store per node (POSIX shm):
+        # rank 0 creates and fills it, the others attach once it is filled
+        shm = f"/ef_store_{os.environ.get('MASTER_PORT', '0')}_{cfg.name}"
+        if rank == 0:
+            eng = MoEEngine(cfg, host_store_shm=shm, **kw)
+            dist.barrier()
+        else:
+            dist.barrier()
+            eng = MoEEngine(cfg, host_store_shm=shm, host_store_attach=True, **kw)
+        dist.barrier()
+    else:
+        eng = MoEEngine(cfg, **kw)
     init_s = time.perf_counter() - t_init
 
     # decode inputs: AR(1) in time with correlation rho, unit variance, in HBM

@@ -292,6 +292,9 @@ typedef struct ef_engine_cfg {
   int32_t timing; /* record per-layer stall events (physical stall %) */
   int32_t record_routing; /* keep every layer's logits / selection for parity checks */
   int32_t max_prefill;    /* > 0: allocate prefill buffers for up to this many tokens (bf16) */
+  const char* host_store_shm; /* non-null: pinned host expert store in POSIX shared memory of
+                                 this name, shared by the processes of one node */
+  int32_t host_store_attach;  /* 1: attach to a store another process created and filled */
 } ef_engine_cfg;
 int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim, const ef_ladder_cfg* ladder,
                      ef_engine** out);

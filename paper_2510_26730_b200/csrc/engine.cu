@@ -28,6 +28,10 @@
 #include <cuda_runtime.h>
 #include <immintrin.h>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -142,6 +146,10 @@ struct ef_engine {
     }
   }
   std::vector<char*> store;  // per layer: M * stride bytes
+  void* shm_base = nullptr;  // shared store (ef_engine_cfg.host_store_shm)
+  size_t shm_bytes = 0;
+  std::string shm_name;      // set by the creating process, which unlinks it
+  bool store_filled = false;  // attached to a store another process filled
   cudaStream_t copy_stream = nullptr, side_stream = nullptr;
   // slot table
   std::vector<int32_t> phys_of;    // [L*M] -> slot or -1
@@ -332,6 +340,11 @@ void ef_engine::init_weights() {
                             ef_stream_key(cfg.seed, l, 0, 7), scale_for(d), 0));
     }
   }
+  if (store_filled) {  // experts already generated by the process that created the store
+    CK(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+    return;
+  }
   // experts: generate on device (two staging buffers), copy into the pinned store
   char* stage[2];
   cudaEvent_t done[2];
@@ -384,8 +397,14 @@ ef_engine::~ef_engine() {
   for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring, (void*)host_tab,
                   (void*)plogits_h, (void*)psel_h, (void*)ptiles_h})
     if (p) cudaFreeHost(p);
-  for (char* p : store)
-    if (p) cudaFreeHost(p);
+  if (shm_base) {
+    cudaHostUnregister(shm_base);
+    munmap(shm_base, shm_bytes);
+    if (!shm_name.empty()) shm_unlink(shm_name.c_str());
+  } else {
+    for (char* p : store)
+      if (p) cudaFreeHost(p);
+  }
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (side_stream) cudaStreamDestroy(side_stream);
   if (compute_stream) cudaStreamDestroy(compute_stream);
@@ -1054,8 +1073,30 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     CK(cudaHostAlloc(&e->logits_h, (size_t)e->Rmax * B * M * 4, cudaHostAllocDefault));
     CK(cudaHostAlloc(&e->seq_ring, sizeof(uint32_t) * ef_engine::kSeqRing, cudaHostAllocDefault));
     e->store.assign(L, nullptr);
-    for (int l = 0; l < L; ++l)
-      CK(cudaHostAlloc(&e->store[l], (size_t)M * e->stride, cudaHostAllocDefault));
+    if (c.host_store_shm && c.host_store_shm[0]) {
+      // one pinned host store shared by every process on the node (replica
+      // ranks): POSIX shared memory, registered with CUDA in each process
+      const size_t bytes = (size_t)L * M * e->stride;
+      const bool create = !c.host_store_attach;
+      int fd = shm_open(c.host_store_shm, create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+      if (fd < 0) throw RuntimeErr(std::string("shm_open failed for ") + c.host_store_shm);
+      if (create && ftruncate(fd, (off_t)bytes) != 0) {
+        close(fd);
+        throw RuntimeErr("ftruncate of the shared host store failed (is /dev/shm large enough?)");
+      }
+      void* base = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+      close(fd);
+      if (base == MAP_FAILED) throw RuntimeErr("mmap of the shared host store failed");
+      e->shm_base = base;
+      e->shm_bytes = bytes;
+      if (create) e->shm_name = c.host_store_shm;
+      CK(cudaHostRegister(base, bytes, cudaHostRegisterDefault));
+      for (int l = 0; l < L; ++l) e->store[l] = (char*)base + (size_t)l * M * e->stride;
+      e->store_filled = !create;
+    } else {
+      for (int l = 0; l < L; ++l)
+        CK(cudaHostAlloc(&e->store[l], (size_t)M * e->stride, cudaHostAllocDefault));
+    }
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     CK(cudaStreamCreateWithPriority(&e->copy_stream, cudaStreamNonBlocking, prio_hi));

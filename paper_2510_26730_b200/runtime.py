@@ -87,7 +87,8 @@ class MoEEngine:
                  routing_bias: float = 0.0, staging_slots: Optional[int] = None,
                  forest: Optional[ForestModel] = None, table: Optional[EmbeddingTable] = None,
                  emit_events: bool = False, timing: bool = False, record_routing: bool = False,
-                 device: int = 0, max_prefill: int = 0):
+                 device: int = 0, max_prefill: int = 0, host_store_shm: Optional[str] = None,
+                 host_store_attach: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
@@ -125,6 +126,11 @@ class MoEEngine:
         ec.timing = int(timing)
         ec.record_routing = int(record_routing)
         ec.max_prefill = int(max_prefill)
+        # one pinned host store per node for replica ranks: the first process
+        # creates and fills it, the others attach (bench.py --gpus N)
+        self._shm_name = host_store_shm.encode() if host_store_shm else None
+        ec.host_store_shm = self._shm_name
+        ec.host_store_attach = int(host_store_attach)
         torch.cuda.set_device(device)
         torch.cuda.init()
         h = L.vp()

@@ -295,3 +295,25 @@ def test_pipeline_variants_parity(monkeypatch, fuse, pdl):
     monkeypatch.setenv("EF_PDL", pdl)
     run_and_check(PRESETS["tiny"], ef.PolicyConfig("a", "adaptive", predictor="pregate"), B=2,
                   steps=3, budget=12, link_bw=2 * ef.GB, layer_s=0.0002, bias=1e4)
+
+
+def test_shared_host_store_attach():
+    """Two engines on one node sharing one pinned host expert store (POSIX
+    shared memory): the second attaches to the store the first filled and
+    decodes identically (the replica path of bench.py --gpus N)."""
+    import os
+    cfg = PRESETS["tiny-bf16"]
+    pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
+    kw = dict(budget_experts=12, policy=pol, link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2,
+              seed=9, routing_bias=1e4)
+    name = f"/ef_test_store_{os.getpid()}"
+    a = MoEEngine(cfg, host_store_shm=name, **kw)
+    b = MoEEngine(cfg, host_store_shm=name, host_store_attach=True, **kw)
+    for t in range(4):
+        h1 = synthetic_hidden(cfg, 9, t, 2, DEV)
+        h2 = h1.clone()
+        a.step(h1)
+        b.step(h2)
+        torch.cuda.synchronize()
+        assert torch.equal(h1, h2), t
+    assert a.stats()["copies"] == b.stats()["copies"] > 0
