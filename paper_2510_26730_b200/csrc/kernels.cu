@@ -160,6 +160,8 @@ __device__ float combine_row(int t, const float* h, float* vout, const float* __
     }
   for (int base = threadIdx.x * 4; base < d; base += step * P) {
     float4 hv[P], sv[P], acc[P];
+    float4 y0[P];  // rank 0's row, issued with h so both land in one round trip
+    const float* yr0 = y + (int64_t)ir_s[0] * d;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int i = base + p * step;
@@ -167,10 +169,18 @@ __device__ float combine_row(int t, const float* h, float* vout, const float* __
       if (i < d) {
         hv[p] = __ldcg(reinterpret_cast<const float4*>(hr + i));
         if (ys) sv[p] = __ldcg(reinterpret_cast<const float4*>(ys + (int64_t)t * d + i));
+        y0[p] = __ldcg(reinterpret_cast<const float4*>(yr0 + i));
       }
     }
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+    for (int p = 0; p < P; ++p) {
+      acc[p].x = fmaf(wr_s[0], y0[p].x, acc[p].x);
+      acc[p].y = fmaf(wr_s[0], y0[p].y, acc[p].y);
+      acc[p].z = fmaf(wr_s[0], y0[p].z, acc[p].z);
+      acc[p].w = fmaf(wr_s[0], y0[p].w, acc[p].w);
+    }
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
       if (r >= k) break;
       const float w = wr_s[r];
       const float* yr = y + (int64_t)ir_s[r] * d;
