@@ -160,8 +160,11 @@ __device__ float combine_row(int t, const float* h, float* vout, const float* __
     }
   for (int base = threadIdx.x * 4; base < d; base += step * P) {
     float4 hv[P], sv[P], acc[P];
-    float4 y0[P];  // rank 0's row, issued with h so both land in one round trip
+    // the first two ranks' y rows are issued with h, so at top-2 every load
+    // of the row lands in one round trip
+    float4 y0[P], y1[P];
     const float* yr0 = y + (int64_t)ir_s[0] * d;
+    const float* yr1 = y + (int64_t)ir_s[k > 1 ? 1 : 0] * d;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int i = base + p * step;
@@ -170,6 +173,7 @@ __device__ float combine_row(int t, const float* h, float* vout, const float* __
         hv[p] = __ldcg(reinterpret_cast<const float4*>(hr + i));
         if (ys) sv[p] = __ldcg(reinterpret_cast<const float4*>(ys + (int64_t)t * d + i));
         y0[p] = __ldcg(reinterpret_cast<const float4*>(yr0 + i));
+        if (k > 1) y1[p] = __ldcg(reinterpret_cast<const float4*>(yr1 + i));
       }
     }
 #pragma unroll
@@ -178,9 +182,15 @@ __device__ float combine_row(int t, const float* h, float* vout, const float* __
       acc[p].y = fmaf(wr_s[0], y0[p].y, acc[p].y);
       acc[p].z = fmaf(wr_s[0], y0[p].z, acc[p].z);
       acc[p].w = fmaf(wr_s[0], y0[p].w, acc[p].w);
+      if (k > 1) {
+        acc[p].x = fmaf(wr_s[1], y1[p].x, acc[p].x);
+        acc[p].y = fmaf(wr_s[1], y1[p].y, acc[p].y);
+        acc[p].z = fmaf(wr_s[1], y1[p].z, acc[p].z);
+        acc[p].w = fmaf(wr_s[1], y1[p].w, acc[p].w);
+      }
     }
 #pragma unroll
-    for (int r = 1; r < 16; ++r) {
+    for (int r = 2; r < 16; ++r) {
       if (r >= k) break;
       const float w = wr_s[r];
       const float* yr = y + (int64_t)ir_s[r] * d;
@@ -872,7 +882,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
 // shared-memory bandwidth at B = 1: 8 warps x 16 KB per SM, tools/router_lab.cu)
 // and the rows spread over R*M SMs.  Same ticket / route / combine contract.
 template <typename WT>
-__global__ void __launch_bounds__(128) router_route_row_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(256) router_route_row_kernel(const float* __restrict__ x,
                                                                const WT* __restrict__ w, int rows,
                                                                int d, float* __restrict__ logits,
                                                                unsigned long long* stamp,
@@ -882,7 +892,7 @@ __global__ void __launch_bounds__(128) router_route_row_kernel(const float* __re
   const int M = ra.M;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int row = blockIdx.x;
-  const int span = d / 4;
+  const int span = d / 8;  // 8 warps split the row
   const int cb0 = wid * span + lane * V;
   const WT* wr = w + (int64_t)row * d;
   uint4 wv0[UQ];
@@ -905,13 +915,13 @@ __global__ void __launch_bounds__(128) router_route_row_kernel(const float* __re
     stamp[7] = clock64();
   }
   extern __shared__ float hs[];
-  __shared__ float red[32], part[4];
+  __shared__ float red[32], part[8];
   __shared__ float invn_s;
   __shared__ int last;
   const bool comb = cb.h != nullptr;
   if (comb) {
-    // 128 threads x 8 float4 passes: a 4096-wide row in one round of loads
-    const float ss = combine_row<8>(0, cb.h, hs, cb.y, cb.inv, cb.wts, cb.ys, cb.gate_logit, d,
+    // 256 threads x 4 float4 passes: a 4096-wide row in one round of loads
+    const float ss = combine_row<4>(0, cb.h, hs, cb.y, cb.inv, cb.wts, cb.ys, cb.gate_logit, d,
                                     cb.k, red);
     if (threadIdx.x == 0) invn_s = 1.0f / sqrtf(ss / (float)d + cb.eps);
     __syncthreads();
@@ -952,7 +962,8 @@ __global__ void __launch_bounds__(128) router_route_row_kernel(const float* __re
   if (lane == 0) part[wid] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    logits[row] = (part[0] + part[1]) + (part[2] + part[3]);  // B = 1: [r][0][m] = row
+    logits[row] = ((part[0] + part[1]) + (part[2] + part[3])) +
+                  ((part[4] + part[5]) + (part[6] + part[7]));  // B = 1: [r][0][m] = row
     if (stamp && blockIdx.x == 0) stamp[6] = clock64();
     __threadfence();
     last = atomicAdd(ra.counter, 1) == (int)gridDim.x - 1;
@@ -997,12 +1008,12 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
   const int rows = R * M, threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
   const int vq = dtype == EF_BF16 ? 8 : 4;
-  if (B == 1 && d % (4 * 32 * vq) == 0 && k <= 32 && (!host_done || R == 1)) {
+  if (B == 1 && d % (8 * 32 * vq) == 0 && k <= 32 && (!host_done || R == 1)) {
     if (dtype == EF_BF16)
-      EF_CUDA_RET(launch_k(router_route_row_kernel<__nv_bfloat16>, dim3(rows), dim3(128), smem, st,
+      EF_CUDA_RET(launch_k(router_route_row_kernel<__nv_bfloat16>, dim3(rows), dim3(256), smem, st,
                            x, (const __nv_bfloat16*)w, rows, d, logits, stamp_router, ra, cb));
     else
-      EF_CUDA_RET(launch_k(router_route_row_kernel<float>, dim3(rows), dim3(128), smem, st, x,
+      EF_CUDA_RET(launch_k(router_route_row_kernel<float>, dim3(rows), dim3(256), smem, st, x,
                            (const float*)w, rows, d, logits, stamp_router, ra, cb));
     return EF_OK;
   }
