@@ -780,13 +780,15 @@ void ef_engine::fold_stats(int i) {
       char line[320];
       snprintf(line, sizeof line,
               "layer %2d router %5.1f route %5.1f pub->gate %5.1f wait %6.1f gate %5.1f "
-              "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f%s\n",
+              "gate->up %5.1f ready %5.1f ffn %7.1f stall %7.1f combine %5.1f period %6.1f "
+              "route->ffn %5.1f ffn->router %5.1f%s\n",
               j, us(sj[7], sj[6]), us(sj[6], sj[9]), us(sj[9], sj[0]), us(sj[0], sj[1]),
               us(sj[1], sj[8]), sj[10] != ~0ull ? us(sj[8], sj[10]) : 0.0,
               sj[3] != ~0ull && sj[10] != ~0ull ? us(sj[10], sj[3]) : 0.0,
               sj[3] != ~0ull ? us(sj[3], sj[4]) : 0.0, sj[2] * 1e-3, us(sj[4], sj[5]),
               j + 1 < L ? us(sj[7], stats_h[kStats * (j + 1) + 7]) : 0.0,
-              sj[11] ? " fast" : "");
+              sj[3] != ~0ull ? us(sj[6], sj[3]) : 0.0,
+              j + 1 < L ? us(sj[4], stats_h[kStats * (j + 1) + 7]) : 0.0, sj[11] ? " fast" : "");
       dump_text += line;
     }
   }
