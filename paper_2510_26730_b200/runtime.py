@@ -12,7 +12,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass, replace
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 import torch
@@ -199,6 +199,17 @@ class MoEEngine:
                                           L.as_ptr(toks, C.c_int64),
                                           len(token_ids) if token_ids else 0))
         return h_out
+
+    def activation_log(self) -> List[str]:
+        """The engine's prediction samples as activation-log lines in the
+        reference's wire format (workload.py:1-16, ``format_log_line``): one
+        line per (token batch, layer) the predictor scored, with the token ids
+        passed to step()/prefill(), the predicted and the actual expert sets
+        and the horizon in effect — the input of the reference's offline forest
+        training (``moesim train``), whose JSON model ``model_from_json`` loads
+        back into ``MoEEngine(..., forest=...)``."""
+        from .workload import format_log_line
+        return [format_log_line(s) for s in self.metrics().samples]
 
     def metrics(self) -> SimMetrics:
         return collect_metrics(self.policy.name, self._h.ptr, L.lib.ef_engine_metrics,

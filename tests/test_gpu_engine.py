@@ -317,3 +317,24 @@ def test_shared_host_store_attach():
         torch.cuda.synchronize()
         assert torch.equal(h1, h2), t
     assert a.stats()["copies"] == b.stats()["copies"] > 0
+
+
+def test_activation_log_round_trip():
+    """GPU decode -> activation-log lines in the reference's wire format ->
+    parse_activation_log gives back the engine's samples (the input of the
+    reference's offline forest training)."""
+    cfg = MoEConfig("forest6", 6, 8, 2, 256, 256, dtype="f32", embed_dim=8, vocab_size=64)
+    eng = MoEEngine(cfg, budget_experts=20, policy=ef.PolicyConfig("a", "adaptive",
+                                                                   predictor="pregate"),
+                    link_bw=2 * ef.GB, layer_time_s=1e-4, max_batch=2, seed=4)
+    for t in range(4):
+        eng.step(synthetic_hidden(cfg, 4, t, 2, DEV), [3 * t, 3 * t + 1])
+    torch.cuda.synchronize()
+    lines = eng.activation_log()
+    samples = eng.metrics().samples
+    assert lines and len(lines) == len(samples)
+    parsed = ef.parse_activation_log(lines, cfg.model_spec())
+    key = lambda x: (tuple(x.token_ids), x.layer_idx, tuple(x.predicted_experts),  # noqa: E731
+                     tuple(x.actual_experts), x.step_size)
+    assert [key(x) for x in parsed] == [key(x) for x in samples]
+    assert all(s.token_ids in ((3 * t, 3 * t + 1) for t in range(4)) for s in parsed)
