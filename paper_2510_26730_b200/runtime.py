@@ -294,3 +294,45 @@ def synthetic_hidden(cfg: MoEConfig, seed: int, step: int, B: int, device) -> to
     L.check(L.lib.ef_fill_uniform(C.c_void_p(stream), C.c_void_p(h.data_ptr()), 0, h.numel(),
                                   key, float(scale), 0))
     return h
+
+
+def compare_engines(cfg: MoEConfig, policies: Sequence[PolicyConfig],
+                    workloads: Sequence[Sequence[torch.Tensor]], *,
+                    token_ids: Optional[Sequence[Sequence[Sequence[int]]]] = None,
+                    **engine_kw) -> "ComparisonResult":
+    """``moesim compare`` for real decode (engine.py:777-823 report schema):
+    every policy runs a fresh MoEEngine over the same hidden-state sequence of
+    every workload; rows carry the engines' SimMetrics and the reduction of
+    waiting + miss time against the first policy, so ``to_csv()`` prints the
+    reference's comparison table.  Also returns the device time per run in
+    ``device_ms[(workload, policy)]``."""
+    from .engine import ComparisonResult, RunRow
+    if not policies:
+        raise ValueError("no policies to compare")
+    names = [p.name for p in policies]
+    if len(set(names)) != len(names):
+        raise ValueError(f"duplicate policy names: {names}")
+    rows, device_ms = [], {}
+    for w, steps in enumerate(workloads):
+        for p in policies:
+            eng = MoEEngine(cfg, policy=p, max_batch=max(int(h.shape[0]) for h in steps),
+                            **engine_kw)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for t, h in enumerate(steps):
+                eng.step(h.clone(), token_ids[w][t] if token_ids else None)
+            e.record()
+            torch.cuda.synchronize()
+            device_ms[(w, p.name)] = s.elapsed_time(e)
+            rows.append(RunRow(w, p.name, eng.metrics()))
+            eng.close()
+    red = {}
+    for w in range(len(workloads)):
+        mine = {r.policy: r for r in rows if r.workload == w}
+        base = mine[policies[0].name].stall_plus_miss_ns
+        for p in policies:
+            red[(w, p.name)] = (100.0 * (1.0 - mine[p.name].stall_plus_miss_ns / base)
+                                if base > 0 else None)
+    out = ComparisonResult(rows, policies[0].name, red)
+    out.device_ms = device_ms
+    return out

@@ -338,3 +338,23 @@ def test_activation_log_round_trip():
                      tuple(x.actual_experts), x.step_size)
     assert [key(x) for x in parsed] == [key(x) for x in samples]
     assert all(s.token_ids in ((3 * t, 3 * t + 1) for t in range(4)) for s in parsed)
+
+
+def test_compare_engines_report():
+    """compare-style reporting for real decode: the reactive baseline and the
+    adaptive policy over the same hidden-state sequences, in the reference's
+    comparison-table schema (header and paired reductions)."""
+    cfg = PRESETS["tiny"]
+    pols = [ef.PolicyConfig("reactive", "reactive"),
+            ef.PolicyConfig("adaptive", "adaptive", predictor="pregate")]
+    work = [[synthetic_hidden(cfg, 20 + w, t, 2, DEV) for t in range(3)] for w in range(2)]
+    res = ef.compare_engines(cfg, pols, work, budget_experts=12, link_bw=2 * ef.GB,
+                             layer_time_s=2e-4, seed=3)
+    lines = res.to_csv().strip().split("\n")
+    assert lines[0] == ("workload,policy,waiting_ns,cache_miss_ns,total_ns,final_step,"
+                        "hit_rate,miss_rate,reduction_pct")
+    assert len(lines) == 1 + 2 * 2
+    for w in range(2):
+        base = res.reduction_pct[(w, "reactive")]
+        assert base is None or base == 0.0
+        assert (w, "adaptive") in res.device_ms
