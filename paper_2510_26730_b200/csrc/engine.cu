@@ -7,18 +7,22 @@
 // admit / evict trace, predictions and step sizes are exactly the oracle's
 // for the routing the GPU produced.  Data movement is PHYSICAL: every
 // logical transfer start issues one cudaMemcpyAsync of the expert blob into
-// a free HBM slot on the copy stream, followed by a 1-thread kernel that
-// publishes the slot's fill sequence number; the routed FFN of a layer spins
-// on those numbers for the slots it reads, so swap-ins overlap compute and
-// the measured spin is the physical expert stall.
+// a free HBM slot on the copy stream, followed on the same stream by a
+// 4-byte copy of the blob's fill sequence number into ready[slot]; the routed
+// FFN spins on those numbers for the slots it reads, so swap-ins overlap
+// compute and the measured spin is the physical expert stall.
 //
-// Pipeline (per layer l, kernels enqueued one layer ahead; no per-layer host
-// synchronisation or launch on the critical path):
-//   router(l) -> route(l) [publishes sel + row-0 logits + done flag to mapped
-//   host memory] -> shared expert(l) -> gate(l) [waits for the host's go
-//   flag, copies the decision to device memory] -> routed FFN(l) -> combine(l)
-// Host: spin on done(l) -> Stepper begin_layer/run_layer (issues copies) ->
-// write slots + next layer's bias mask -> go(l).
+// Pipeline (per layer l; kernels enqueued one layer ahead with programmatic
+// dependent launch):
+//   router_route(l) [slot-table row l passed in the launch; previous layer's
+//   combine + rmsnorm; router GEMV + pre-gate rows; last CTA: top-k, permute,
+//   device-side slot resolution] -> shared expert(l) -> gate/up GEMV(l)
+//   [grid column 0 publishes sel + logit rows + done to mapped host memory;
+//   on a non-resolved layer it waits for the host's go and copies its
+//   decision] -> down GEMV(l)
+// Host: spin on done(l) -> pin the slots FFN(l) may read -> Stepper
+// begin_layer/run_layer (issues copies, mirrors residency into the slot
+// table) -> decision block + go(l) -> enqueue layer l+1.
 //
 // Slot safety: when the host decides layer l, route(l) has completed, so
 // every kernel of layers < l has completed (stream order); the only pending

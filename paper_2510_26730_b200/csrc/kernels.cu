@@ -8,6 +8,9 @@
 //   (d) ef_expert_ffn_decode                 : slot-indirected weight-streaming
 //       GEMV (gate+up+SiLU fused, then down), 16-byte L1-bypassing loads,
 //       warp-shuffle reductions
+//   engine pipeline (pipeline.h): router_route_kernel / router_route_row_kernel
+//       (router + route + previous combine + device-side slot resolution in one
+//       launch), ffn_gemv_kernel with the gate folded into grid column 0
 // Decode GEMVs are HBM-bound (arithmetic intensity ~ n_rows FLOP/B); they keep
 // many independent 16 B loads in flight per lane instead of using tensor cores.
 #include <cuda_bf16.h>
