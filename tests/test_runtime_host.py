@@ -1,0 +1,48 @@
+"""CPU tests of the engine's host-side API surface: the product path has no
+CPU fallback (it fails loudly without a CUDA device), argument validation of
+the new entry points, and the C-ABI engine struct layout."""
+
+import ctypes as C
+
+import pytest
+import torch
+
+import paper_2510_26730_b200 as ef
+from paper_2510_26730_b200 import _lib as L
+from paper_2510_26730_b200.runtime import PRESETS, MoEEngine
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_engine_refuses_to_run_without_cuda():
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        MoEEngine(PRESETS["tiny"], budget_experts=16, policy=ef.PolicyConfig("s", "static"),
+                  link_bw=ef.GB, layer_time_s=1e-4)
+
+
+def test_compare_engines_validates_policies():
+    cfg = PRESETS["tiny"]
+    with pytest.raises(ValueError, match="no policies"):
+        ef.compare_engines(cfg, [], [])
+    p = ef.PolicyConfig("a", "adaptive", predictor="pregate")
+    with pytest.raises(ValueError, match="duplicate"):
+        ef.compare_engines(cfg, [p, p], [])
+
+
+def test_engine_cfg_struct_matches_header():
+    """ef_engine_cfg in include/expertflow.h and the ctypes mirror agree on
+    field order (the last fields were appended for prefill and the shared
+    host store)."""
+    names = [f[0] for f in L.EngineCfg._fields_]
+    assert names[-3:] == ["max_prefill", "host_store_shm", "host_store_attach"]
+    hdr = open(__import__("os").path.join(__import__("os").path.dirname(__file__), "..",
+                                          "include", "expertflow.h")).read()
+    body = hdr[hdr.index("typedef struct ef_engine_cfg"):hdr.index("} ef_engine_cfg;")]
+    pos = [body.index(n) for n in ("record_routing", "max_prefill", "host_store_shm",
+                                   "host_store_attach")]
+    assert pos == sorted(pos)
+    assert C.sizeof(L.EngineCfg) >= 96
+
+
+def test_new_entry_points_exported():
+    for name in ("ef_engine_prefill", "ef_engine_step_host", "ef_grouped_gemm_bf16"):
+        assert hasattr(L.lib, name)

@@ -100,6 +100,49 @@ __global__ void __launch_bounds__(WARPS * 32) up_k(Args a) {
   }
 }
 
+// gate/up with a grid-stride loop over row blocks (grid = resident capacity):
+// no ragged last wave
+template <int R, int U, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) up_gs(Args a, int nblocks) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int blk = blockIdx.x; blk < nblocks * NA; blk += gridDim.x) {
+    const int ea = blk / nblocks, bx = blk % nblocks;
+    const int e = (a.e0 + ea) % E;
+    const __nv_bfloat16* W1 = a.w + (int64_t)e * 3 * FF * D;
+    const __nv_bfloat16* W3 = W1 + (int64_t)FF * D;
+    const int j0 = (bx * WARPS + wid) * R;
+    float ag[R], au[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) ag[r] = au[r] = 0.f;
+    for (int c0 = lane * 8; c0 < D; c0 += 32 * 8 * U) {
+      uint4 g[U][R], u[U][R];
+#pragma unroll
+      for (int v = 0; v < U; ++v)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          g[v][r] = ldw(W1 + (int64_t)(j0 + r) * D + c0 + v * 256);
+          u[v][r] = ldw(W3 + (int64_t)(j0 + r) * D + c0 + v * 256);
+        }
+#pragma unroll
+      for (int v = 0; v < U; ++v) {
+        const float4* xp = reinterpret_cast<const float4*>(a.x + c0 + v * 256);
+        float4 x0 = __ldg(xp), x1 = __ldg(xp + 1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          ag[r] = dot8(g[v][r], x0, x1, ag[r]);
+          au[r] = dot8(u[v][r], x0, x1, au[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float gg = wsum(ag[r]), uu = wsum(au[r]);
+      if (lane == 0)
+        a.act[ea * FF + j0 + r] = __float2bfloat16_rn(gg / (1.f + __expf(-gg)) * uu);
+    }
+  }
+}
+
 template <int R, int U, int WARPS, bool PDL, bool LDG = false>
 __global__ void __launch_bounds__(WARPS * 32) down_k(Args a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -427,6 +470,14 @@ int main() {
       launch(p.d.fn, D, p.d.rows_per_cta, p.d.threads, a, s, p.pdl);
     });
     printf("%-28s %8.1f us %7.0f GB/s\n", p.name, t, (up_bytes + dn_bytes) / t * 1e-3);
+  }
+  // grid-stride gate/up (grid = resident capacity)
+  for (int per_sm : {8, 7, 6}) {
+    float t = time_it([&](int i) {
+      constexpr int R = 2, W = 4;
+      up_gs<R, 2, W><<<148 * per_sm, W * 32, 0, s>>>(Args{w, (2 * i) % E, x, act, y}, FF / (R * W));
+    });
+    printf("up grid-stride %d/SM           %8.1f us %7.0f GB/s\n", per_sm, t, up_bytes / t * 1e-3);
   }
   // persistent fused variant
   int* ctr;
