@@ -1137,6 +1137,19 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     ef::g_use_pdl = !(pdl && pdl[0] == '0');
     const char* fz = getenv("EF_FUSE");
     if (fz) e->fuse = atoi(fz);
+    // Under an injected profiler (Nsight Compute sets these variables) every
+    // launch is serialised and may block the host until the kernel finishes;
+    // the run-ahead pipeline, whose fused gate waits on the host, would then
+    // never finish.  Fall back to the debug pipeline (host decides each layer
+    // before its FFN is enqueued; gate in its own kernel) unless the caller
+    // chose explicitly.  Timings under a profiler are never bench values.
+    const bool profiled = getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") ||
+                          getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
+                          getenv("CUDA_INJECTION64_PATH");
+    if (profiled && !dbg && !fz) {
+      e->debug = true;
+      e->fuse = 1;
+    }
     *out = e.release();
   });
 }

@@ -75,14 +75,14 @@ def summarise(rep, name, rnd):
     return per_kernel
 
 
-def launch_list(path, rnd):
+def launch_list(path, rnd, name="decode", command=None):
     lines = [l for l in open(path) if not l.startswith("==")]
     rows = list(csv.reader(lines))
     hdr, data = rows[0], rows[1:]
     ki, gi, bi, vi = (hdr.index("Kernel Name"), hdr.index("Grid Size"), hdr.index("Block Size"),
                       hdr.index("Metric Value"))
     keep = [r for r in data if "fill_uniform" not in r[ki]]
-    out = os.path.join(PROF, f"{rnd}_decode_launches.csv")
+    out = os.path.join(PROF, f"{rnd}_{name}_launches.csv")
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["id", "kernel", "grid", "block", "duration_ns"])
@@ -95,21 +95,23 @@ def launch_list(path, rnd):
         tot[k] += float(r[vi])
         cnt[k] += 1
     all_ns = sum(tot.values())
+    default_cmd = (
+        "Command: `EF_PIPE_DEBUG=1 EF_FUSE=1 ncu --metrics gpu__time_duration.sum "
+        "--clock-control none python tools/profile_decode.py --layers 32 --steps 3 "
+        "--policy adaptive --budget-frac 0.4 --bias 10000` (Mixtral-8x7B shape, 32 layers, "
+        "B=1, the bench's policy and budget).  ncu makes every launch synchronous, so the "
+        "run-ahead pipeline (whose fused gate waits on the host) cannot run under it: "
+        "EF_PIPE_DEBUG=1 decides each layer before enqueueing its FFN and EF_FUSE=1 keeps "
+        "the gate in its own kernel.  The default pipeline has no gate_kernel launch, no "
+        "combine_kernel launch (folded into the next router) and no host wait.")
     md = [f"# {rnd}: kernel share of the decode steps (ncu launch list)", "",
-          "Command: `EF_PIPE_DEBUG=1 EF_FUSE=1 ncu --metrics gpu__time_duration.sum "
-          "--clock-control none python tools/profile_decode.py --layers 32 --steps 3 "
-          "--policy adaptive --budget-frac 0.4 --bias 10000` (Mixtral-8x7B shape, 32 layers, "
-          "B=1, the bench's policy and budget).  ncu makes every launch synchronous, so the "
-          "run-ahead pipeline (whose fused gate waits on the host) cannot run under it: "
-          "EF_PIPE_DEBUG=1 decides each layer before enqueueing its FFN and EF_FUSE=1 keeps "
-          "the gate in its own kernel.  The default pipeline has no gate_kernel launch, no "
-          "combine_kernel launch (folded into the next router) and no host wait.", "",
+          command or default_cmd, "",
           "Per-launch times are cold-cache and serialised: compare shares, not absolutes.", "",
           "| kernel | launches | total us | mean us | share |", "|---|---:|---:|---:|---:|"]
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
         md.append(f"| `{k}` | {cnt[k]} | {v / 1e3:.1f} | {v / cnt[k] / 1e3:.1f} | "
                   f"{v / all_ns:.1%} |")
-    with open(os.path.join(PROF, f"{rnd}_decode_launch_share.md"), "w") as f:
+    with open(os.path.join(PROF, f"{rnd}_{name}_launch_share.md"), "w") as f:
         f.write("\n".join(md) + "\n")
 
 
@@ -117,6 +119,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
     ap.add_argument("--launches")
+    ap.add_argument("--launch-name", default="decode")
+    ap.add_argument("--launch-command")
     ap.add_argument("--ffn")
     ap.add_argument("--router")
     ap.add_argument("--gemm")
@@ -125,7 +129,7 @@ def main():
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
-        launch_list(a.launches, a.round)
+        launch_list(a.launches, a.round, a.launch_name, a.launch_command)
     traffic = {}
     if a.up and a.down:
         ku = summarise(a.up, "decode_ffn_up", a.round)
