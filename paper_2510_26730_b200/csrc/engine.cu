@@ -128,7 +128,6 @@ struct ef_engine {
   char* hout = nullptr;  // [L] x out_stride, mapped
   char* hout_dev = nullptr;
   int64_t out_stride = 0;
-  float* logits_h = nullptr;  // pre-gate rows fetched on demand
   static constexpr uint32_t kSeqRing = 1u << 16;  // pinned sources of the ready-flag copies
   uint32_t* seq_ring = nullptr;
   std::vector<unsigned long long> stats_h;
@@ -154,7 +153,7 @@ struct ef_engine {
   size_t shm_bytes = 0;
   std::string shm_name;      // set by the creating process, which unlinks it
   bool store_filled = false;  // attached to a store another process filled
-  cudaStream_t copy_stream = nullptr, side_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
   // slot table
   std::vector<int32_t> phys_of;    // [L*M] -> slot or -1
   std::vector<uint32_t> slot_seq;  // fill sequence of each slot's current content
@@ -398,7 +397,7 @@ ef_engine::~ef_engine() {
                   (void*)ptiles_d})
     if (p) cudaFree(p);
   if (copy_mark) cudaEventDestroy(copy_mark);
-  for (void* p : {(void*)hctrl, (void*)hout, (void*)logits_h, (void*)seq_ring, (void*)host_tab,
+  for (void* p : {(void*)hctrl, (void*)hout, (void*)seq_ring, (void*)host_tab,
                   (void*)plogits_h, (void*)psel_h, (void*)ptiles_h})
     if (p) cudaFreeHost(p);
   if (shm_base) {
@@ -410,7 +409,6 @@ ef_engine::~ef_engine() {
       if (p) cudaFreeHost(p);
   }
   if (copy_stream) cudaStreamDestroy(copy_stream);
-  if (side_stream) cudaStreamDestroy(side_stream);
   if (compute_stream) cudaStreamDestroy(compute_stream);
   if (join_in) cudaEventDestroy(join_in);
   if (join_out) cudaEventDestroy(join_out);
@@ -1076,7 +1074,6 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     CK(cudaHostAlloc(&e->hout, e->out_stride * L, cudaHostAllocMapped));
     std::memset(e->hout, 0, e->out_stride * L);
     CK(cudaHostGetDevicePointer((void**)&e->hout_dev, e->hout, 0));
-    CK(cudaHostAlloc(&e->logits_h, (size_t)e->Rmax * B * M * 4, cudaHostAllocDefault));
     CK(cudaHostAlloc(&e->seq_ring, sizeof(uint32_t) * ef_engine::kSeqRing, cudaHostAllocDefault));
     e->store.assign(L, nullptr);
     if (c.host_store_shm && c.host_store_shm[0]) {
@@ -1106,7 +1103,6 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     CK(cudaStreamCreateWithPriority(&e->copy_stream, cudaStreamNonBlocking, prio_hi));
-    CK(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking));
     if (!getenv("EF_CALLER_STREAM")) {
       CK(cudaStreamCreateWithPriority(&e->compute_stream, cudaStreamNonBlocking, prio_hi));
       CK(cudaEventCreateWithFlags(&e->join_in, cudaEventDisableTiming));
