@@ -240,17 +240,21 @@ def test_step_host_matches_device_step():
         e_host.step_host(torch.zeros(3, cfg.d_model))  # not pinned
 
 
-@pytest.mark.parametrize("shape", ["tiny", "qwen"])
+@pytest.mark.parametrize("shape", ["tiny", "qwen", "deepseek"])
 def test_prefill_then_decode_parity(shape):
     """Prefill (tcgen05/TMA grouped GEMM path) of T tokens as one scheduler
     step, then decode steps from the same cache: every decision bit-exact
     with the oracle replay, every output within the bf16 tolerance."""
     if shape == "tiny":
         cfg, T, B, budget = PRESETS["tiny-bf16"], 96, 2, 12
-    else:
+    elif shape == "qwen":
         cfg = MoEConfig("qwen-2l", 2, 60, 4, 2048, 1408, dtype="bf16", route_mode="softmax_topk",
                         shared_ff=5632, shared_gate=True)
         T, B, budget = 160, 4, 80
+    else:  # DeepSeek-V2-Lite expert shape: 64 experts top-6, two ungated shared experts
+        cfg = MoEConfig("ds-2l", 2, 64, 6, 2048, 1408, dtype="bf16", route_mode="softmax_topk",
+                        shared_ff=2816)
+        T, B, budget = 256, 2, 100
     pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
     link_bw, layer_s, seed = 4 * ef.GB, 2e-4, 3
     eng = MoEEngine(cfg, budget_experts=budget, policy=pol, link_bw=link_bw, layer_time_s=layer_s,
