@@ -339,12 +339,18 @@ def run_ours(args, cfg, bias):
     import gc
     gc.collect()
     torch.cuda.synchronize()
-    baseline = unbiased = None
+    baseline = unbiased = peer = None
     if not args.no_baseline and rank == 0 and world == 1:
         baseline = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K)
         if bias != 0.0:
             unbiased = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
                                          strategy=args.strategy, bias=0.0)
+            # the same unbiased run with every expert's home copy in the
+            # peer-HBM tier, pool on this device as the
+            # one-GPU stand-in for a peer reached over NVLink
+            peer = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
+                                     strategy=args.strategy, bias=0.0,
+                                     peer_pool=cfg.total_experts)
 
     traffic = ncu_traffic()
     if rank == 0:
@@ -402,6 +408,8 @@ def run_ours(args, cfg, bias):
             line["reactive_baseline"] = baseline
         if unbiased:
             line["unbiased_routing"] = unbiased
+        if peer:
+            line["unbiased_routing_peer_tier"] = peer
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -412,7 +420,7 @@ def _rate(h, m):
 
 
 def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
-                      strategy="reactive", bias=0.0):
+                      strategy="reactive", bias=0.0, peer_pool=0):
     """The reactive per-layer baseline (engine.py:488-489) on the same
     engine type, budget and inputs; no routing bias.  With strategy=adaptive
     it is the headline policy with unbiased routing (the PCIe-bound case)."""
@@ -425,7 +433,7 @@ def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
                     policy=ef.PolicyConfig(strategy, strategy, predictor="pregate",
                                            cache_aware_routing=strategy != "reactive"),
                     link_bw=link_bw, layer_time_s=layer_s, max_batch=args.batch, seed=args.seed,
-                    routing_bias=bias, timing=True)
+                    routing_bias=bias, timing=True, peer_pool_experts=peer_pool)
     n = min(K, 6)
     for t in range(min(W, 2)):
         eng.step(inputs[t].clone())
@@ -443,6 +451,11 @@ def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
            "expert_stall_pct": 100.0 * (st1["stall_ms"] - st0["stall_ms"]) / ms,
            "copies_per_step": (st1["copies"] - st0["copies"]) / n,
            "policy": f"{strategy}/pregate, routing_bias {bias:g}"}
+    if peer_pool:
+        out["peer_pool_experts"] = peer_pool
+        out["peer_copies_per_step"] = (st1["peer_copies"] - st0["peer_copies"]) / n
+        out["peer_tier"] = ("home copies in a pool on the engine's own device (one-GPU "
+                            "stand-in for a peer GPU over NVLink; same cudaMemcpyPeerAsync path)")
     eng.close()
     del eng
     import gc

@@ -295,6 +295,14 @@ typedef struct ef_engine_cfg {
   const char* host_store_shm; /* non-null: pinned host expert store in POSIX shared memory of
                                  this name, shared by the processes of one node */
   int32_t host_store_attach;  /* 1: attach to a store another process created and filled */
+  int32_t peer_device;        /* device holding the peer pool (may equal `device`) */
+  int64_t peer_pool_experts;  /* N: pool size in experts; 0 turns the tier off */
+  /* Peer-HBM miss tier (the reference models one host link,
+     SPEC.md:557): home copies of the first N experts (flat index l*M+e from 0)
+     live in a pool on the peer device; a swap-in of one of them is a
+     cudaMemcpyPeerAsync over NVLink instead of the host copy.  Tiers change
+     only latency, never which experts are requested or admitted.  A pool on
+     the engine's own device is the one-GPU stand-in (same code path). */
 } ef_engine_cfg;
 int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim, const ef_ladder_cfg* ladder,
                      ef_engine** out);
@@ -322,7 +330,8 @@ int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len, int64_t* n
    preload_copies, d2h_bytes, ffn_bytes (routed expert weight bytes streamed), ffn_launches,
    gate_wait_ms (GPU time spent waiting for the host's per-layer decision),
    fast_layers (layers whose routed FFN started from the device-side slot table,
-   without waiting for the host) */
+   without waiting for the host), peer_copies, peer_bytes (swap-ins served by the
+   peer-HBM tier) */
 int ef_engine_stats(ef_engine* e, double* out, int n);
 /* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
    6 perm, 7 inv, 8 y, 9 x */

@@ -154,6 +154,13 @@ struct ef_engine {
   std::string shm_name;      // set by the creating process, which unlinks it
   bool store_filled = false;  // attached to a store another process filled
   cudaStream_t copy_stream = nullptr;
+  // peer-HBM tier (ef_engine_cfg.peer_device / peer_pool_experts): home copies
+  // of experts [0, peer_n) (flat l*M+e) on device peer_dev
+  char* peer_pool = nullptr;
+  int64_t peer_n = 0;
+  int peer_dev = -1;
+  int64_t peer_copies = 0, peer_bytes = 0;
+  void init_peer_pool();
   // slot table
   std::vector<int32_t> phys_of;    // [L*M] -> slot or -1
   std::vector<uint32_t> slot_seq;  // fill sequence of each slot's current content
@@ -227,9 +234,19 @@ struct ef_engine {
       throw RuntimeErr("no free physical expert slot (raise staging_slots)");
     int s = free_slots.front();
     free_slots.pop_front();
-    const char* src = store[eid_layer(key)] + (int64_t)eid_expert(key) * stride;
-    CK(cudaMemcpyAsync(slab + (int64_t)s * stride, src, stride, cudaMemcpyHostToDevice,
-                       copy_stream));
+    const int64_t flat = idx(key);
+    if (flat < peer_n) {
+      // miss served from the peer's HBM over NVLink (copy engine, same stream,
+      // so the ready flag below still lands after the blob)
+      CK(cudaMemcpyPeerAsync(slab + (int64_t)s * stride, cfg.device, peer_pool + flat * stride,
+                             peer_dev, stride, copy_stream));
+      ++peer_copies;
+      peer_bytes += stride;
+    } else {
+      const char* src = store[eid_layer(key)] + (int64_t)eid_expert(key) * stride;
+      CK(cudaMemcpyAsync(slab + (int64_t)s * stride, src, stride, cudaMemcpyHostToDevice,
+                         copy_stream));
+    }
     uint32_t seq = ++copy_seq;
     // Publish the fill sequence with the copy engine (a 4-byte H2D copy from a
     // pinned ring right behind the blob on the same stream).  A kernel would
@@ -379,9 +396,41 @@ void ef_engine::init_weights() {
   cudaStreamDestroy(s);
 }
 
+// Fill the peer pool from the host store (once, at create).  Cross-device
+// pools need peer access in both directions; the copies then run over NVLink.
+void ef_engine::init_peer_pool() {
+  peer_n = std::min<int64_t>(cfg.peer_pool_experts, (int64_t)cfg.L * cfg.M);
+  peer_dev = cfg.peer_device;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (peer_dev < 0 || peer_dev >= ndev) throw ValueError("peer_device is not a visible device");
+  if (peer_dev != cfg.device) {
+    int ok = 0;
+    CK(cudaDeviceCanAccessPeer(&ok, cfg.device, peer_dev));
+    if (!ok) throw RuntimeErr("no peer access between the engine device and peer_device");
+    for (int a : {cfg.device, peer_dev}) {
+      CK(cudaSetDevice(a));
+      cudaError_t r = cudaDeviceEnablePeerAccess(a == cfg.device ? peer_dev : cfg.device, 0);
+      if (r == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else CK(r);
+    }
+  }
+  CK(cudaSetDevice(peer_dev));
+  CK(cudaMalloc(&peer_pool, (size_t)peer_n * stride));
+  for (int64_t f = 0; f < peer_n; ++f)
+    CK(cudaMemcpy(peer_pool + f * stride, store[f / cfg.M] + (f % cfg.M) * stride, stride,
+                  cudaMemcpyHostToDevice));
+  CK(cudaSetDevice(cfg.device));
+}
+
 ef_engine::~ef_engine() {
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   cudaDeviceSynchronize();
+  if (peer_pool) {
+    cudaSetDevice(peer_dev);
+    cudaFree(peer_pool);
+    cudaSetDevice(cfg.device);
+  }
   for (int i = 0; i < 2; ++i) {
     if (stats_pin[i]) cudaFreeHost(stats_pin[i]);
     for (int j = 0; j < 3; ++j)
@@ -1115,6 +1164,8 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
     e->init_weights();
+    if (c.peer_pool_experts < 0) throw ValueError("peer_pool_experts must be >= 0");
+    if (c.peer_pool_experts > 0) e->init_peer_pool();
     if (preload_pipeline_kernels() < 30) throw CudaErr("could not load the pipeline kernels");
     const char* dbg = getenv("EF_PIPE_DEBUG");
     e->debug = dbg && dbg[0] == '1';
@@ -1201,7 +1252,7 @@ extern "C" int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len,
 extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   EF_TRY({
     e->flush_stats();
-    double v[17] = {(double)e->steps,         (double)e->copies,
+    double v[19] = {(double)e->steps,         (double)e->copies,
                     (double)e->copy_bytes,    e->stall_ms,
                     (double)e->P,             (double)e->st->cache().capacity(),
                     (double)e->cfg.staging_slots, (double)e->launches,
@@ -1209,8 +1260,9 @@ extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
                     e->step_ms,               (double)e->preload_copies,
                     (double)e->d2h_bytes,     (double)e->ffn_bytes,
                     (double)e->ffn_launches,  e->bubble_ms,
-                    (double)e->fast_layers};
-    for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];
+                    (double)e->fast_layers,   (double)e->peer_copies,
+                    (double)e->peer_bytes};
+    for (int i = 0; i < n && i < 19; ++i) out[i] = v[i];
   });
 }
 

@@ -88,7 +88,8 @@ class MoEEngine:
                  forest: Optional[ForestModel] = None, table: Optional[EmbeddingTable] = None,
                  emit_events: bool = False, timing: bool = False, record_routing: bool = False,
                  device: int = 0, max_prefill: int = 0, host_store_shm: Optional[str] = None,
-                 host_store_attach: bool = False):
+                 host_store_attach: bool = False, peer_device: Optional[int] = None,
+                 peer_pool_experts: int = 0):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
@@ -131,6 +132,12 @@ class MoEEngine:
         self._shm_name = host_store_shm.encode() if host_store_shm else None
         ec.host_store_shm = self._shm_name
         ec.host_store_attach = int(host_store_attach)
+        # peer-HBM miss tier (E3): home copies of experts [0, peer_pool_experts)
+        # on peer_device (default: this device, the one-GPU stand-in)
+        if peer_pool_experts < 0:
+            raise ValueError("peer_pool_experts must be >= 0")
+        ec.peer_device = device if peer_device is None else int(peer_device)
+        ec.peer_pool_experts = int(peer_pool_experts)
         torch.cuda.set_device(device)
         torch.cuda.init()
         h = L.vp()
@@ -228,7 +235,7 @@ class MoEEngine:
         keys = ["steps", "copies", "copy_bytes", "stall_ms", "phys_slots", "logical_capacity",
                 "staging_slots", "kernel_launches", "host_decision_ms", "ffn_ms", "step_ms",
                 "preload_copies", "d2h_bytes", "ffn_bytes", "ffn_launches", "gate_wait_ms",
-                "fast_layers"]
+                "fast_layers", "peer_copies", "peer_bytes"]
         out = (C.c_double * len(keys))()
         L.check(L.lib.ef_engine_stats(self._h.ptr, out, len(keys)))
         return dict(zip(keys, list(out)))

@@ -362,3 +362,36 @@ def test_compare_engines_report():
         base = res.reduction_pct[(w, "reactive")]
         assert base is None or base == 0.0
         assert (w, "adaptive") in res.device_ms
+
+
+@pytest.mark.gpu
+def test_peer_hbm_tier_changes_latency_not_decisions():
+    """Peer-HBM miss tier: swap-ins of experts with a home copy
+    in the peer pool are served by cudaMemcpyPeerAsync instead of the host
+    copy.  The tier changes only where the bytes come from: outputs, the cache
+    event trace and every scheduler counter equal the host-only engine's.  On
+    a one-GPU box the pool sits on the engine's own device (same code path)."""
+    cfg = PRESETS["tiny-bf16"]
+    pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
+    kw = dict(budget_experts=12, policy=pol, link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2,
+              seed=5, emit_events=True)
+    n_pool = cfg.num_layers * cfg.num_experts // 2
+    a = MoEEngine(cfg, **kw)
+    b = MoEEngine(cfg, peer_pool_experts=n_pool, **kw)
+    for t in range(6):
+        h1 = synthetic_hidden(cfg, 5, t, 2, DEV)
+        h2 = h1.clone()
+        a.step(h1)
+        b.step(h2)
+        torch.cuda.synchronize()
+        assert torch.equal(h1, h2), t
+    assert a.cache_events() == b.cache_events()
+    import dataclasses
+    ma, mb = (dataclasses.replace(m.metrics(), bandwidth_estimate=0.0) for m in (a, b))
+    assert ma == mb
+    sa, sb = a.stats(), b.stats()
+    assert sa["peer_copies"] == 0 and sa["copies"] == sb["copies"]
+    assert 0 < sb["peer_copies"] < sb["copies"]
+    assert sb["peer_bytes"] == sb["peer_copies"] * cfg.expert_bytes
+    with pytest.raises(ValueError):
+        MoEEngine(cfg, peer_pool_experts=-1, **kw)
