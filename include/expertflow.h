@@ -303,6 +303,10 @@ typedef struct ef_engine_cfg {
      cudaMemcpyPeerAsync over NVLink instead of the host copy.  Tiers change
      only latency, never which experts are requested or admitted.  A pool on
      the engine's own device is the one-GPU stand-in (same code path). */
+  const void* peer_ipc_handle; /* non-null: 64-byte cudaIpcMemHandle_t of a pool another
+                                  process (one process per GPU) created and filled on
+                                  peer_device (ef_engine_peer_pool_handle); opened, not
+                                  allocated or filled */
 } ef_engine_cfg;
 int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim, const ef_ladder_cfg* ladder,
                      ef_engine** out);
@@ -336,6 +340,10 @@ int ef_engine_stats(ef_engine* e, double* out, int n);
 /* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
    6 perm, 7 inv, 8 y, 9 x */
 int ef_engine_ptr(ef_engine* e, int which, void** out);
+/* export this engine's peer pool (allocated on its own device) as a 64-byte
+   cudaIpcMemHandle_t, for the engine of another process to open through
+   ef_engine_cfg.peer_ipc_handle */
+int ef_engine_peer_pool_handle(ef_engine* e, void* handle64);
 /* routing log entry `index` (one per executed layer, in order): R scored router
    matrices of logits [R][B][M] fp32, sel [B][k], cache-aware bias mask.  Pass
    null buffers to query sizes; *n_entries = log length. */

@@ -63,7 +63,8 @@ class EngineCfg(C.Structure):
                 ("shared_gate", i32), ("budget_slots", i64), ("staging_slots", i32),
                 ("routing_bias", f32), ("seed", u64), ("device", i32), ("timing", i32),
                 ("record_routing", i32), ("max_prefill", i32), ("host_store_shm", C.c_char_p),
-                ("host_store_attach", i32), ("peer_device", i32), ("peer_pool_experts", i64)]
+                ("host_store_attach", i32), ("peer_device", i32), ("peer_pool_experts", i64),
+                ("peer_ipc_handle", vp)]
 
 
 _SIGS = {
@@ -143,6 +144,7 @@ _SIGS = {
     "ef_engine_output": (C.c_int, [vp, i32, P(i64), i64, P(i64)]),
     "ef_engine_event_details": (C.c_int, [vp, C.c_char_p, i64, P(i64)]),
     "ef_engine_stats": (C.c_int, [vp, P(f64), C.c_int]),
+    "ef_engine_peer_pool_handle": (C.c_int, [vp, vp]),
     "ef_engine_ptr": (C.c_int, [vp, C.c_int, P(vp)]),
     "ef_engine_slot_of": (C.c_int, [vp, i32, i32, P(i32)]),
     "ef_engine_routing_log": (C.c_int, [vp, i64, P(f32), i64, P(i32), i64, P(i32), P(i32), P(u64),

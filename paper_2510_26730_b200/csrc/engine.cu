@@ -159,6 +159,7 @@ struct ef_engine {
   char* peer_pool = nullptr;
   int64_t peer_n = 0;
   int peer_dev = -1;
+  bool peer_ipc = false;  // pool opened from another process's IPC handle
   int64_t peer_copies = 0, peer_bytes = 0;
   void init_peer_pool();
   // slot table
@@ -401,6 +402,16 @@ void ef_engine::init_weights() {
 void ef_engine::init_peer_pool() {
   peer_n = std::min<int64_t>(cfg.peer_pool_experts, (int64_t)cfg.L * cfg.M);
   peer_dev = cfg.peer_device;
+  if (cfg.peer_ipc_handle) {
+    // pool created and filled by the process that owns peer_dev
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, cfg.peer_ipc_handle, sizeof(h));
+    CK(cudaSetDevice(cfg.device));
+    CK(cudaIpcOpenMemHandle((void**)&peer_pool, h, cudaIpcMemLazyEnablePeerAccess));
+    peer_ipc = true;
+    peer_dev = cfg.device;  // mapped into this context: the copy is a D2D over NVLink
+    return;
+  }
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (peer_dev < 0 || peer_dev >= ndev) throw ValueError("peer_device is not a visible device");
@@ -426,7 +437,9 @@ void ef_engine::init_peer_pool() {
 ef_engine::~ef_engine() {
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   cudaDeviceSynchronize();
-  if (peer_pool) {
+  if (peer_pool && peer_ipc) {
+    cudaIpcCloseMemHandle(peer_pool);
+  } else if (peer_pool) {
     cudaSetDevice(peer_dev);
     cudaFree(peer_pool);
     cudaSetDevice(cfg.device);
@@ -1263,6 +1276,16 @@ extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
                     (double)e->fast_layers,   (double)e->peer_copies,
                     (double)e->peer_bytes};
     for (int i = 0; i < n && i < 19; ++i) out[i] = v[i];
+  });
+}
+
+extern "C" int ef_engine_peer_pool_handle(ef_engine* e, void* handle64) {
+  EF_TRY({
+    if (!e->peer_pool || e->peer_ipc || e->peer_dev != e->cfg.device)
+      throw ValueError("no peer pool allocated on this engine's device to export");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, e->peer_pool));
+    std::memcpy(handle64, &h, sizeof(h));
   });
 }
 

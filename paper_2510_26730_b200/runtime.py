@@ -89,7 +89,7 @@ class MoEEngine:
                  emit_events: bool = False, timing: bool = False, record_routing: bool = False,
                  device: int = 0, max_prefill: int = 0, host_store_shm: Optional[str] = None,
                  host_store_attach: bool = False, peer_device: Optional[int] = None,
-                 peer_pool_experts: int = 0):
+                 peer_pool_experts: int = 0, peer_ipc_handle: Optional[bytes] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
@@ -138,6 +138,14 @@ class MoEEngine:
             raise ValueError("peer_pool_experts must be >= 0")
         ec.peer_device = device if peer_device is None else int(peer_device)
         ec.peer_pool_experts = int(peer_pool_experts)
+        # a pool another process (one process per GPU) created on peer_device:
+        # its 64-byte handle from that engine's peer_pool_handle()
+        self._peer_ipc = None
+        if peer_ipc_handle is not None:
+            if len(peer_ipc_handle) != 64:
+                raise ValueError("peer_ipc_handle must be the 64-byte handle of peer_pool_handle()")
+            self._peer_ipc = C.create_string_buffer(bytes(peer_ipc_handle), 64)
+            ec.peer_ipc_handle = C.cast(self._peer_ipc, L.vp)
         torch.cuda.set_device(device)
         torch.cuda.init()
         h = L.vp()
@@ -230,6 +238,13 @@ class MoEEngine:
         names = {0: "miss", 1: "hit", 2: "admit", 3: "evict"}
         return [(rows[i], names[rows[i + 1]], ExpertId(rows[i + 2], rows[i + 3]))
                 for i in range(0, len(rows), 4)]
+
+    def peer_pool_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this engine's peer pool, for the engines
+        of other processes (``peer_ipc_handle=``) to serve misses from it."""
+        buf = C.create_string_buffer(64)
+        L.check(L.lib.ef_engine_peer_pool_handle(self._h.ptr, buf))
+        return buf.raw
 
     def stats(self) -> dict:
         keys = ["steps", "copies", "copy_bytes", "stall_ms", "phys_slots", "logical_capacity",

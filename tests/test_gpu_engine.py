@@ -395,3 +395,52 @@ def test_peer_hbm_tier_changes_latency_not_decisions():
     assert sb["peer_bytes"] == sb["peer_copies"] * cfg.expert_bytes
     with pytest.raises(ValueError):
         MoEEngine(cfg, peer_pool_experts=-1, **kw)
+
+
+_IPC_CHILD = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2510_26730_b200 as ef
+from paper_2510_26730_b200.runtime import PRESETS, MoEEngine, synthetic_hidden
+cfg = PRESETS["tiny-bf16"]
+kw = dict(budget_experts=12, policy=ef.PolicyConfig("a", "adaptive", predictor="pregate"),
+          link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2, seed=5)
+n = int(sys.argv[3])
+a = MoEEngine(cfg, **kw)
+b = MoEEngine(cfg, peer_pool_experts=n, peer_ipc_handle=bytes.fromhex(sys.argv[2]), **kw)
+for t in range(6):
+    h1 = synthetic_hidden(cfg, 5, t, 2, torch.device("cuda", 0))
+    h2 = h1.clone()
+    a.step(h1)
+    b.step(h2)
+    torch.cuda.synchronize()
+    assert torch.equal(h1, h2), t
+assert a.cache_events() == b.cache_events()
+sb = b.stats()
+assert 0 < sb["peer_copies"] < sb["copies"], sb
+print("ipc ok", int(sb["peer_copies"]), int(sb["copies"]))
+"""
+
+
+@pytest.mark.gpu
+def test_peer_pool_ipc_across_processes():
+    """One process per GPU: this process fills a peer pool and exports its
+    CUDA IPC handle; an engine in another process opens it
+    (``peer_ipc_handle``) and serves its misses from it, decoding exactly like
+    a host-only engine.  On a one-GPU box both processes share the device."""
+    import os
+    import subprocess
+    import sys
+    cfg = PRESETS["tiny-bf16"]
+    n_pool = cfg.num_layers * cfg.num_experts // 2
+    owner = MoEEngine(cfg, budget_experts=12, policy=ef.PolicyConfig("a", "adaptive",
+                                                                     predictor="pregate"),
+                      link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2, seed=5,
+                      peer_pool_experts=n_pool)
+    handle = owner.peer_pool_handle()
+    assert len(handle) == 64
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _IPC_CHILD, root, handle.hex(), str(n_pool)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ipc ok" in r.stdout, r.stdout + r.stderr
+    owner.close()
