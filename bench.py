@@ -345,12 +345,14 @@ def run_ours(args, cfg, bias):
         if bias != 0.0:
             unbiased = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
                                          strategy=args.strategy, bias=0.0)
-            # the same unbiased run with every expert's home copy in the
-            # peer-HBM tier, pool on this device as the
-            # one-GPU stand-in for a peer reached over NVLink
-            peer = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
-                                     strategy=args.strategy, bias=0.0,
-                                     peer_pool=cfg.total_experts)
+            if torch.cuda.device_count() > 1:
+                # the same unbiased run with every expert's home copy in a
+                # second GPU's HBM (peer-HBM tier): misses are
+                # NVLink copies instead of PCIe.  Needs a second GPU: a pool on
+                # this device would copy on SMs (tools/peer_copy_lab.cu)
+                peer = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
+                                         strategy=args.strategy, bias=0.0,
+                                         peer_pool=cfg.total_experts, peer_device=1)
 
     traffic = ncu_traffic()
     if rank == 0:
@@ -420,7 +422,7 @@ def _rate(h, m):
 
 
 def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
-                      strategy="reactive", bias=0.0, peer_pool=0):
+                      strategy="reactive", bias=0.0, peer_pool=0, peer_device=None):
     """The reactive per-layer baseline (engine.py:488-489) on the same
     engine type, budget and inputs; no routing bias.  With strategy=adaptive
     it is the headline policy with unbiased routing (the PCIe-bound case)."""
@@ -433,7 +435,8 @@ def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
                     policy=ef.PolicyConfig(strategy, strategy, predictor="pregate",
                                            cache_aware_routing=strategy != "reactive"),
                     link_bw=link_bw, layer_time_s=layer_s, max_batch=args.batch, seed=args.seed,
-                    routing_bias=bias, timing=True, peer_pool_experts=peer_pool)
+                    routing_bias=bias, timing=True, peer_pool_experts=peer_pool,
+                    peer_device=peer_device)
     n = min(K, 6)
     for t in range(min(W, 2)):
         eng.step(inputs[t].clone())
@@ -454,8 +457,7 @@ def reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
     if peer_pool:
         out["peer_pool_experts"] = peer_pool
         out["peer_copies_per_step"] = (st1["peer_copies"] - st0["peer_copies"]) / n
-        out["peer_tier"] = ("home copies in a pool on the engine's own device (one-GPU "
-                            "stand-in for a peer GPU over NVLink; same cudaMemcpyPeerAsync path)")
+        out["peer_tier"] = f"home copies of every expert in cuda:{peer_device} HBM (NVLink)"
     eng.close()
     del eng
     import gc

@@ -302,7 +302,8 @@ typedef struct ef_engine_cfg {
      live in a pool on the peer device; a swap-in of one of them is a
      cudaMemcpyPeerAsync over NVLink instead of the host copy.  Tiers change
      only latency, never which experts are requested or admitted.  A pool on
-     the engine's own device is the one-GPU stand-in (same code path). */
+     the engine's own device is a test-only stand-in (EF_PEER_SAME_DEVICE=1):
+     same-device copies run on SMs and can deadlock a GPU-filling FFN. */
   const void* peer_ipc_handle; /* non-null: 64-byte cudaIpcMemHandle_t of a pool another
                                   process (one process per GPU) created and filled on
                                   peer_device (ef_engine_peer_pool_handle); opened, not

@@ -162,6 +162,17 @@ struct ef_engine {
   bool peer_ipc = false;  // pool opened from another process's IPC handle
   int64_t peer_copies = 0, peer_bytes = 0;
   void init_peer_pool();
+  // A same-device copy runs on SMs, not on a copy engine (tools/peer_copy_lab.cu:
+  // it never starts while a kernel holds every SM).  A routed FFN that fills the
+  // GPU and spins on the slot such a copy fills would never finish, so the
+  // same-device stand-in of the peer tier is a test-only mode.
+  static void check_same_device_pool() {
+    const char* v = getenv("EF_PEER_SAME_DEVICE");
+    if (!(v && v[0] == '1'))
+      throw ValueError("peer pool on the engine's own device: its copies need SMs and can "
+                       "deadlock the routed FFN; set EF_PEER_SAME_DEVICE=1 (tests, small "
+                       "shapes only)");
+  }
   // slot table
   std::vector<int32_t> phys_of;    // [L*M] -> slot or -1
   std::vector<uint32_t> slot_seq;  // fill sequence of each slot's current content
@@ -409,12 +420,16 @@ void ef_engine::init_peer_pool() {
     CK(cudaSetDevice(cfg.device));
     CK(cudaIpcOpenMemHandle((void**)&peer_pool, h, cudaIpcMemLazyEnablePeerAccess));
     peer_ipc = true;
+    cudaPointerAttributes pa{};
+    CK(cudaPointerGetAttributes(&pa, peer_pool));
+    if (pa.device == cfg.device) check_same_device_pool();
     peer_dev = cfg.device;  // mapped into this context: the copy is a D2D over NVLink
     return;
   }
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (peer_dev < 0 || peer_dev >= ndev) throw ValueError("peer_device is not a visible device");
+  if (peer_dev == cfg.device) check_same_device_pool();
   if (peer_dev != cfg.device) {
     int ok = 0;
     CK(cudaDeviceCanAccessPeer(&ok, cfg.device, peer_dev));

@@ -365,12 +365,14 @@ def test_compare_engines_report():
 
 
 @pytest.mark.gpu
-def test_peer_hbm_tier_changes_latency_not_decisions():
+def test_peer_hbm_tier_changes_latency_not_decisions(monkeypatch):
     """Peer-HBM miss tier: swap-ins of experts with a home copy
     in the peer pool are served by cudaMemcpyPeerAsync instead of the host
     copy.  The tier changes only where the bytes come from: outputs, the cache
     event trace and every scheduler counter equal the host-only engine's.  On
-    a one-GPU box the pool sits on the engine's own device (same code path)."""
+    a one-GPU box the pool sits on the engine's own device (test-only mode: a
+    same-device copy runs on SMs, so the shape must leave SMs free)."""
+    monkeypatch.setenv("EF_PEER_SAME_DEVICE", "1")
     cfg = PRESETS["tiny-bf16"]
     pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
     kw = dict(budget_experts=12, policy=pol, link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2,
@@ -393,6 +395,9 @@ def test_peer_hbm_tier_changes_latency_not_decisions():
     assert sa["peer_copies"] == 0 and sa["copies"] == sb["copies"]
     assert 0 < sb["peer_copies"] < sb["copies"]
     assert sb["peer_bytes"] == sb["peer_copies"] * cfg.expert_bytes
+    monkeypatch.delenv("EF_PEER_SAME_DEVICE")
+    with pytest.raises(ValueError):
+        MoEEngine(cfg, peer_pool_experts=n_pool, **kw)
     with pytest.raises(ValueError):
         MoEEngine(cfg, peer_pool_experts=-1, **kw)
 
@@ -423,14 +428,16 @@ print("ipc ok", int(sb["peer_copies"]), int(sb["copies"]))
 
 
 @pytest.mark.gpu
-def test_peer_pool_ipc_across_processes():
+def test_peer_pool_ipc_across_processes(monkeypatch):
     """One process per GPU: this process fills a peer pool and exports its
     CUDA IPC handle; an engine in another process opens it
     (``peer_ipc_handle``) and serves its misses from it, decoding exactly like
-    a host-only engine.  On a one-GPU box both processes share the device."""
+    a host-only engine.  On a one-GPU box both processes share the device
+    (the test-only same-device mode, tiny shape)."""
     import os
     import subprocess
     import sys
+    monkeypatch.setenv("EF_PEER_SAME_DEVICE", "1")  # inherited by the child process
     cfg = PRESETS["tiny-bf16"]
     n_pool = cfg.num_layers * cfg.num_experts // 2
     owner = MoEEngine(cfg, budget_experts=12, policy=ef.PolicyConfig("a", "adaptive",
