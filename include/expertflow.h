@@ -298,12 +298,15 @@ typedef struct ef_engine_cfg {
   int32_t peer_device;        /* device holding the peer pool (may equal `device`) */
   int64_t peer_pool_experts;  /* N: pool size in experts; 0 turns the tier off */
   /* Peer-HBM miss tier (the reference models one host link,
-     SPEC.md:557): home copies of the first N experts (flat index l*M+e from 0)
-     live in a pool on the peer device; a swap-in of one of them is a
+     SPEC.md:557): home copies of N experts (the first N flat ids l*M+e, or the
+     list below) live in a pool on the peer device; a swap-in of one of them is a
      cudaMemcpyPeerAsync over NVLink instead of the host copy.  Tiers change
      only latency, never which experts are requested or admitted.  A pool on
      the engine's own device is a test-only stand-in (EF_PEER_SAME_DEVICE=1):
      same-device copies run on SMs and can deadlock a GPU-filling FFN. */
+  const int32_t* peer_pool_ids; /* optional [N] flat expert ids (l*M+e) in pool order; null:
+                                   the first N experts.  Expert-parallel placement: the home
+                                   copies of one rank's owned experts (ep.peer_pool_ids) */
   const void* peer_ipc_handle; /* non-null: 64-byte cudaIpcMemHandle_t of a pool another
                                   process (one process per GPU) created and filled on
                                   peer_device (ef_engine_peer_pool_handle); opened, not

@@ -64,7 +64,7 @@ class EngineCfg(C.Structure):
                 ("routing_bias", f32), ("seed", u64), ("device", i32), ("timing", i32),
                 ("record_routing", i32), ("max_prefill", i32), ("host_store_shm", C.c_char_p),
                 ("host_store_attach", i32), ("peer_device", i32), ("peer_pool_experts", i64),
-                ("peer_ipc_handle", vp)]
+                ("peer_pool_ids", P(i32)), ("peer_ipc_handle", vp)]
 
 
 _SIGS = {

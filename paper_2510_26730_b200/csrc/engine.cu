@@ -158,6 +158,7 @@ struct ef_engine {
   // of experts [0, peer_n) (flat l*M+e) on device peer_dev
   char* peer_pool = nullptr;
   int64_t peer_n = 0;
+  std::vector<int64_t> pool_slot_of;  // [L*M] -> index in the peer pool, -1 = not pooled
   int peer_dev = -1;
   bool peer_ipc = false;  // pool opened from another process's IPC handle
   int64_t peer_copies = 0, peer_bytes = 0;
@@ -247,10 +248,11 @@ struct ef_engine {
     int s = free_slots.front();
     free_slots.pop_front();
     const int64_t flat = idx(key);
-    if (flat < peer_n) {
+    const int64_t ps = peer_n ? pool_slot_of[flat] : -1;
+    if (ps >= 0) {
       // miss served from the peer's HBM over NVLink (copy engine, same stream,
       // so the ready flag below still lands after the blob)
-      CK(cudaMemcpyPeerAsync(slab + (int64_t)s * stride, cfg.device, peer_pool + flat * stride,
+      CK(cudaMemcpyPeerAsync(slab + (int64_t)s * stride, cfg.device, peer_pool + ps * stride,
                              peer_dev, stride, copy_stream));
       ++peer_copies;
       peer_bytes += stride;
@@ -413,6 +415,15 @@ void ef_engine::init_weights() {
 void ef_engine::init_peer_pool() {
   peer_n = std::min<int64_t>(cfg.peer_pool_experts, (int64_t)cfg.L * cfg.M);
   peer_dev = cfg.peer_device;
+  const int64_t LM = (int64_t)cfg.L * cfg.M;
+  std::vector<int64_t> ids((size_t)peer_n);
+  pool_slot_of.assign((size_t)LM, -1);
+  for (int64_t i = 0; i < peer_n; ++i) {
+    ids[i] = cfg.peer_pool_ids ? cfg.peer_pool_ids[i] : i;
+    if (ids[i] < 0 || ids[i] >= LM || pool_slot_of[ids[i]] >= 0)
+      throw ValueError("peer_pool_ids must be distinct flat expert ids in [0, L*M)");
+    pool_slot_of[ids[i]] = i;
+  }
   if (cfg.peer_ipc_handle) {
     // pool created and filled by the process that owns peer_dev
     cudaIpcMemHandle_t h;
@@ -443,9 +454,9 @@ void ef_engine::init_peer_pool() {
   }
   CK(cudaSetDevice(peer_dev));
   CK(cudaMalloc(&peer_pool, (size_t)peer_n * stride));
-  for (int64_t f = 0; f < peer_n; ++f)
-    CK(cudaMemcpy(peer_pool + f * stride, store[f / cfg.M] + (f % cfg.M) * stride, stride,
-                  cudaMemcpyHostToDevice));
+  for (int64_t i = 0; i < peer_n; ++i)
+    CK(cudaMemcpy(peer_pool + i * stride, store[ids[i] / cfg.M] + (ids[i] % cfg.M) * stride,
+                  stride, cudaMemcpyHostToDevice));
   CK(cudaSetDevice(cfg.device));
 }
 

@@ -34,6 +34,21 @@ def owned_experts(rank: int, M: int, G: int) -> List[int]:
     return [e for e in range(M) if owner(e, M, G) == rank]
 
 
+def home_pool_rank(rank: int, G: int) -> int:
+    """GPU whose spare HBM holds the home copies of ``rank``'s owned experts
+    (the peer-HBM miss tier): the next rank, so a miss never
+    reads its own device and every pool is on a different GPU."""
+    return (rank + 1) % G
+
+
+def peer_pool_ids(rank: int, L: int, M: int, G: int) -> List[int]:
+    """Flat expert ids (l*M + e) of every layer's experts owned by ``rank``,
+    in (layer, expert) order: the pool that ``home_pool_rank(rank, G)`` fills
+    and exports, and the ``peer_pool_ids`` the owner's engine opens it with."""
+    own = owned_experts(rank, M, G)
+    return [l * M + e for l in range(L) for e in own]
+
+
 @dataclass
 class DispatchPlan:
     """Where each (token, rank) row goes, in a canonical order.

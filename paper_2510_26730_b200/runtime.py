@@ -89,7 +89,8 @@ class MoEEngine:
                  emit_events: bool = False, timing: bool = False, record_routing: bool = False,
                  device: int = 0, max_prefill: int = 0, host_store_shm: Optional[str] = None,
                  host_store_attach: bool = False, peer_device: Optional[int] = None,
-                 peer_pool_experts: int = 0, peer_ipc_handle: Optional[bytes] = None):
+                 peer_pool_experts: int = 0, peer_ipc_handle: Optional[bytes] = None,
+                 peer_pool_ids: Optional[Sequence[int]] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
@@ -138,6 +139,13 @@ class MoEEngine:
             raise ValueError("peer_pool_experts must be >= 0")
         ec.peer_device = device if peer_device is None else int(peer_device)
         ec.peer_pool_experts = int(peer_pool_experts)
+        self._peer_ids = None
+        if peer_pool_ids is not None:
+            ids = [int(i) for i in peer_pool_ids]
+            if len(ids) != peer_pool_experts:
+                raise ValueError("peer_pool_ids must list peer_pool_experts flat expert ids")
+            self._peer_ids = (C.c_int32 * max(len(ids), 1))(*ids)
+            ec.peer_pool_ids = self._peer_ids
         # a pool another process (one process per GPU) created on peer_device:
         # its 64-byte handle from that engine's peer_pool_handle()
         self._peer_ipc = None

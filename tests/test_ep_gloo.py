@@ -96,6 +96,23 @@ def test_owner_partition_and_budget():
     assert ep.shard_budget(102, 8, 2, 32) == 51
 
 
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_peer_pool_placement(G):
+    """E3 placement: the pools partition every layer's experts (each expert's
+    home copy exactly once) and, for G > 1, no pool sits on its owner's GPU."""
+    L, M = 56, 8
+    seen = []
+    for r in range(G):
+        ids = ep.peer_pool_ids(r, L, M, G)
+        assert all(ep.owner(i % M, M, G) == r for i in ids)
+        assert ids == sorted(ids)
+        if G > 1:
+            assert ep.home_pool_rank(r, G) != r
+        seen += ids
+    assert sorted(seen) == list(range(L * M))
+    assert sorted(ep.home_pool_rank(r, G) for r in range(G)) == list(range(G))
+
+
 def test_per_shard_cache_traces_match_oracle():
     """E2: each rank's ExpertCache sees only its owned experts; replaying the
     same access stream through the oracle per shard gives the same trace."""

@@ -395,6 +395,18 @@ def test_peer_hbm_tier_changes_latency_not_decisions(monkeypatch):
     assert sa["peer_copies"] == 0 and sa["copies"] == sb["copies"]
     assert 0 < sb["peer_copies"] < sb["copies"]
     assert sb["peer_bytes"] == sb["peer_copies"] * cfg.expert_bytes
+    # expert-parallel placement: the home copies of rank 0's experts at G=2
+    from paper_2510_26730_b200 import ep
+    ids = ep.peer_pool_ids(0, cfg.num_layers, cfg.num_experts, 2)
+    c = MoEEngine(cfg, peer_pool_experts=len(ids), peer_pool_ids=ids, **kw)
+    for t in range(6):
+        h1 = synthetic_hidden(cfg, 5, t, 2, DEV)
+        c.step(h1)
+    torch.cuda.synchronize()
+    assert c.cache_events() == a.cache_events()
+    assert 0 < c.stats()["peer_copies"] < c.stats()["copies"]
+    with pytest.raises(ValueError):
+        MoEEngine(cfg, peer_pool_experts=2, peer_pool_ids=[3, 3], **kw)
     monkeypatch.delenv("EF_PEER_SAME_DEVICE")
     with pytest.raises(ValueError):
         MoEEngine(cfg, peer_pool_experts=n_pool, **kw)

@@ -33,14 +33,14 @@ def test_engine_cfg_struct_matches_header():
     field order (the last fields were appended for prefill and the shared
     host store)."""
     names = [f[0] for f in L.EngineCfg._fields_]
-    assert names[-6:] == ["max_prefill", "host_store_shm", "host_store_attach", "peer_device",
-                          "peer_pool_experts", "peer_ipc_handle"]
+    assert names[-7:] == ["max_prefill", "host_store_shm", "host_store_attach", "peer_device",
+                          "peer_pool_experts", "peer_pool_ids", "peer_ipc_handle"]
     hdr = open(__import__("os").path.join(__import__("os").path.dirname(__file__), "..",
                                           "include", "expertflow.h")).read()
     body = hdr[hdr.index("typedef struct ef_engine_cfg"):hdr.index("} ef_engine_cfg;")]
     pos = [body.index(n) for n in ("record_routing", "max_prefill", "host_store_shm",
                                    "host_store_attach", "peer_device", "peer_pool_experts",
-                                   "peer_ipc_handle")]
+                                   "peer_pool_ids", "peer_ipc_handle")]
     assert pos == sorted(pos)
     assert C.sizeof(L.EngineCfg) >= 96
 
