@@ -350,9 +350,12 @@ def run_ours(args, cfg, bias):
                 # second GPU's HBM (peer-HBM tier): misses are
                 # NVLink copies instead of PCIe.  Needs a second GPU: a pool on
                 # this device would copy on SMs (tools/peer_copy_lab.cu)
-                peer = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
-                                         strategy=args.strategy, bias=0.0,
-                                         peer_pool=cfg.total_experts, peer_device=1)
+                try:
+                    peer = reactive_baseline(args, cfg, budget, link_bw, layer_s, inputs, W, K,
+                                             strategy=args.strategy, bias=0.0,
+                                             peer_pool=cfg.total_experts, peer_device=1)
+                except (RuntimeError, ValueError) as exc:
+                    peer = {"unavailable": str(exc)}
 
     traffic = ncu_traffic()
     if rank == 0:
