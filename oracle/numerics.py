@@ -126,6 +126,35 @@ def router_logits(x: np.ndarray, wr: np.ndarray) -> np.ndarray:
     return np.asarray(x, np.float64) @ np.asarray(wr, np.float64).T
 
 
+def routing_mask(resident, M: int, k: int, budget_experts: int, L: int, ntok: int) -> int:
+    """Experts that get the cache-aware routing bias in one layer (engine.cu
+    ``residency_mask``): the layer's residents; when the batch could touch more
+    than the layer's share of the cache (ntok*k > U, U = max(k, budget // L))
+    and fewer than k experts are resident, topped up with the lowest-index
+    non-resident experts to U, so every token picks inside a set of at most U
+    experts and the per-layer unions fit the cache together (no cyclic-LRU
+    thrash at large batch).  No reference counterpart (routing bias is ours)."""
+    mask = 0
+    n = 0
+    for e in range(M):
+        if resident[e]:
+            mask |= 1 << e
+            n += 1
+    U = max(k, budget_experts // L)
+    if ntok * k > U and n < k:
+        for e in range(M):
+            if n >= U:
+                break
+            if not (mask >> e) & 1:
+                mask |= 1 << e
+                n += 1
+    return mask
+
+
+def mask_bits(mask: int, M: int) -> np.ndarray:
+    return np.array([(mask >> e) & 1 for e in range(M)], dtype=bool)
+
+
 def topk_select(logits: np.ndarray, k: int, bias: float = 0.0,
                 resident: Optional[np.ndarray] = None) -> np.ndarray:
     """Rank-ordered top-k keyed on fp32 (logit + bias*resident); ties -> low

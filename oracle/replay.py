@@ -44,7 +44,8 @@ def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, pol
     def pregate_fn(tt, layer, h):
         logits = log[cur["t"] * L + layer][0]
         cache = holder["st"].cache
-        mask = sum(1 << e for e in range(M) if (layer + h, e) in cache) if bias else 0
+        mask = N.routing_mask([(layer + h, e) in cache for e in range(M)], M, k, budget_experts,
+                              L, logits.shape[1]) if bias else 0
         return N.batch_gate(logits[h], bias, mask)
 
     st = OracleStepper(num_layers=L, experts_per_layer=M, top_k=k, expert_size_bytes=expert_bytes,
@@ -56,11 +57,11 @@ def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, pol
 
     def hook(layer, resident):
         logits, sel, mask = log[cur["t"] * L + layer]
-        want = sum(1 << e for e in range(M) if (layer, e) in resident) if bias else 0
+        want = N.routing_mask([(layer, e) in resident for e in range(M)], M, k, budget_experts,
+                              L, logits.shape[1]) if bias else 0
         if mask != want:
             mask_bad.append((cur["t"], layer, mask, want))
-        res = np.array([(layer, e) in resident for e in range(M)])
-        ref = N.topk_select(logits[0], k, bias, res if bias else None)
+        ref = N.topk_select(logits[0], k, bias, N.mask_bits(want, M) if bias else None)
         if not np.array_equal(ref, sel):
             sel_bad.append((cur["t"], layer))
 

@@ -280,11 +280,29 @@ struct ef_engine {
     }
   }
 
+  // Experts that get the cache-aware routing bias in `layer` (oracle/numerics.py
+  // routing_mask): its residents; when the batch could touch more than the
+  // layer's share of the cache (tokens*k > U, U = max(k, capacity / L)) and
+  // fewer than k are resident, topped up with the lowest-index non-resident
+  // experts to U, so each layer's union stays within its share and the unions
+  // fit the cache together (without it, B=32 Qwen thrashes the global LRU).
+  int mask_tokens = 1;  // tokens of the current step / prefill
   void residency_mask(int layer, uint64_t* m) const {
     m[0] = m[1] = 0;
     if (cfg.routing_bias == 0.f || layer >= cfg.L) return;
+    int n = 0;
     for (int e = 0; e < cfg.M; ++e)
-      if (st->resident(layer, e)) m[e >> 6] |= 1ull << (e & 63);
+      if (st->resident(layer, e)) {
+        m[e >> 6] |= 1ull << (e & 63);
+        ++n;
+      }
+    const int64_t U = std::max<int64_t>(cfg.top_k, st->cache().capacity() / cfg.L);
+    if ((int64_t)mask_tokens * cfg.top_k > U && n < cfg.top_k)
+      for (int e = 0; e < cfg.M && n < U; ++e)
+        if (!((m[e >> 6] >> (e & 63)) & 1ull)) {
+          m[e >> 6] |= 1ull << (e & 63);
+          ++n;
+        }
   }
 
   void enqueue_layer(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask);
@@ -691,6 +709,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
   CKS(launch_init_stats(stream, stats_d, L));
   CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
   launches += 2;
+  mask_tokens = B;
   residency_mask(0, cur_mask);
 
   std::vector<int64_t> gsizes(B, 1);
@@ -922,6 +941,7 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
   std::vector<int64_t> gsizes(T, 1);
   CKS(ef_rmsnorm(stream, h, px_d, T, d, 1e-6f));
   ++launches;
+  mask_tokens = T;
   residency_mask(0, cur_mask);
   int R = Rmax;
   for (int l = 0; l < L; ++l) {

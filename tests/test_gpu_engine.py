@@ -82,8 +82,10 @@ def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feat
 
     def pregate_fn(tt, layer, h):
         cache = holder["st"].cache
-        mask = sum(1 << e for e in range(M) if (layer + h, e) in cache) if bias else 0
-        return N.batch_gate(log[cur["t"] * L + layer][0][h], bias, mask)
+        lg = log[cur["t"] * L + layer][0]
+        mask = N.routing_mask([(layer + h, e) in cache for e in range(M)], M, cfg.top_k, budget,
+                              L, lg.shape[1]) if bias else 0
+        return N.batch_gate(lg[h], bias, mask)
 
     st = OracleStepper(num_layers=L, experts_per_layer=cfg.num_experts, top_k=cfg.top_k,
                        expert_size_bytes=cfg.expert_bytes, link_bw=link_bw,
@@ -96,10 +98,11 @@ def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feat
 
     def hook(layer, resident):
         logits, sel, mask = log[cur["t"] * L + layer]
-        want = sum(1 << e for e in range(cfg.num_experts) if (layer, e) in resident) if bias else 0
+        want = N.routing_mask([(layer, e) in resident for e in range(M)], M, cfg.top_k, budget, L,
+                              logits.shape[1]) if bias else 0
         if mask != want:
             mask_bad.append((cur["t"], layer))
-        res = np.array([(layer, e) in resident for e in range(cfg.num_experts)])
+        res = N.mask_bits(want, M)
         if not np.array_equal(N.topk_select(logits[0], cfg.top_k, bias, res if bias else None), sel):
             sel_bad.append((cur["t"], layer))
     st.pre_layer_hook = hook

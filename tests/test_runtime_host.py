@@ -70,3 +70,19 @@ def test_bench_reference_arm_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_routing_mask_top_up_rule():
+    """Cache-aware routing mask (oracle/numerics.py routing_mask, engine.cu
+    residency_mask): residents only, unless the batch could exceed the layer's
+    cache share (ntok*k > U) and fewer than k experts are resident; then the
+    lowest-index non-resident experts top it up to U = max(k, budget // L)."""
+    from oracle import numerics as N
+    M, k, L, budget = 8, 2, 4, 12  # U = 3
+    res = [False, False, True, False, False, False, False, False]
+    assert N.routing_mask(res, M, k, budget, L, 1) == 1 << 2          # 1*2 <= 3: residents only
+    assert N.routing_mask(res, M, k, budget, L, 2) == 0b111           # top up to 3 experts
+    two = [True, False, False, True, False, False, False, False]
+    assert N.routing_mask(two, M, k, budget, L, 32) == 0b1001         # k resident: no top-up
+    assert N.routing_mask([False] * M, M, k, 0, L, 32) == 0b11        # U = k when budget < L
+    assert N.mask_bits(0b101, 4).tolist() == [True, False, True, False]
