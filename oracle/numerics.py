@@ -133,7 +133,8 @@ def routing_mask(resident, M: int, k: int, budget_experts: int, L: int, ntok: in
     and fewer than k experts are resident, topped up with the lowest-index
     non-resident experts to U, so every token picks inside a set of at most U
     experts and the per-layer unions fit the cache together (no cyclic-LRU
-    thrash at large batch).  No reference counterpart (routing bias is ours)."""
+    thrash at large batch).  Decode steps only: the engine's prefill passes
+    ntok = 0 (residents only).  No reference counterpart (routing bias is ours)."""
     mask = 0
     n = 0
     for e in range(M):

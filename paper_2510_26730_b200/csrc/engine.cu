@@ -941,7 +941,10 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
   std::vector<int64_t> gsizes(T, 1);
   CKS(ef_rmsnorm(stream, h, px_d, T, d, 1e-6f));
   ++launches;
-  mask_tokens = T;
+  // prefill keeps residents-only biasing: a 2K-token prompt routed into a
+  // U-expert subset per layer would change the prompt's routing wholesale, and
+  // the grouped GEMM streams each expert once whatever the union
+  mask_tokens = 0;
   residency_mask(0, cur_mask);
   int R = Rmax;
   for (int l = 0; l < L; ++l) {
