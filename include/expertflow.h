@@ -241,21 +241,6 @@ int ef_expert_ffn_decode(void* stream, const float* x, const int32_t* perm, int 
                          const void* slab, int64_t slot_stride_bytes, const int32_t* act_slot,
                          const int32_t* act_off, const int32_t* act_rows, int n_active, int d,
                          int ff, int dtype, void* act, float* y);
-/* (d) the engine's persistent decode FFN (one launch: gate/up tiles then down
-   tiles) on an explicit active list, for tests.  scratch: device buffer of at least
-   4096 + 4 * (max slot + 1) bytes. */
-int ef_expert_ffn_persistent_test(void* stream, const float* x, const int32_t* perm, int k,
-                                  const void* slab, int64_t slot_stride_bytes,
-                                  const int32_t* act_slot, const int32_t* act_off,
-                                  const int32_t* act_rows, int n_active, int max_rows, int d,
-                                  int ff, int dtype, void* act, float* y, void* scratch);
-/* same, mode 0 = persistent register-streaming kernel, 1 = bulk-copy
-   (cp.async.bulk + mbarrier) streaming kernel (the engine default) */
-int ef_expert_ffn_ctrl_test(void* stream, const float* x, const int32_t* perm, int k,
-                            const void* slab, int64_t slot_stride_bytes, const int32_t* act_slot,
-                            const int32_t* act_off, const int32_t* act_rows, int n_active,
-                            int max_rows, int d, int ff, int dtype, void* act, float* y,
-                            void* scratch, int mode);
 /* (c) unpermute + weighted combine (rank order) + optional shared expert +
    residual + next rmsnorm:  h[t] += sum_r wts[t,r]*y[inv[t,r]] + g_t*ys[t];
    x = rmsnorm(h).  ys/shared_gate nullable. */
@@ -354,6 +339,12 @@ int ef_engine_peer_pool_handle(ef_engine* e, void* handle64);
 int ef_engine_routing_log(ef_engine* e, int64_t index, float* logits, int64_t max_logits,
                           int32_t* sel, int64_t max_sel, int32_t* R, int32_t* B,
                           uint64_t* mask_lo, uint64_t* mask_hi, int64_t* n_entries);
+/* the router input x_l [B][d] fp32 of routing log entry `index`, as the GPU
+   computed it (copied off the device when the layer was decided), and the token
+   count the cache-aware bias mask's top-up rule used (0: prefill).  Null x
+   queries *n_x.  For parity checks of every scored router row. */
+int ef_engine_routing_x(ef_engine* e, int64_t index, float* x, int64_t max_x, int64_t* n_x,
+                        int32_t* mask_tokens);
 /* physical slot of (layer, expert) or -1 */
 int ef_engine_slot_of(ef_engine* e, int32_t layer, int32_t expert, int32_t* slot);
 

@@ -83,14 +83,22 @@ def cast(a: np.ndarray, dtype: str) -> np.ndarray:
 class ModelWeights:
     """Lazily regenerates the synthetic weights of a model shape."""
 
-    def __init__(self, *, L, M, d, ff, dtype, seed, shared_ff=0, shared_gate=False):
+    def __init__(self, *, L, M, d, ff, dtype, seed, shared_ff=0, shared_gate=False,
+                 cache: bool = False):
         self.L, self.M, self.d, self.ff, self.dtype, self.seed = L, M, d, ff, dtype, seed
         self.shared_ff, self.shared_gate = shared_ff, shared_gate
+        self._cache = {} if cache else None  # regenerated matrices (large shapes, tests)
 
     def _mat(self, layer, expert, mat, rows, cols, fan_in):
+        ck = (layer, expert, mat)
+        if self._cache is not None and ck in self._cache:
+            return self._cache[ck]
         key = stream_key(self.seed, layer, expert, mat)
         v = fill_uniform(key, rows * cols, fan_scale(fan_in))
-        return cast(v, self.dtype).reshape(rows, cols)
+        m = cast(v, self.dtype).reshape(rows, cols)
+        if self._cache is not None:
+            self._cache[ck] = m
+        return m
 
     def expert(self, layer, e):
         d, ff = self.d, self.ff

@@ -35,17 +35,24 @@ def token_traces(log, L: int, tokens_per_step: Sequence[Sequence[int]],
 
 
 def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, policy: Policy,
-           tokens_per_step, bias: float = 0.0, emit_events=True):
-    """Returns (stepper, mask_mismatches, selection_mismatches)."""
+           tokens_per_step, bias: float = 0.0, emit_events=True, mask_tokens=None):
+    """Returns (stepper, mask_mismatches, selection_mismatches).
+    ``mask_tokens[i]``: the token count the engine's bias-mask top-up rule
+    used for log entry i (MoEEngine.routing_x(); 0 for prefill layers);
+    default: the entry's batch size."""
     traces = token_traces(log, L, tokens_per_step, bias)
     cur = {"t": 0}
     holder = {}
 
+    def ntok(i):
+        return log[i][0].shape[1] if mask_tokens is None else mask_tokens[i]
+
     def pregate_fn(tt, layer, h):
-        logits = log[cur["t"] * L + layer][0]
+        i = cur["t"] * L + layer
+        logits = log[i][0]
         cache = holder["st"].cache
         mask = N.routing_mask([(layer + h, e) in cache for e in range(M)], M, k, budget_experts,
-                              L, logits.shape[1]) if bias else 0
+                              L, ntok(i)) if bias else 0
         return N.batch_gate(logits[h], bias, mask)
 
     st = OracleStepper(num_layers=L, experts_per_layer=M, top_k=k, expert_size_bytes=expert_bytes,
@@ -56,9 +63,10 @@ def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, pol
     mask_bad, sel_bad = [], []
 
     def hook(layer, resident):
-        logits, sel, mask = log[cur["t"] * L + layer]
+        i = cur["t"] * L + layer
+        logits, sel, mask = log[i]
         want = N.routing_mask([(layer, e) in resident for e in range(M)], M, k, budget_experts,
-                              L, logits.shape[1]) if bias else 0
+                              L, ntok(i)) if bias else 0
         if mask != want:
             mask_bad.append((cur["t"], layer, mask, want))
         ref = N.topk_select(logits[0], k, bias, N.mask_bits(want, M) if bias else None)
@@ -73,14 +81,37 @@ def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, pol
 
 
 def forward_step(h0: np.ndarray, log, step: int, weights: N.ModelWeights, L: int, k: int,
-                 mode: str) -> np.ndarray:
-    """fp64 oracle of one decode step using the GPU's logits for selection."""
+                 mode: str, xs=None, x_errs: Optional[list] = None) -> np.ndarray:
+    """fp64 oracle of one decode step using the GPU's logits for selection.
+    With ``xs`` (MoEEngine.routing_x()), the GPU's router input of every layer
+    is compared with the oracle's x_l = rmsnorm(h_l): the relative error of
+    each layer is appended to ``x_errs`` as (step, layer, err)."""
     h = np.asarray(h0, dtype=np.float64)
     for l in range(L):
         logits, sel, _mask = log[step * L + l]
-        h = N.moe_layer(h, weights, l, k, mode, logits_override=logits[0],
-                        sel_override=sel)["h_next"]
+        out = N.moe_layer(h, weights, l, k, mode, logits_override=logits[0], sel_override=sel)
+        if xs is not None and x_errs is not None:
+            x_errs.append((step, l, rel_err(xs[step * L + l][0], out["x"])))
+        h = out["h_next"]
     return h
+
+
+def router_row_errors(log, xs, weights: N.ModelWeights, L: int):
+    """Every router row the GPU scored — the layer's own row (h = 0) and every
+    pre-gate row (h >= 1, layer l+h's router applied to x_l, kernel (b)) —
+    against the fp64 product x_l . W_r^(l+h)^T of the GPU's own x_l, so the
+    check isolates the router GEMV from the layers before it.  Returns
+    [(entry, h, token, rel_err)] with rel_err = ||gpu - ref|| / ||ref|| over
+    the M logits of one token."""
+    out = []
+    for i, ((logits, _sel, _mask), (x, _mt)) in enumerate(zip(log, xs)):
+        l = i % L
+        x64 = np.asarray(x, np.float64)
+        for h in range(logits.shape[0]):
+            ref = N.router_logits(x64, weights.router(l + h))
+            for t in range(ref.shape[0]):
+                out.append((i, h, t, rel_err(logits[h][t], ref[t])))
+    return out
 
 
 def rel_err(got, want) -> float:

@@ -125,12 +125,6 @@ _SIGS = {
                                    vp, vp, vp, vp, vp]),
     "ef_expert_ffn_decode": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
                                        C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]),
-    "ef_expert_ffn_persistent_test": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
-                                                C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
-                                                vp, vp]),
-    "ef_expert_ffn_ctrl_test": (C.c_int, [vp, vp, vp, C.c_int, vp, i64, P(i32), P(i32), P(i32),
-                                          C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp,
-                                          C.c_int]),
     "ef_combine": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, f32]),
     "ef_gather_rows_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "ef_grouped_gemm_bf16": (C.c_int, [vp, vp, i64, C.c_int, vp, i64, i64, vp, C.c_int, C.c_int,
@@ -149,6 +143,7 @@ _SIGS = {
     "ef_engine_slot_of": (C.c_int, [vp, i32, i32, P(i32)]),
     "ef_engine_routing_log": (C.c_int, [vp, i64, P(f32), i64, P(i32), i64, P(i32), P(i32), P(u64),
                                         P(u64), P(i64)]),
+    "ef_engine_routing_x": (C.c_int, [vp, i64, P(f32), i64, P(i64), P(i32)]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -189,8 +189,19 @@ struct ef_engine {
     std::vector<int32_t> sel;
     int R, B;
     uint64_t mlo, mhi;
+    std::vector<float> x;  // the layer's router input x_l [B, d] as the GPU computed it
+    int mask_tokens;       // tokens the bias mask's top-up rule saw (0: prefill)
   };
   std::vector<RoutingRec> rlog;
+  // record_routing: the router input of each executed layer, copied by the
+  // copy engine (never an SM: the FFN may be spinning on a host flag)
+  float* xrec_h = nullptr;
+  cudaStream_t rec_stream = nullptr;
+  std::vector<float> record_x(const float* xd, int64_t n) {
+    CK(cudaMemcpyAsync(xrec_h, xd, sizeof(float) * n, cudaMemcpyDeviceToHost, rec_stream));
+    CK(cudaStreamSynchronize(rec_stream));
+    return std::vector<float>(xrec_h, xrec_h + n);
+  }
   // stats
   int64_t steps = 0, copies = 0, copy_bytes = 0, launches = 0, preload_copies = 0,
           d2h_bytes = 0, ffn_bytes = 0, ffn_launches = 0;
@@ -310,8 +321,6 @@ struct ef_engine {
   std::vector<int> layer_R;  // router matrices scored at each layer this step
   void enqueue_back(cudaStream_t stream, int l, int B, float* h);
   bool debug = false;  // EF_PIPE_DEBUG=1: no run-ahead, sync + check after each half-layer
-  int ffn_mode = 2;  // EF_FFN: split (GEMV pair, default) | stream (bulk-copy) | persistent
-  int* counters_d = nullptr;
   // EF_FUSE bit mask: 1 router+route in one kernel, 2 gate folded into the
   // up kernel, 8 combine(l-1) + rmsnorm folded into router_route(l)
   int fuse = 27;
@@ -327,10 +336,10 @@ struct ef_engine {
   int2* host_tab = nullptr;  // [L*M] {slot, fill seq} host mirror of phys_of
   unsigned* fast_words = nullptr;  // [L]
   int64_t fast_layers = 0;
-  bool fast_path() const { return (fuse & 16) && (fuse & 3) == 3 && ffn_mode == 2 && !debug; }
+  bool fast_path() const { return (fuse & 16) && (fuse & 3) == 3 && !debug; }
   // the gate folded into the up kernel waits for go >= its launch sequence
   // number (monotonic); the separate gate kernel uses a 0/1 flag it resets
-  bool fused_gate() const { return (fuse & 2) && ffn_mode == 2; }
+  bool fused_gate() const { return (fuse & 2) != 0; }
   void set_phys(int64_t i, int s) {
     phys_of[i] = s;
     host_tab[i] = make_int2(s, s >= 0 ? (int)slot_seq[s] : 0);
@@ -496,7 +505,7 @@ ef_engine::~ef_engine() {
   for (void* p : {(void*)slab, router_w, (void*)shared_w, sgate_w, (void*)x_d, (void*)logits_d,
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
-                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)counters_d, (void*)fuse_d, (void*)h_io_d,
+                  (void*)dctrl, (void*)ready, (void*)stats_d, (void*)fuse_d, (void*)h_io_d,
                   (void*)fast_words, (void*)px_d, (void*)plogits_d, (void*)pwts_d, (void*)py_d,
                   (void*)pys_d, (void*)psgl_d, (void*)psel_d, (void*)pcounts_d, (void*)poffsets_d,
                   (void*)pperm_d, (void*)pinv_d, (void*)piota_d, pA_d, pact_d, pacts_d,
@@ -514,6 +523,8 @@ ef_engine::~ef_engine() {
     for (char* p : store)
       if (p) cudaFreeHost(p);
   }
+  if (xrec_h) cudaFreeHost(xrec_h);
+  if (rec_stream) cudaStreamDestroy(rec_stream);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (compute_stream) cudaStreamDestroy(compute_stream);
   if (join_in) cudaEventDestroy(join_in);
@@ -585,7 +596,7 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   const int M = cfg.M, k = cfg.top_k, d = cfg.d;
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
   const bool comb_next = comb_in_router(l + 1, B);
-  if ((fuse & 2) && ffn_mode == 2) {
+  if (fuse & 2) {
     GateIO io{};
     if (fast_path()) {
       io = GateIO{fast_words + l, sel_d, logits_d, B * k, layer_R[l] * B * M,
@@ -604,22 +615,11 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
     }
     return;
   }
-  CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + kStats * l,
-                  ffn_mode != 2 ? counters_d : nullptr));
+  CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + kStats * l));
   ++launches;
-  if (ffn_mode == 0) {
-    CKS(expert_ffn_stream(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
-                          counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
-    launches += 1;
-  } else if (ffn_mode == 1) {
-    CKS(expert_ffn_persistent(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready,
-                              stats_d + kStats * l, counters_d, B, d, cfg.ff, cfg.dtype, act_d, y_d));
-    launches += 1;
-  } else {
-    CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
-                        std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
-    launches += 2;
-  }
+  CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
+                      std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
+  launches += 2;
   if (comb_next) return;
   CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
                       sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
@@ -784,9 +784,11 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
         batch_gate(lg0 + (int64_t)hz * B * M, B, M, cfg.routing_bias, m, o);
       };
       if (cfg.record_routing) {
+        // route(l) has completed, so x_d holds x_l until layer l+1 is enqueued
         std::vector<float> lg(lg0, lg0 + (int64_t)R * B * M);
         rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(sel, sel + B * k), R, B,
-                                  cur_mask[0], cur_mask[1]});
+                                  cur_mask[0], cur_mask[1], record_x(x_d, (int64_t)B * cfg.d),
+                                  mask_tokens});
       }
       // the route kernel may have started FFN(l) on the slots of its table
       // row (fast path): keep them until FFN(l) is done, whatever this
@@ -988,7 +990,8 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
     if (cfg.record_routing) {
       std::vector<float> lg(lg0, lg0 + (int64_t)R * T * M);
       rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(psel_h, psel_h + T * k), R, T,
-                                cur_mask[0], cur_mask[1]});
+                                cur_mask[0], cur_mask[1], record_x(px_d, (int64_t)T * d),
+                                mask_tokens});
     }
     if (l == 0) st->begin_token(tokens, gsizes, r);
     std::fill(layer_use.begin(), layer_use.end(), -1);
@@ -1219,6 +1222,11 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       CK(cudaEventCreateWithFlags(&e->join_in, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&e->join_out, cudaEventDisableTiming));
     }
+    if (c.record_routing) {
+      CK(cudaHostAlloc(&e->xrec_h, sizeof(float) * std::max(B, c.max_prefill) * d,
+                       cudaHostAllocDefault));
+      CK(cudaStreamCreateWithFlags(&e->rec_stream, cudaStreamNonBlocking));
+    }
     e->slot_seq.assign(e->P, 0);
     e->pinned.assign(e->P, 0);
     e->phys_of.assign((size_t)L * M, -1);
@@ -1231,10 +1239,6 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     if (preload_pipeline_kernels() < 30) throw CudaErr("could not load the pipeline kernels");
     const char* dbg = getenv("EF_PIPE_DEBUG");
     e->debug = dbg && dbg[0] == '1';
-    const char* ffn = getenv("EF_FFN");
-    if (ffn && std::string(ffn) == "persistent") e->ffn_mode = 1;
-    if (ffn && std::string(ffn) == "stream") e->ffn_mode = 0;
-    CK(cudaMalloc(&e->counters_d, sizeof(int) * (kMaxActive + 1)));
     CK(cudaHostAlloc(&e->host_tab, sizeof(int2) * L * M, cudaHostAllocDefault));
     for (int64_t i = 0; i < (int64_t)L * M; ++i) e->host_tab[i] = make_int2(-1, 0);
     CK(cudaMalloc(&e->fast_words, sizeof(unsigned) * L));
@@ -1366,6 +1370,18 @@ extern "C" int ef_engine_routing_log(ef_engine* e, int64_t index, float* logits,
     if (sel)
       std::memcpy(sel, r.sel.data(),
                   sizeof(int32_t) * std::min<int64_t>(max_sel, (int64_t)r.sel.size()));
+  });
+}
+
+extern "C" int ef_engine_routing_x(ef_engine* e, int64_t index, float* x, int64_t max_x,
+                                   int64_t* n_x, int32_t* mask_tokens) {
+  EF_TRY({
+    if (index < 0 || index >= (int64_t)e->rlog.size())
+      throw ValueError("routing log index out of range");
+    const auto& r = e->rlog[index];
+    *n_x = (int64_t)r.x.size();
+    *mask_tokens = r.mask_tokens;
+    if (x) std::memcpy(x, r.x.data(), sizeof(float) * std::min<int64_t>(max_x, *n_x));
   });
 }
 

@@ -1489,538 +1489,6 @@ int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k,
   return EF_OK;
 }
 
-// ------------------------------------------------------------ persistent FFN
-// One launch per layer for the routed experts (engine pipeline).  CTAs claim
-// tiles from an atomic counter: first every gate/up tile of every active
-// expert (8 rows of ff each, one row per warp: W1 and W3 rows streamed
-// together, fused SiLU*up), then every down tile (8 rows of d).  A down tile
-// waits only for the up tiles of its own expert (per-expert completion
-// counter) and prefetches its first W2 chunks before waiting.  Claiming is
-// dynamic, so a CTA only ever waits on tiles that running CTAs already
-// claimed: deadlock-free at any occupancy.  Up tiles of an expert whose
-// swap-in is still in flight spin on ready[slot]; tiles of resident experts
-// keep the GPU streaming meanwhile.
-struct PersistArgs {
-  const DevCtrl* ctrl;
-  const char* slab;
-  int64_t stride;
-  const volatile uint32_t* ready;
-  unsigned long long* stats;
-  int* counters;  // [0] tile counter, [1 + a] up tiles done for active expert a
-  const float* x;
-  const int32_t* perm;
-  int k, d, ff;
-  void* act;
-  float* y;
-};
-
-constexpr int kPWarps = 8;  // rows per tile
-constexpr int kPUnroll = 4; // 16-byte chunks in flight per matrix per lane
-
-template <typename WT, int NT>
-__global__ void __launch_bounds__(kPWarps * 32) ffn_persist_kernel(PersistArgs p) {
-  constexpr int V = WTraits<WT>::kPer16;
-  constexpr int CH = 32 * V;  // columns per warp-wide chunk
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __shared__ int tile_sh[2];
-  __shared__ int4 ent_sh;
-  __shared__ int landed_sh;  // down tile: slot copy already landed -> W2 prefetch is safe
-  const int n_active = p.ctrl->n_active;
-  const int n_up = (p.ff + kPWarps - 1) / kPWarps;
-  const int n_dn = (p.d + kPWarps - 1) / kPWarps;
-  const int total_up = n_active * n_up;
-  const int total = total_up + n_active * n_dn;
-  const int64_t es = sizeof(WT);
-  WT* act = reinterpret_cast<WT*>(p.act);
-  bool started = false;
-  if (threadIdx.x == 0) tile_sh[0] = atomicAdd(&p.counters[0], 1);
-  __syncthreads();
-  int buf = 0;
-  for (;;) {
-    const int t = tile_sh[buf];
-    if (t >= total) break;
-    // claim the next tile early so its atomic latency overlaps this tile
-    if (threadIdx.x == 0) tile_sh[buf ^ 1] = atomicAdd(&p.counters[0], 1);
-    const bool up = t < total_up;
-    const int a = up ? t / n_up : (t - total_up) / n_dn;
-    const int row = (up ? t % n_up : (t - total_up) % n_dn) * kPWarps + wid;
-    if (threadIdx.x == 0) {
-      int4 e = p.ctrl->ent[a];
-      if (up) {
-        unsigned need = (unsigned)e.w;
-        if (p.ready[e.x] < need) {
-          unsigned long long t0 = globaltimer();
-          const long long c0 = clock64();
-          while (p.ready[e.x] < need) {
-            __nanosleep(256);
-            if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
-          }
-          unsigned long long t1 = globaltimer();
-          if (t1 > t0) atomicMax(&p.stats[2], t1 - t0);
-        }
-      }
-      else {
-        landed_sh = p.ready[e.x] >= (unsigned)e.w;
-        __threadfence();
-      }
-      ent_sh = e;
-      if (!started) atomicMin(&p.stats[3], globaltimer());
-    }
-    started = true;
-    __syncthreads();
-    const int4 e = ent_sh;
-    const char* w = p.slab + (int64_t)e.x * p.stride;
-    const int p0 = e.y, n_all = e.z;
-    if (up) {
-      const int rows = p.ff, cols = p.d;
-      const WT* A = reinterpret_cast<const WT*>(w) + (int64_t)min(row, rows - 1) * cols;
-      const WT* Bm = reinterpret_cast<const WT*>(w + (int64_t)rows * cols * es) +
-                     (int64_t)min(row, rows - 1) * cols;
-      for (int tc = 0; tc < n_all; tc += NT) {
-        const int nt = min(NT, n_all - tc);
-        const float* xr[NT];
-#pragma unroll
-        for (int q = 0; q < NT; ++q) xr[q] = p.x + (int64_t)(p.perm[p0 + tc + (q < nt ? q : 0)] / p.k) * cols;
-        float ga[NT], ua[NT];
-#pragma unroll
-        for (int q = 0; q < NT; ++q) ga[q] = ua[q] = 0.f;
-        for (int c0 = lane * V; c0 < cols; c0 += kPUnroll * CH) {
-          uint4 wa[kPUnroll], wb[kPUnroll];
-#pragma unroll
-          for (int u = 0; u < kPUnroll; ++u) {
-            int c = c0 + u * CH;
-            if (c < cols) {
-              wa[u] = ld_stream16(A + c);
-              wb[u] = ld_stream16(Bm + c);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kPUnroll; ++u) {
-            int c = c0 + u * CH;
-            if (c < cols) {
-              float fa[V], fb[V];
-              WTraits<WT>::unpack(wa[u], fa);
-              WTraits<WT>::unpack(wb[u], fb);
-#pragma unroll
-              for (int q = 0; q < NT; ++q) {
-                if (q < nt) {
-                  const float4* xp = reinterpret_cast<const float4*>(xr[q] + c);
-#pragma unroll
-                  for (int v4 = 0; v4 < V / 4; ++v4) {
-                    float4 xv = __ldg(xp + v4);
-                    float xs[4] = {WTraits<WT>::cast(xv.x), WTraits<WT>::cast(xv.y),
-                                   WTraits<WT>::cast(xv.z), WTraits<WT>::cast(xv.w)};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                      ga[q] = fmaf(fa[4 * v4 + i], xs[i], ga[q]);
-                      ua[q] = fmaf(fb[4 * v4 + i], xs[i], ua[q]);
-                    }
-                  }
-                }
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < NT; ++q) {
-          if (q < nt) {
-            float g = warp_sum(ga[q]);
-            float u = warp_sum(ua[q]);
-            if (lane == 0 && row < rows)
-              WTraits<WT>::store(act + (int64_t)(p0 + tc + q) * rows + row, g / (1.0f + expf(-g)) * u);
-          }
-        }
-      }
-      __threadfence();  // every writer publishes its act rows before the count
-      __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(&p.counters[1 + a], 1);
-    } else {
-      const int rows = p.d, cols = p.ff;
-      const WT* A = reinterpret_cast<const WT*>(w + 2 * (int64_t)p.ff * p.d * es) +
-                    (int64_t)min(row, rows - 1) * cols;
-      // prefetch the first W2 chunks (only if the slot's swap-in has landed),
-      // then wait for this expert's up tiles
-      const bool pref = landed_sh != 0;
-      uint4 pre[kPUnroll];
-#pragma unroll
-      for (int u = 0; u < kPUnroll; ++u) {
-        int c = lane * V + u * CH;
-        if (pref && c < cols) pre[u] = ld_stream16(A + c);
-      }
-      if (threadIdx.x == 0) {
-        volatile int* done = p.counters + 1 + a;
-        const long long c0 = clock64();
-        while (*done < n_up) {
-          __nanosleep(64);
-          if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
-        }
-        __threadfence();
-      }
-      __syncthreads();
-      for (int tc = 0; tc < n_all; tc += NT) {
-        const int nt = min(NT, n_all - tc);
-        float acc[NT];
-#pragma unroll
-        for (int q = 0; q < NT; ++q) acc[q] = 0.f;
-        for (int c0 = lane * V; c0 < cols; c0 += kPUnroll * CH) {
-          uint4 wa[kPUnroll];
-#pragma unroll
-          for (int u = 0; u < kPUnroll; ++u) {
-            int c = c0 + u * CH;
-            if (c < cols) wa[u] = (pref && tc == 0 && c0 == lane * V) ? pre[u] : ld_stream16(A + c);
-          }
-#pragma unroll
-          for (int u = 0; u < kPUnroll; ++u) {
-            int c = c0 + u * CH;
-            if (c < cols) {
-              float fa[V];
-              WTraits<WT>::unpack(wa[u], fa);
-#pragma unroll
-              for (int q = 0; q < NT; ++q) {
-                if (q < nt) {
-                  // act was written by other CTAs of this launch: bypass L1
-                  uint4 av = __ldcg(reinterpret_cast<const uint4*>(
-                      act + (int64_t)(p0 + tc + q) * cols + c));
-                  float fx[V];
-                  WTraits<WT>::unpack(av, fx);
-#pragma unroll
-                  for (int i = 0; i < V; ++i) acc[q] = fmaf(fa[i], fx[i], acc[q]);
-                }
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < NT; ++q) {
-          if (q < nt) {
-            float g = warp_sum(acc[q]);
-            if (lane == 0 && row < rows) p.y[(int64_t)(p0 + tc + q) * rows + row] = g;
-          }
-        }
-      }
-    }
-    __syncthreads();  // tile_sh[buf] consumed; the claim for the next slot is visible
-    buf ^= 1;
-  }
-  if (started && threadIdx.x == 0) atomicMax(&p.stats[4], globaltimer());
-}
-
-// ------------------------------------------------------------ bulk-streaming FFN
-// The engine's default decode FFN.  One CTA per SM; a producer warp streams
-// weight tiles HBM -> shared memory with cp.async.bulk (one bulk copy per
-// contiguous row block, mbarrier transaction counts), 8 consumer warps dot
-// them against the token vectors.  Bytes in flight per SM = STAGES x tile, no
-// longer tied to register pressure or occupancy.
-//   up tile   = rows [j0, j0+RU) of W1 and of W3 (two copies, one stage);
-//               warp w computes one row-dot, g/u exchanged through smem,
-//               act = T(silu(g) * u) stored to global
-//   down tile = rows [i0, i0+RD) of W2 (one copy); WPR warps per row split the
-//               columns, partials reduced through smem, y stored
-// Tiles are claimed dynamically by the producer (atomic counter): every up
-// tile precedes every down tile in claim order, so a down tile waiting for
-// its expert's up tiles only waits on tiles running CTAs already hold.  The
-// producer waits on an expert's ready flag before its first copy; consumers
-// keep computing the stages already loaded.
-constexpr int kSWarps = 8;                 // consumer warps
-constexpr int kSThreads = (kSWarps + 1) * 32;
-constexpr int kSStages = 3;
-constexpr int kSStageBytes = 64 * 1024;
-
-struct StreamArgs {
-  const DevCtrl* ctrl;
-  const char* slab;
-  int64_t stride;
-  const volatile uint32_t* ready;
-  unsigned long long* stats;
-  int* counters;  // [0] tile counter, [1 + a] up tiles done of active expert a
-  const float* x;
-  const int32_t* perm;
-  int k, d, ff;
-  int RU, RD, WPR;  // rows per up tile, rows per down tile, warps per down row
-  void* act;
-  float* y;
-};
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          (uint32_t)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
-      : "memory");
-}
-__device__ __forceinline__ void sbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(count));
-}
-__device__ __forceinline__ void sbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void sbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-__device__ __forceinline__ void sbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(bar);
-  uint32_t done = 0;
-  const long long c0 = clock64();
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (!done && clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
-  } while (!done);
-}
-
-template <typename WT, int NT>
-__global__ void __launch_bounds__(kSThreads, 1) ffn_stream_kernel(StreamArgs p) {
-  constexpr int V = WTraits<WT>::kPer16;
-  constexpr int64_t es = sizeof(WT);
-  extern __shared__ __align__(128) uint8_t sm[];
-  uint8_t* stage_buf = sm;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kSStages * kSStageBytes);
-  uint64_t* empty = full + kSStages;
-  int* stage_tile = reinterpret_cast<int*>(empty + kSStages);
-  float* red = reinterpret_cast<float*>(stage_tile + kSStages);  // [kSWarps][NT] partials
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_active = p.ctrl->n_active;
-  const int n_up = (p.ff + p.RU - 1) / p.RU;
-  const int n_dn = (p.d + p.RD - 1) / p.RD;
-  const int total_up = n_active * n_up;
-  const int total = total_up + n_active * n_dn;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kSStages; ++s) {
-      sbar_init(&full[s], 1);
-      sbar_init(&empty[s], kSWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == kSWarps) {  // ---------------- producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int last_ready_a = -1;
-      bool started = false;
-      for (;;) {
-        const int t = atomicAdd(&p.counters[0], 1);
-        sbar_wait(&empty[stage], phase ^ 1);
-        if (t >= total) {  // sentinel: tell the consumers to stop
-          stage_tile[stage] = -1;
-          sbar_arrive(&full[stage]);
-          break;
-        }
-        const bool up = t < total_up;
-        const int a = up ? t / n_up : (t - total_up) / n_dn;
-        const int4 e = p.ctrl->ent[a];
-        if (a != last_ready_a && p.ready[e.x] < (unsigned)e.w) {
-          unsigned long long t0 = globaltimer();
-          const long long c0 = clock64();
-          while (p.ready[e.x] < (unsigned)e.w) {
-            __nanosleep(256);
-            if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
-          }
-          unsigned long long t1 = globaltimer();
-          if (t1 > t0) atomicMax(&p.stats[2], t1 - t0);
-        }
-        last_ready_a = a;
-        if (!started) {
-          atomicMin(&p.stats[3], globaltimer());
-          started = true;
-        }
-        const char* w = p.slab + (int64_t)e.x * p.stride;
-        uint8_t* dst = stage_buf + (int64_t)stage * kSStageBytes;
-        stage_tile[stage] = t;
-        if (up) {
-          const int j0 = (t % n_up) * p.RU, nr = min(p.RU, p.ff - j0);
-          const uint32_t bytes = (uint32_t)(nr * p.d * es);
-          sbar_expect_tx(&full[stage], 2 * bytes);
-          bulk_g2s(dst, w + (int64_t)j0 * p.d * es, bytes, &full[stage]);
-          bulk_g2s(dst + (int64_t)p.RU * p.d * es, w + ((int64_t)p.ff + j0) * p.d * es, bytes,
-                   &full[stage]);
-        } else {
-          const int i0 = ((t - total_up) % n_dn) * p.RD, nr = min(p.RD, p.d - i0);
-          const uint32_t bytes = (uint32_t)(nr * p.ff * es);
-          sbar_expect_tx(&full[stage], bytes);
-          bulk_g2s(dst, w + (2 * (int64_t)p.ff * p.d + (int64_t)i0 * p.ff) * es, bytes,
-                   &full[stage]);
-        }
-        if (++stage == kSStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers
-  WT* act = reinterpret_cast<WT*>(p.act);
-  int stage = 0;
-  uint32_t phase = 0;
-  for (;;) {
-    sbar_wait(&full[stage], phase);
-    const int t = stage_tile[stage];
-    if (t < 0) break;
-    const bool up = t < total_up;
-    const int a = up ? t / n_up : (t - total_up) / n_dn;
-    const int4 e = p.ctrl->ent[a];
-    const int p0 = e.y, n_all = e.z;
-    const uint8_t* tile = stage_buf + (int64_t)stage * kSStageBytes;
-    if (up) {
-      const int j0 = (t % n_up) * p.RU, nr = min(p.RU, p.ff - j0);
-      const int rows_total = 2 * p.RU;  // W1 rows then W3 rows (RU each) in the stage
-      for (int tc = 0; tc < n_all; tc += NT) {
-        const int nt = min(NT, n_all - tc);
-        const float* xr[NT];
-#pragma unroll
-        for (int q = 0; q < NT; ++q)
-          xr[q] = p.x + (int64_t)(p.perm[p0 + tc + (q < nt ? q : 0)] / p.k) * p.d;
-        for (int rr = warp; rr < rows_total; rr += kSWarps) {
-          const int mat = rr / p.RU, r = rr % p.RU;
-          float acc[NT];
-#pragma unroll
-          for (int q = 0; q < NT; ++q) acc[q] = 0.f;
-          if (r < nr) {
-            const WT* row = reinterpret_cast<const WT*>(tile) + (int64_t)(mat * p.RU + r) * p.d;
-            for (int c = lane * V; c < p.d; c += 32 * V) {
-              float f[V];
-              WTraits<WT>::unpack(*reinterpret_cast<const uint4*>(row + c), f);
-#pragma unroll
-              for (int q = 0; q < NT; ++q) {
-                if (q < nt) {
-                  const float4* xp = reinterpret_cast<const float4*>(xr[q] + c);
-#pragma unroll
-                  for (int v4 = 0; v4 < V / 4; ++v4) {
-                    float4 xv = __ldg(xp + v4);
-                    acc[q] = fmaf(f[4 * v4 + 0], WTraits<WT>::cast(xv.x), acc[q]);
-                    acc[q] = fmaf(f[4 * v4 + 1], WTraits<WT>::cast(xv.y), acc[q]);
-                    acc[q] = fmaf(f[4 * v4 + 2], WTraits<WT>::cast(xv.z), acc[q]);
-                    acc[q] = fmaf(f[4 * v4 + 3], WTraits<WT>::cast(xv.w), acc[q]);
-                  }
-                }
-              }
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < NT; ++q) {
-            float v = warp_sum(acc[q]);
-            if (lane == 0) red[rr * NT + q] = v;  // red holds 2*RU*NT partials
-          }
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));  // consumers only
-        for (int i = threadIdx.x; i < nr * nt; i += kSWarps * 32) {
-          const int r = i / nt, q = i % nt;
-          const float g = red[r * NT + q], u = red[(p.RU + r) * NT + q];
-          WTraits<WT>::store(act + (int64_t)(p0 + tc + q) * p.ff + j0 + r, g / (1.0f + expf(-g)) * u);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
-      }
-      // this stage is consumed; publish the act rows, then count the tile
-      __threadfence();
-      asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
-      if (lane == 0) sbar_arrive(&empty[stage]);
-      if (threadIdx.x == 0) atomicAdd(&p.counters[1 + a], 1);
-    } else {
-      const int i0 = ((t - total_up) % n_dn) * p.RD, nr = min(p.RD, p.d - i0);
-      if (threadIdx.x == 0) {  // wait for this expert's up tiles (act complete)
-        volatile int* done = p.counters + 1 + a;
-        const long long c0 = clock64();
-        while (*done < n_up) {
-          __nanosleep(64);
-          if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
-        }
-        __threadfence();
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
-      const int r = warp / p.WPR, part = warp % p.WPR;
-      const int span = ((p.ff + p.WPR - 1) / p.WPR + 32 * V - 1) / (32 * V) * (32 * V);
-      const int c_begin = part * span, c_end = min(p.ff, c_begin + span);
-      for (int tc = 0; tc < n_all; tc += NT) {
-        const int nt = min(NT, n_all - tc);
-        float acc[NT];
-#pragma unroll
-        for (int q = 0; q < NT; ++q) acc[q] = 0.f;
-        if (r < nr) {
-          const WT* row = reinterpret_cast<const WT*>(tile) + (int64_t)r * p.ff;
-          for (int c = c_begin + lane * V; c < c_end; c += 32 * V) {
-            float f[V];
-            WTraits<WT>::unpack(*reinterpret_cast<const uint4*>(row + c), f);
-#pragma unroll
-            for (int q = 0; q < NT; ++q) {
-              if (q < nt) {
-                uint4 av = __ldcg(reinterpret_cast<const uint4*>(act + (int64_t)(p0 + tc + q) * p.ff + c));
-                float fx[V];
-                WTraits<WT>::unpack(av, fx);
-#pragma unroll
-                for (int i = 0; i < V; ++i) acc[q] = fmaf(f[i], fx[i], acc[q]);
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < NT; ++q) {
-          float v = warp_sum(acc[q]);
-          if (lane == 0) red[warp * NT + q] = v;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
-        for (int i = threadIdx.x; i < nr * nt; i += kSWarps * 32) {
-          const int rr = i / nt, q = i % nt;
-          float v = 0.f;
-          for (int w = 0; w < p.WPR; ++w) v += red[(rr * p.WPR + w) * NT + q];
-          p.y[(int64_t)(p0 + tc + q) * p.d + i0 + rr] = v;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kSWarps * 32));
-      }
-      if (lane == 0) sbar_arrive(&empty[stage]);
-    }
-    if (++stage == kSStages) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-  if (threadIdx.x == 0) atomicMax(&p.stats[4], globaltimer());
-}
-
-template <typename WT, int NT>
-static int launch_stream_nt(cudaStream_t st, const StreamArgs& sa) {
-  constexpr int smem = kSStages * kSStageBytes + 2 * kSStages * 8 + kSStages * 4 + 16 * NT * 4 + 64;
-  static int grid = 0;
-  if (!grid) {
-    if (cudaFuncSetAttribute(ffn_stream_kernel<WT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess)
-      return EF_ECUDA;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev);
-  }
-  ffn_stream_kernel<WT, NT><<<grid, kSThreads, smem, st>>>(sa);
-  return EF_OK;
-}
-
-template <typename WT, int NT>
-static int launch_persist_nt(cudaStream_t st, const PersistArgs& pa) {
-  static int grid = 0;
-  if (!grid) {
-    int occ = 0, dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffn_persist_kernel<WT, NT>,
-                                                  kPWarps * 32, 0);
-    grid = std::max(1, occ) * sms;
-  }
-  ffn_persist_kernel<WT, NT><<<grid, kPWarps * 32, 0, st>>>(pa);
-  return EF_OK;
-}
-
 // ------------------------------------------------------------ pipeline glue
 __device__ __forceinline__ uint2 ld_acquire_sys_v2(const volatile void* p) {
   uint2 v;
@@ -2041,11 +1509,8 @@ __device__ __forceinline__ int4 ld_volatile_v4(const volatile void* p) {
 
 // One warp: spin on the host's go flag (8-byte acquire load returns go and
 // n_active together), copy the decision with one 16-byte PCIe read per entry.
-__global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats,
-                            int* counters) {
+__global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long* stats) {
   const int lane = threadIdx.x;
-  if (counters)  // fresh tile / completion counters for this layer's persistent FFN
-    for (int i = lane; i <= kMaxActive; i += 32) counters[i] = 0;
   uint2 gn = make_uint2(0, 0);
   if (lane == 0) {
     stats[0] = globaltimer();
@@ -2068,144 +1533,9 @@ __global__ void gate_kernel(volatile HostCtrl* hc, DevCtrl* dc, unsigned long lo
   }
 }
 
-int expert_ffn_persistent(cudaStream_t st, const float* x, const int32_t* perm, int k,
-                          const char* slab, int64_t stride, const void* dctrl,
-                          const uint32_t* ready, unsigned long long* stats, int* counters,
-                          int max_rows, int d, int ff, int dtype, void* act, float* y) {
-  PersistArgs pa{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, counters,
-                 x, perm, k, d, ff, act, y};
-  EF_CHECK_ARG(d % 256 == 0 && ff % 8 == 0, "d must be a multiple of 256 and ff of 8");
-  if (dtype == EF_BF16) {
-    if (max_rows <= 1) launch_persist_nt<__nv_bfloat16, 1>(st, pa);
-    else if (max_rows <= 2) launch_persist_nt<__nv_bfloat16, 2>(st, pa);
-    else if (max_rows <= 4) launch_persist_nt<__nv_bfloat16, 4>(st, pa);
-    else launch_persist_nt<__nv_bfloat16, 8>(st, pa);
-  } else {
-    if (max_rows <= 1) launch_persist_nt<float, 1>(st, pa);
-    else if (max_rows <= 2) launch_persist_nt<float, 2>(st, pa);
-    else if (max_rows <= 4) launch_persist_nt<float, 4>(st, pa);
-    else launch_persist_nt<float, 8>(st, pa);
-  }
-  EF_CUDA_RET(cudaGetLastError());
-  return EF_OK;
-}
-
-// Test entry: run the persistent FFN on an explicit active list (slots are
-// treated as resident).  scratch: device buffer >= sizeof(DevCtrl) +
-// 4*(kMaxActive+1) + 8*8 + 4*max_slot+4 bytes.
-int expert_ffn_stream(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
-                      int64_t stride, const void* dctrl, const uint32_t* ready,
-                      unsigned long long* stats, int* counters, int max_rows, int d, int ff,
-                      int dtype, void* act, float* y);
-
-extern "C" int ef_expert_ffn_ctrl_test(void* stream, const float* x, const int32_t* perm, int k,
-                                       const void* slab, int64_t stride, const int32_t* act_slot,
-                                       const int32_t* act_off, const int32_t* act_rows,
-                                       int n_active, int max_rows, int d, int ff, int dtype,
-                                       void* act, float* y, void* scratch, int mode);
-
-extern "C" int ef_expert_ffn_persistent_test(void* stream, const float* x, const int32_t* perm,
-                                             int k, const void* slab, int64_t stride,
-                                             const int32_t* act_slot, const int32_t* act_off,
-                                             const int32_t* act_rows, int n_active, int max_rows,
-                                             int d, int ff, int dtype, void* act, float* y,
-                                             void* scratch) {
-  return ef_expert_ffn_ctrl_test(stream, x, perm, k, slab, stride, act_slot, act_off, act_rows,
-                                 n_active, max_rows, d, ff, dtype, act, y, scratch, 0);
-}
-
-// mode 0: persistent register-streaming FFN, 1: bulk-copy streaming FFN
-extern "C" int ef_expert_ffn_ctrl_test(void* stream, const float* x, const int32_t* perm, int k,
-                                       const void* slab, int64_t stride, const int32_t* act_slot,
-                                       const int32_t* act_off, const int32_t* act_rows,
-                                       int n_active, int max_rows, int d, int ff, int dtype,
-                                       void* act, float* y, void* scratch, int mode) {
-  EF_CHECK_ARG(n_active >= 0 && n_active <= kMaxActive, "too many active experts");
-  DevCtrl h{};
-  h.n_active = n_active;
-  int max_slot = 0;
-  for (int i = 0; i < n_active; ++i) {
-    h.ent[i] = make_int4(act_slot[i], act_off[i], act_rows[i], 0);
-    max_slot = std::max(max_slot, act_slot[i]);
-  }
-  char* base = reinterpret_cast<char*>(scratch);
-  DevCtrl* dc = reinterpret_cast<DevCtrl*>(base);
-  int* counters = reinterpret_cast<int*>(base + sizeof(DevCtrl));
-  unsigned long long* stats =
-      reinterpret_cast<unsigned long long*>(base + sizeof(DevCtrl) + 4 * (kMaxActive + 2));
-  uint32_t* ready = reinterpret_cast<uint32_t*>(base + sizeof(DevCtrl) + 4 * (kMaxActive + 2) + 64);
-  cudaStream_t st = S(stream);
-  EF_CUDA_RET(cudaMemcpyAsync(dc, &h, sizeof(DevCtrl), cudaMemcpyHostToDevice, st));
-  EF_CUDA_RET(cudaMemsetAsync(counters, 0, 4 * (kMaxActive + 1), st));
-  EF_CUDA_RET(cudaMemsetAsync(stats, 0, 64, st));
-  EF_CUDA_RET(cudaMemsetAsync(ready, 0, 4 * (max_slot + 1), st));
-  EF_CUDA_RET(cudaStreamSynchronize(st));  // h is on the host stack
-  if (mode == 1)
-    return expert_ffn_stream(st, x, perm, k, reinterpret_cast<const char*>(slab), stride, dc,
-                             ready, stats, counters, max_rows, d, ff, dtype, act, y);
-  return expert_ffn_persistent(st, x, perm, k, reinterpret_cast<const char*>(slab), stride, dc,
-                               ready, stats, counters, max_rows, d, ff, dtype, act, y);
-}
-
-// Tile geometry of the streaming FFN: up tile = RU rows of W1 and W3,
-// down tile = RD rows of W2, both within one stage; WPR warps per down row.
-static bool stream_geometry(int d, int ff, int64_t es, int* RU, int* RD, int* WPR) {
-  int ru = (int)std::min<int64_t>(kSWarps, kSStageBytes / (2 * (int64_t)d * es));
-  int rd = (int)std::min<int64_t>(16, kSStageBytes / ((int64_t)ff * es));
-  if (ru < 1 || rd < 1) return false;
-  // WPR must divide kSWarps and cover rd rows with kSWarps warps
-  int wpr = kSWarps / std::min(rd, kSWarps);
-  if (rd > kSWarps) {
-    rd = kSWarps;
-    wpr = 1;
-  }
-  *RU = ru;
-  *RD = rd;
-  *WPR = wpr;
-  return 2 * ru * (int)1 <= 16 && rd * wpr <= kSWarps;
-}
-
-int expert_ffn_stream(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
-                      int64_t stride, const void* dctrl, const uint32_t* ready,
-                      unsigned long long* stats, int* counters, int max_rows, int d, int ff,
-                      int dtype, void* act, float* y) {
-  const int64_t es = dtype == EF_BF16 ? 2 : 4;
-  StreamArgs sa{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, counters, x,
-                perm, k, d, ff, 0, 0, 0, act, y};
-  EF_CHECK_ARG(stream_geometry(d, ff, es, &sa.RU, &sa.RD, &sa.WPR),
-               "expert rows do not fit the streaming FFN stage");
-  EF_CHECK_ARG(d % 256 == 0 && ff % 8 == 0, "d must be a multiple of 256 and ff of 8");
-  int rc;
-  if (dtype == EF_BF16) {
-    if (max_rows <= 1) rc = launch_stream_nt<__nv_bfloat16, 1>(st, sa);
-    else if (max_rows <= 2) rc = launch_stream_nt<__nv_bfloat16, 2>(st, sa);
-    else if (max_rows <= 4) rc = launch_stream_nt<__nv_bfloat16, 4>(st, sa);
-    else rc = launch_stream_nt<__nv_bfloat16, 8>(st, sa);
-  } else {
-    if (max_rows <= 1) rc = launch_stream_nt<float, 1>(st, sa);
-    else if (max_rows <= 2) rc = launch_stream_nt<float, 2>(st, sa);
-    else if (max_rows <= 4) rc = launch_stream_nt<float, 4>(st, sa);
-    else rc = launch_stream_nt<float, 8>(st, sa);
-  }
-  if (rc != EF_OK) return rc;
-  EF_CUDA_RET(cudaGetLastError());
-  return EF_OK;
-}
-
-int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats,
-                int* counters) {
+int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats) {
   gate_kernel<<<1, 32, 0, st>>>(reinterpret_cast<HostCtrl*>(host_ctrl_dev),
-                                reinterpret_cast<DevCtrl*>(dctrl), stats, counters);
-  EF_CUDA_RET(cudaGetLastError());
-  return EF_OK;
-}
-
-__global__ void set_ready_kernel(uint32_t* ready, int slot, uint32_t seq) {
-  *(volatile uint32_t*)(ready + slot) = seq;
-}
-
-int launch_set_ready(cudaStream_t st, uint32_t* ready, int slot, uint32_t seq) {
-  set_ready_kernel<<<1, 1, 0, st>>>(ready, slot, seq);
+                                reinterpret_cast<DevCtrl*>(dctrl), stats);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -2327,14 +1657,6 @@ static void preload_dtype(int& n) {
                        kCombSmemMax);
   cudaFuncSetAttribute(router_route_kernel<WT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kCombSmemMax);
-  preload(ffn_persist_kernel<WT, 1>, n);
-  preload(ffn_persist_kernel<WT, 2>, n);
-  preload(ffn_persist_kernel<WT, 4>, n);
-  preload(ffn_persist_kernel<WT, 8>, n);
-  preload(ffn_stream_kernel<WT, 1>, n);
-  preload(ffn_stream_kernel<WT, 2>, n);
-  preload(ffn_stream_kernel<WT, 4>, n);
-  preload(ffn_stream_kernel<WT, 8>, n);
   preload(ffn_gemv_kernel<WT, 1, kUpR, true, XGather<WT>, kUpU>, n);
   preload(ffn_gemv_kernel<WT, 1, 1, true, XGather<WT>, 4>, n);
   preload(ffn_gemv_kernel<WT, 2, kUpR, true, XGather<WT>, kUpU>, n);
@@ -2378,7 +1700,6 @@ int preload_pipeline_kernels() {
   preload(init_stats_kernel, n);
   preload(rmsnorm_kernel, n);
   preload(combine_kernel, n);
-  preload(set_ready_kernel, n);
   preload(host_io_kernel, n);
   return n;
 }

@@ -62,19 +62,9 @@ int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k,
                     int64_t stride, const void* dctrl, const uint32_t* ready,
                     unsigned long long* stats, int max_active, int max_rows, int d, int ff,
                     int dtype, void* act, float* y);
-int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats,
-                int* counters);
-int expert_ffn_persistent(cudaStream_t st, const float* x, const int32_t* perm, int k,
-                          const char* slab, int64_t stride, const void* dctrl,
-                          const uint32_t* ready, unsigned long long* stats, int* counters,
-                          int max_rows, int d, int ff, int dtype, void* act, float* y);
-int launch_set_ready(cudaStream_t st, uint32_t* ready, int slot, uint32_t seq);
+int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats);
 int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L);
 int preload_pipeline_kernels();
-int expert_ffn_stream(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
-                      int64_t stride, const void* dctrl, const uint32_t* ready,
-                      unsigned long long* stats, int* counters, int max_rows, int d, int ff,
-                      int dtype, void* act, float* y);
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
                          float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
                          int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,

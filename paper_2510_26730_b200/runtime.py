@@ -286,6 +286,25 @@ class MoEEngine:
                         lo.value | (hi.value << 64)))
         return out
 
+    def routing_x(self):
+        """[(x[B, d] fp32, mask_tokens)] per executed layer, aligned with
+        routing_log(): the router input the GPU computed for that layer and the
+        token count the bias mask's top-up rule used (0 for prefill)."""
+        n = C.c_int64()
+        R, B, lo, hi = C.c_int32(), C.c_int32(), C.c_uint64(), C.c_uint64()
+        L.check(L.lib.ef_engine_routing_log(self._h.ptr, -1, None, 0, None, 0, C.byref(R),
+                                            C.byref(B), C.byref(lo), C.byref(hi), C.byref(n)))
+        out = []
+        d = self.cfg.d_model
+        for i in range(n.value):
+            nx, mt = C.c_int64(), C.c_int32()
+            L.check(L.lib.ef_engine_routing_x(self._h.ptr, i, None, 0, C.byref(nx), C.byref(mt)))
+            x = np.empty(max(1, nx.value), dtype=np.float32)
+            L.check(L.lib.ef_engine_routing_x(self._h.ptr, i, L.as_ptr(x, C.c_float), x.size,
+                                              C.byref(nx), C.byref(mt)))
+            out.append((x[:nx.value].reshape(-1, d).copy(), mt.value))
+        return out
+
     def device_ptr(self, which: int) -> int:
         p = L.vp()
         L.check(L.lib.ef_engine_ptr(self._h.ptr, which, C.byref(p)))

@@ -30,10 +30,11 @@ def oracle_policy(p: ef.PolicyConfig) -> Policy:
 
 def run_and_check(cfg: MoEConfig, policy, *, B=2, steps=3, budget, link_bw, layer_s, seed=11,
                   bias=0.0, tol=None, check_numerics=True, token_ids=None, forest=None,
-                  table=None):
+                  table=None, timing=False):
     eng = MoEEngine(cfg, budget_experts=budget, policy=policy, link_bw=link_bw,
                     layer_time_s=layer_s, max_batch=B, seed=seed, routing_bias=bias,
-                    record_routing=True, emit_events=True, forest=forest, table=table)
+                    record_routing=True, emit_events=True, forest=forest, table=table,
+                    timing=timing)
     h_in, h_out, toks = [], [], []
     for t in range(steps):
         h = synthetic_hidden(cfg, seed, t, B, DEV)
@@ -44,7 +45,12 @@ def run_and_check(cfg: MoEConfig, policy, *, B=2, steps=3, budget, link_bw, laye
         h_out.append(h.cpu().numpy())
     torch.cuda.synchronize()
     log = eng.routing_log()
-    assert len(log) == steps * cfg.num_layers
+    xs = eng.routing_x()
+    assert len(log) == len(xs) == steps * cfg.num_layers
+    w = N.ModelWeights(L=cfg.num_layers, M=cfg.num_experts, d=cfg.d_model, ff=cfg.d_ff,
+                       dtype=cfg.dtype, seed=seed, shared_ff=cfg.shared_ff,
+                       shared_gate=cfg.shared_gate, cache=True)
+    check_router_rows(log, xs, w, cfg.num_layers)
     feats = None
     ofo = None
     if forest is not None:
@@ -55,25 +61,48 @@ def run_and_check(cfg: MoEConfig, policy, *, B=2, steps=3, budget, link_bw, laye
         def feats(tokens, step, target, hist):
             return F.features(tv, cfg.num_layers, cfg.num_experts, tokens, step, target, hist)
     st, mask_bad, sel_bad = _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, ofo,
-                                    feats)
+                                    feats, [m for _, m in xs])
     assert not mask_bad, mask_bad[:3]
     assert not sel_bad, sel_bad[:3]
     got = R.product_metrics_dict(eng.metrics(), eng.cache_events())
     want = R.oracle_metrics_dict(st)
     assert R.diff_dicts(got, want) == []
     if check_numerics:
-        w = N.ModelWeights(L=cfg.num_layers, M=cfg.num_experts, d=cfg.d_model, ff=cfg.d_ff,
-                           dtype=cfg.dtype, seed=seed, shared_ff=cfg.shared_ff,
-                           shared_gate=cfg.shared_gate)
-        tol = tol or (1e-5 if cfg.dtype == "f32" else 2e-2)
-        for t in range(steps):
-            ref = R.forward_step(h_in[t], log, t, w, cfg.num_layers, cfg.top_k, cfg.route_mode)
-            err = R.rel_err(h_out[t], ref)
-            assert err < tol, (t, err)
+        check_layer_numerics(h_in, h_out, log, xs, w, cfg, tol)
     return eng, log
 
 
-def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feats):
+# Router rows: the GPU's logits against the fp64 product of the GPU's own x_l
+# with W_r^(l+h), for the layer's row and every pre-gate row.  Both dtypes
+# accumulate in fp32 over identical inputs, so the bound is fp32 rounding.
+ROUTER_ROW_TOL = 1e-5
+
+
+def check_router_rows(log, xs, w, L):
+    errs = R.router_row_errors(log, xs, w, L)
+    assert errs, "no router rows checked"
+    worst = max(errs, key=lambda e: e[3])
+    assert worst[3] < ROUTER_ROW_TOL, ("router row mismatch (entry, h, token, rel)", worst)
+    return len(errs)
+
+
+def check_layer_numerics(h_in, h_out, log, xs, w, cfg, tol=None):
+    """Every layer's router input x_l (GPU, incl. a combine folded into the
+    router kernel) and every step output against the fp64 oracle: rel 1e-5
+    (fp32) / 2e-2 (bf16), the north star's tolerances."""
+    tol = tol or (1e-5 if cfg.dtype == "f32" else 2e-2)
+    for t in range(len(h_in)):
+        x_errs = []
+        ref = R.forward_step(h_in[t], log, t, w, cfg.num_layers, cfg.top_k, cfg.route_mode,
+                             xs=xs, x_errs=x_errs)
+        for (_s, layer, e) in x_errs:
+            assert e < tol, ("layer input x", t, layer, e)
+        err = R.rel_err(h_out[t], ref)
+        assert err < tol, (t, err)
+
+
+def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feats,
+            mask_tokens):
     from oracle.sim import OracleStepper
     traces = R.token_traces(log, cfg.num_layers, toks, bias)
     L, M = cfg.num_layers, cfg.num_experts
@@ -82,9 +111,10 @@ def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feat
 
     def pregate_fn(tt, layer, h):
         cache = holder["st"].cache
-        lg = log[cur["t"] * L + layer][0]
+        i = cur["t"] * L + layer
+        lg = log[i][0]
         mask = N.routing_mask([(layer + h, e) in cache for e in range(M)], M, cfg.top_k, budget,
-                              L, lg.shape[1]) if bias else 0
+                              L, mask_tokens[i]) if bias else 0
         return N.batch_gate(lg[h], bias, mask)
 
     st = OracleStepper(num_layers=L, experts_per_layer=cfg.num_experts, top_k=cfg.top_k,
@@ -97,9 +127,10 @@ def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feat
     mask_bad, sel_bad = [], []
 
     def hook(layer, resident):
-        logits, sel, mask = log[cur["t"] * L + layer]
+        i = cur["t"] * L + layer
+        logits, sel, mask = log[i]
         want = N.routing_mask([(layer, e) in resident for e in range(M)], M, cfg.top_k, budget, L,
-                              logits.shape[1]) if bias else 0
+                              mask_tokens[i]) if bias else 0
         if mask != want:
             mask_bad.append((cur["t"], layer))
         res = N.mask_bits(want, M)
@@ -128,13 +159,6 @@ POLICIES = [
 def test_tiny_f32_engine_parity(policy):
     run_and_check(PRESETS["tiny"], policy, B=3, steps=3, budget=16, link_bw=4 * ef.GB,
                   layer_s=0.0002)
-
-
-def test_split_ffn_kernel_pair_parity(monkeypatch):
-    """The two-launch GEMV pair (EF_FFN=split) against the same oracle."""
-    monkeypatch.setenv("EF_FFN", "split")
-    run_and_check(PRESETS["tiny"], ef.PolicyConfig("a", "adaptive", predictor="pregate"), B=3,
-                  steps=2, budget=16, link_bw=4 * ef.GB, layer_s=0.0002)
 
 
 def test_tiny_bf16_batch32_engine_parity():
@@ -243,11 +267,14 @@ def test_step_host_matches_device_step():
         e_host.step_host(torch.zeros(3, cfg.d_model))  # not pinned
 
 
-@pytest.mark.parametrize("shape", ["tiny", "qwen", "deepseek"])
-def test_prefill_then_decode_parity(shape):
+@pytest.mark.parametrize("shape,bias", [("tiny", 0.0), ("tiny", 1e4), ("qwen", 0.0),
+                                        ("qwen", 1e4), ("deepseek", 0.0)])
+def test_prefill_then_decode_parity(shape, bias):
     """Prefill (tcgen05/TMA grouped GEMM path) of T tokens as one scheduler
     step, then decode steps from the same cache: every decision bit-exact
-    with the oracle replay, every output within the bf16 tolerance."""
+    with the oracle replay (with the residency bias too: prefill masks are
+    residents-only, mask_tokens = 0), every router row within fp32 rounding
+    of x_l . W_r^T, every layer input and output within the bf16 tolerance."""
     if shape == "tiny":
         cfg, T, B, budget = PRESETS["tiny-bf16"], 96, 2, 12
     elif shape == "qwen":
@@ -261,7 +288,8 @@ def test_prefill_then_decode_parity(shape):
     pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
     link_bw, layer_s, seed = 4 * ef.GB, 2e-4, 3
     eng = MoEEngine(cfg, budget_experts=budget, policy=pol, link_bw=link_bw, layer_time_s=layer_s,
-                    max_batch=B, seed=seed, record_routing=True, emit_events=True, max_prefill=T)
+                    max_batch=B, seed=seed, record_routing=True, emit_events=True, max_prefill=T,
+                    routing_bias=bias)
     hs_in, hs_out, toks = [], [], []
     h = synthetic_hidden(cfg, seed, 0, T, DEV)
     hs_in.append(h.cpu().numpy())
@@ -277,19 +305,45 @@ def test_prefill_then_decode_parity(shape):
         hs_out.append(h.cpu().numpy())
         toks.append((1000 + t,))
     log = eng.routing_log()
-    assert len(log) == 3 * cfg.num_layers
+    xs = eng.routing_x()
+    L = cfg.num_layers
+    assert len(log) == len(xs) == 3 * L
     assert log[0][1].shape == (T, cfg.top_k)
-    st, mask_bad, sel_bad = _replay(log, cfg, budget, link_bw, layer_s, pol, toks, 0.0, None, None)
-    assert not mask_bad and not sel_bad
+    assert [m for _, m in xs] == [0] * L + [B] * (2 * L)
+    st, mask_bad, sel_bad = _replay(log, cfg, budget, link_bw, layer_s, pol, toks, bias, None, None,
+                                    [m for _, m in xs])
+    assert not mask_bad and not sel_bad, (mask_bad[:3], sel_bad[:3])
     got = R.product_metrics_dict(eng.metrics(), eng.cache_events())
     assert R.diff_dicts(got, R.oracle_metrics_dict(st)) == []
-    w = N.ModelWeights(L=cfg.num_layers, M=cfg.num_experts, d=cfg.d_model, ff=cfg.d_ff,
-                       dtype=cfg.dtype, seed=seed, shared_ff=cfg.shared_ff,
-                       shared_gate=cfg.shared_gate)
-    for t in range(3):
-        ref = R.forward_step(hs_in[t], log, t, w, cfg.num_layers, cfg.top_k, cfg.route_mode)
-        assert R.rel_err(hs_out[t], ref) < 2e-2, t
+    w = N.ModelWeights(L=L, M=cfg.num_experts, d=cfg.d_model, ff=cfg.d_ff, dtype=cfg.dtype,
+                       seed=seed, shared_ff=cfg.shared_ff, shared_gate=cfg.shared_gate, cache=True)
+    check_router_rows(log, xs, w, L)
+    check_layer_numerics(hs_in, hs_out, log, xs, w, cfg)
     assert eng.stats()["steps"] == 2
+
+
+@pytest.mark.parametrize("shape", ["mixtral", "qwen", "deepseek"])
+def test_b1_headline_path_numerics(shape):
+    """The batch-1 decode path the headline runs — router_route_row_kernel
+    (one CTA per router row, the previous layer's combine + rmsnorm folded
+    in), device-side slot resolution, the fused gate/up + down GEMVs — at the
+    real expert shapes with L = 2 and the residency-first bias of the bench:
+    every router row (incl. pre-gate rows) within fp32 rounding, every layer
+    input x_l and every step output within the bf16 tolerance, decisions
+    bit-exact."""
+    if shape == "mixtral":
+        cfg, budget = MoEConfig("mixtral-2l", 2, 8, 2, 4096, 14336), 6
+    elif shape == "qwen":
+        cfg = MoEConfig("qwen-2l", 2, 60, 4, 2048, 1408, route_mode="softmax_topk",
+                        shared_ff=5632, shared_gate=True)
+        budget = 48
+    else:
+        cfg = MoEConfig("ds-2l", 2, 64, 6, 2048, 1408, route_mode="softmax_topk", shared_ff=2816)
+        budget = 51
+    eng, _ = run_and_check(cfg, ef.PolicyConfig("a", "adaptive", predictor="pregate"), B=1,
+                           steps=3, budget=budget, link_bw=50 * ef.GB, layer_s=1e-4, seed=4,
+                           bias=1e4, timing=True)
+    assert eng.stats()["fast_layers"] > 0  # the device-resolved (headline) path ran
 
 
 @pytest.mark.parametrize("fuse,pdl", [("0", "1"), ("1", "1"), ("3", "1"), ("11", "0"), ("27", "0"),

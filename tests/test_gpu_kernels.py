@@ -108,8 +108,7 @@ def test_route_cache_aware_bias():
                                               ("bf16", 4096, 14336, [1, 1]),
                                               ("bf16", 2048, 1408, [9, 12, 1]),
                                               ("f32", 512, 768, [4, 8, 3])])
-@pytest.mark.parametrize("variant", ["pair", "persistent", "stream"])
-def test_expert_ffn_decode(dtype, d, ff, rows, variant):
+def test_expert_ffn_decode(dtype, d, ff, rows):
     E = len(rows)
     es = 2 if dtype == "bf16" else 4
     stride = 3 * d * ff * es
@@ -133,19 +132,10 @@ def test_expert_ffn_decode(dtype, d, ff, rows, variant):
     y = torch.empty(n, d, device=DEV)
     offs = np.cumsum([0] + rows[:-1]).astype(np.int32)
     a_slot, a_off, a_rows = L.i32arr(slots), L.i32arr(offs), L.i32arr(rows)
-    if variant in ("persistent", "stream"):
-        scratch = torch.empty(1 << 16, dtype=torch.uint8, device=DEV)
-        L.check(L.lib.ef_expert_ffn_ctrl_test(
-            stream(), ptr(x), ptr(perm), k, ptr(slab), stride, L.as_ptr(a_slot, C.c_int32),
-            L.as_ptr(a_off, C.c_int32), L.as_ptr(a_rows, C.c_int32), E, max(rows), d, ff,
-            1 if dtype == "bf16" else 0, ptr(act), ptr(y), ptr(scratch),
-            1 if variant == "stream" else 0))
-        torch.cuda.synchronize()
-    else:
-        L.check(L.lib.ef_expert_ffn_decode(
-            stream(), ptr(x), ptr(perm), k, ptr(slab), stride, L.as_ptr(a_slot, C.c_int32),
-            L.as_ptr(a_off, C.c_int32), L.as_ptr(a_rows, C.c_int32), E, d, ff,
-            1 if dtype == "bf16" else 0, ptr(act), ptr(y)))
+    L.check(L.lib.ef_expert_ffn_decode(
+        stream(), ptr(x), ptr(perm), k, ptr(slab), stride, L.as_ptr(a_slot, C.c_int32),
+        L.as_ptr(a_off, C.c_int32), L.as_ptr(a_rows, C.c_int32), E, d, ff,
+        1 if dtype == "bf16" else 0, ptr(act), ptr(y)))
     got = y.cpu().numpy()
     xe = N.cast(x.cpu().numpy(), dtype)
     tol = 1e-5 if dtype == "f32" else 2e-2
