@@ -324,7 +324,8 @@ int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len, int64_t* n
    gate_wait_ms (GPU time spent waiting for the host's per-layer decision),
    fast_layers (layers whose routed FFN started from the device-side slot table,
    without waiting for the host), peer_copies, peer_bytes (swap-ins served by the
-   peer-HBM tier) */
+   peer-HBM tier), prefetch_admitted / prefetch_used / prefetch_wasted (experts admitted
+   by a PREFETCH transfer; routed to by a later layer before eviction; evicted unused) */
 int ef_engine_stats(ef_engine* e, double* out, int n);
 /* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
    6 perm, 7 inv, 8 y, 9 x */
@@ -339,6 +340,14 @@ int ef_engine_peer_pool_handle(ef_engine* e, void* handle64);
 int ef_engine_routing_log(ef_engine* e, int64_t index, float* logits, int64_t max_logits,
                           int32_t* sel, int64_t max_sel, int32_t* R, int32_t* B,
                           uint64_t* mask_lo, uint64_t* mask_hi, int64_t* n_entries);
+/* routing-log recording between steps: 0 off, 1 logits + selection + router input x
+   (ef_engine_cfg.record_routing = 1 at creation), 2 logits + selection only (no device
+   copy on the step's path); entries append to the log */
+int ef_engine_set_record(ef_engine* e, int32_t mode);
+/* a fresh scheduler (policy / logical clock of `sim`, same shape) and cache-aware
+   routing bias on the same slab, weights and host store: every slot is emptied, the
+   routing log cleared; physical counters keep accumulating */
+int ef_engine_reset(ef_engine* e, const ef_sim_cfg* sim, float routing_bias);
 /* the router input x_l [B][d] fp32 of routing log entry `index`, as the GPU
    computed it (copied off the device when the layer was decided), and the token
    count the cache-aware bias mask's top-up rule used (0: prefill).  Null x

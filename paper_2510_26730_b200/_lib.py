@@ -143,6 +143,8 @@ _SIGS = {
     "ef_engine_slot_of": (C.c_int, [vp, i32, i32, P(i32)]),
     "ef_engine_routing_log": (C.c_int, [vp, i64, P(f32), i64, P(i32), i64, P(i32), P(i32), P(u64),
                                         P(u64), P(i64)]),
+    "ef_engine_set_record": (C.c_int, [vp, i32]),
+    "ef_engine_reset": (C.c_int, [vp, P(SimCfg), f32]),
     "ef_engine_routing_x": (C.c_int, [vp, i64, P(f32), i64, P(i64), P(i32)]),
 }
 

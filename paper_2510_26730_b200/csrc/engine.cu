@@ -108,7 +108,17 @@ struct ef_engine {
 
   int64_t esz = 2, stride = 0, sstride = 0;  // element size, expert / shared slot bytes
   int P = 0;                                  // physical slots
-  int Rmax = 1;
+  int Rmax = 1;   // router matrices layer 0 scores under the current policy
+  // router rows a layer can score: 1 + the policy's largest horizon
+  int rows_for_policy() const {
+    const auto& p = simcfg.policy;
+    if (p.strategy == 0) return 1;
+    if (p.strategy == 1) return std::min(2, cfg.L);
+    if (p.strategy == 2) return 1 + std::min(p.interval, cfg.L - 1);
+    const int pol_max = p.max_step >= 0 ? p.max_step : std::max(1, cfg.L - 1);
+    return 1 + std::min(pol_max, cfg.L - 1);
+  }
+  void reset(const SimConfig& sc, float bias);
   // device
   char* slab = nullptr;
   void* router_w = nullptr;  // [L][M][d]
@@ -197,6 +207,12 @@ struct ef_engine {
   // copy engine (never an SM: the FFN may be spinning on a host flag)
   float* xrec_h = nullptr;
   cudaStream_t rec_stream = nullptr;
+  void alloc_record() {
+    if (xrec_h) return;
+    CK(cudaHostAlloc(&xrec_h, sizeof(float) * std::max(cfg.max_batch, cfg.max_prefill) * cfg.d,
+                     cudaHostAllocDefault));
+    CK(cudaStreamCreateWithFlags(&rec_stream, cudaStreamNonBlocking));
+  }
   std::vector<float> record_x(const float* xd, int64_t n) {
     CK(cudaMemcpyAsync(xrec_h, xd, sizeof(float) * n, cudaMemcpyDeviceToHost, rec_stream));
     CK(cudaStreamSynchronize(rec_stream));
@@ -207,15 +223,32 @@ struct ef_engine {
           d2h_bytes = 0, ffn_bytes = 0, ffn_launches = 0;
   double stall_ms = 0, host_ms = 0, ffn_ms = 0, step_ms = 0, bubble_ms = 0;
 
+  // prefetch usefulness: experts admitted by a PREFETCH transfer and not yet
+  // routed to; `used` when a later layer routes to one, `wasted` if evicted first
+  std::vector<char> pf_pending;  // [L*M]
+  bool inflight_prefetch = false;
+  int64_t pf_admitted = 0, pf_used = 0, pf_wasted = 0;
+
   struct Mirror : Observer {
     ef_engine* e;
-    void on_transfer_start(uint64_t key, int) override { e->issue_copy(key, false); }
+    void on_transfer_start(uint64_t key, int prio) override {
+      e->issue_copy(key, false);
+      e->inflight_prefetch = prio == 1;  // Priority.PREFETCH (memory.py:169-175)
+    }
     void on_admit(uint64_t key) override {
       if (e->inflight_slot < 0) throw RuntimeErr("admit without a landed transfer");
       e->set_phys(e->idx(key), e->inflight_slot);
       e->inflight_slot = -1;
+      if (e->inflight_prefetch) {
+        e->pf_pending[e->idx(key)] = 1;
+        ++e->pf_admitted;
+      }
     }
     void on_evict(uint64_t key) override {
+      if (e->pf_pending[e->idx(key)]) {
+        e->pf_pending[e->idx(key)] = 0;
+        ++e->pf_wasted;
+      }
       int s = e->phys_of[e->idx(key)];
       e->set_phys(e->idx(key), -1);
       if (s < 0) return;
@@ -609,7 +642,10 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
                          y_d, &io));
     launches += 2;
     if (!comb_next) {  // y is in slot order after the fused FFN: no inv
-      CKS(combine_stamped(stream, h, x_d, y_d, nullptr, wts_d, cfg.shared_ff ? ys_d : nullptr,
+      // after the last layer there is no next rmsnorm: x_d keeps x_{L-1},
+      // which the host may still be reading (record_routing) on the fast path
+      CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_d : nullptr, y_d, nullptr, wts_d,
+                          cfg.shared_ff ? ys_d : nullptr,
                           sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
       ++launches;
     }
@@ -621,7 +657,7 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
                       std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
   launches += 2;
   if (comb_next) return;
-  CKS(combine_stamped(stream, h, x_d, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
+  CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_d : nullptr, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
                       sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
   ++launches;
 }
@@ -787,7 +823,9 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
         // route(l) has completed, so x_d holds x_l until layer l+1 is enqueued
         std::vector<float> lg(lg0, lg0 + (int64_t)R * B * M);
         rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(sel, sel + B * k), R, B,
-                                  cur_mask[0], cur_mask[1], record_x(x_d, (int64_t)B * cfg.d),
+                                  cur_mask[0], cur_mask[1],
+                                  cfg.record_routing == 2 ? std::vector<float>()
+                                                          : record_x(x_d, (int64_t)B * cfg.d),
                                   mask_tokens});
       }
       // the route kernel may have started FFN(l) on the slots of its table
@@ -801,6 +839,11 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
           pinned_list.push_back(s);
         }
       }
+      for (int e : r.actual)
+        if (pf_pending[(int64_t)l * M + e]) {
+          pf_pending[(int64_t)l * M + e] = 0;
+          ++pf_used;
+        }
       if (l == 0) st->begin_token(tokens, gsizes, r);
       std::fill(layer_use.begin(), layer_use.end(), -1);
       st->begin_layer(l);
@@ -1078,6 +1121,40 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
   prefill_tokens += T;
 }
 
+// A fresh scheduler (policy, logical clock) and routing bias on the same
+// slab, weights and host store: every slot is emptied, so the next step
+// starts from a cold cache exactly like a new engine (bench grids and
+// baselines reuse one engine instead of refilling a 90 GB host store).
+void ef_engine::reset(const SimConfig& sc, float bias) {
+  if (sc.L != cfg.L || sc.M != cfg.M || sc.top_k != cfg.top_k || sc.expert_size != stride)
+    throw ValueError("reset: scheduler shape differs from the engine's");
+  if (sc.policy.predictor == 3)
+    throw ValueError("the oracle predictor needs future routing; it exists only in simulate()");
+  if (compute_stream) CK(cudaStreamSynchronize(compute_stream));
+  CK(cudaStreamSynchronize(copy_stream));
+  CK(cudaDeviceSynchronize());
+  flush_stats();
+  simcfg = sc;
+  st = std::make_unique<Stepper>(simcfg, hooks.get());
+  st->set_observer(&mirror);
+  if ((int64_t)P < st->cache().capacity() + 1)
+    throw ValueError("reset: the new budget exceeds the engine's physical slots");
+  cfg.routing_bias = bias;
+  Rmax = rows_for_policy();
+  std::fill(phys_of.begin(), phys_of.end(), -1);
+  for (int64_t i = 0; i < (int64_t)cfg.L * cfg.M; ++i) host_tab[i] = make_int2(-1, 0);
+  std::fill(pf_pending.begin(), pf_pending.end(), 0);
+  std::fill(pinned.begin(), pinned.end(), 0);
+  pinned_list.clear();
+  deferred_free.clear();
+  free_slots.clear();
+  for (int s2 = 0; s2 < P; ++s2) free_slots.push_back(s2);
+  inflight_slot = -1;
+  inflight_prefetch = false;
+  std::fill(layer_use.begin(), layer_use.end(), -1);
+  rlog.clear();
+}
+
 extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
                                 const ef_ladder_cfg* ladder, ef_engine** out) {
   EF_TRY({
@@ -1109,12 +1186,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->st->set_observer(&e->mirror);
     int64_t cap = e->st->cache().capacity();
     e->P = (int)(cap + c.staging_slots);
-    int pol_max =
-        e->simcfg.policy.max_step >= 0 ? e->simcfg.policy.max_step : std::max(1, c.L - 1);
-    e->Rmax = 1 + std::min(pol_max, c.L - 1);
-    if (e->simcfg.policy.strategy == 2) e->Rmax = 1 + std::min(e->simcfg.policy.interval, c.L - 1);
-    if (e->simcfg.policy.strategy == 1) e->Rmax = std::min(2, c.L);
-    if (e->simcfg.policy.strategy == 0) e->Rmax = 1;
+    e->Rmax = e->rows_for_policy();
 
     CK(cudaSetDevice(c.device));
     const int B = c.max_batch, M = c.M, k = c.top_k, d = c.d, L = c.L;
@@ -1135,7 +1207,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       if (d % 128 || c.ff % 128 || sff % 128)
         throw ValueError("prefill needs d, ff and shared_ff multiples of 128");
       CK(cudaMalloc(&e->px_d, T * d * 4));
-      CK(cudaMalloc(&e->plogits_d, (size_t)e->Rmax * T * M * 4));
+      CK(cudaMalloc(&e->plogits_d, (size_t)L * T * M * 4));
       CK(cudaMalloc(&e->pwts_d, T * k * 4));
       CK(cudaMalloc(&e->py_d, T * k * d * 4));
       CK(cudaMalloc(&e->psel_d, T * k * 4));
@@ -1154,7 +1226,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       for (int64_t i = 0; i < T; ++i) iota[i] = (int32_t)i;
       CK(cudaMalloc(&e->piota_d, T * 4));
       CK(cudaMemcpy(e->piota_d, iota.data(), T * 4, cudaMemcpyHostToDevice));
-      CK(cudaHostAlloc(&e->plogits_h, (size_t)e->Rmax * T * M * 4, cudaHostAllocDefault));
+      CK(cudaHostAlloc(&e->plogits_h, (size_t)L * T * M * 4, cudaHostAllocDefault));
       CK(cudaHostAlloc(&e->psel_h, T * k * 4, cudaHostAllocDefault));
       const int64_t widest = std::max<int64_t>({(int64_t)c.ff, (int64_t)d, sff});
       e->ptiles_cap = ((T * k + 127) / 128 + M + 1) * ((widest + 127) / 128);
@@ -1163,7 +1235,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       CK(cudaMalloc(&e->ptiles_d, sizeof(int4) * 4 * e->ptiles_cap));
       CK(cudaEventCreateWithFlags(&e->copy_mark, cudaEventDisableTiming));
     }
-    CK(cudaMalloc(&e->logits_d, (size_t)e->Rmax * B * M * 4));
+    CK(cudaMalloc(&e->logits_d, (size_t)L * B * M * 4));
     CK(cudaMalloc(&e->sgl_d, (size_t)B * 4));
     CK(cudaMalloc(&e->wts_d, (size_t)B * k * 4));
     CK(cudaMalloc(&e->sel_d, (size_t)B * k * 4));
@@ -1183,7 +1255,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     std::memset((void*)e->hctrl, 0, sizeof(HostCtrl) * L);
     CK(cudaHostGetDevicePointer((void**)&e->hctrl_dev, e->hctrl, 0));
     e->out_stride =
-        ((int64_t)sizeof(HostOut) + (int64_t)B * k * 4 + (int64_t)e->Rmax * B * M * 4 + 127) / 128 *
+        ((int64_t)sizeof(HostOut) + (int64_t)B * k * 4 + (int64_t)L * B * M * 4 + 127) / 128 *
         128;
     CK(cudaHostAlloc(&e->hout, e->out_stride * L, cudaHostAllocMapped));
     std::memset(e->hout, 0, e->out_stride * L);
@@ -1222,14 +1294,11 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       CK(cudaEventCreateWithFlags(&e->join_in, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&e->join_out, cudaEventDisableTiming));
     }
-    if (c.record_routing) {
-      CK(cudaHostAlloc(&e->xrec_h, sizeof(float) * std::max(B, c.max_prefill) * d,
-                       cudaHostAllocDefault));
-      CK(cudaStreamCreateWithFlags(&e->rec_stream, cudaStreamNonBlocking));
-    }
+    if (c.record_routing) e->alloc_record();
     e->slot_seq.assign(e->P, 0);
     e->pinned.assign(e->P, 0);
     e->phys_of.assign((size_t)L * M, -1);
+    e->pf_pending.assign((size_t)L * M, 0);
     e->layer_R.assign(L, 1);
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
@@ -1318,7 +1387,7 @@ extern "C" int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len,
 extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   EF_TRY({
     e->flush_stats();
-    double v[19] = {(double)e->steps,         (double)e->copies,
+    double v[22] = {(double)e->steps,         (double)e->copies,
                     (double)e->copy_bytes,    e->stall_ms,
                     (double)e->P,             (double)e->st->cache().capacity(),
                     (double)e->cfg.staging_slots, (double)e->launches,
@@ -1327,8 +1396,9 @@ extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
                     (double)e->d2h_bytes,     (double)e->ffn_bytes,
                     (double)e->ffn_launches,  e->bubble_ms,
                     (double)e->fast_layers,   (double)e->peer_copies,
-                    (double)e->peer_bytes};
-    for (int i = 0; i < n && i < 19; ++i) out[i] = v[i];
+                    (double)e->peer_bytes,    (double)e->pf_admitted,
+                    (double)e->pf_used,       (double)e->pf_wasted};
+    for (int i = 0; i < n && i < 22; ++i) out[i] = v[i];
   });
 }
 
@@ -1370,6 +1440,18 @@ extern "C" int ef_engine_routing_log(ef_engine* e, int64_t index, float* logits,
     if (sel)
       std::memcpy(sel, r.sel.data(),
                   sizeof(int32_t) * std::min<int64_t>(max_sel, (int64_t)r.sel.size()));
+  });
+}
+
+extern "C" int ef_engine_reset(ef_engine* e, const ef_sim_cfg* sim, float routing_bias) {
+  EF_TRY({ e->reset(sim_config_from(sim), routing_bias); });
+}
+
+extern "C" int ef_engine_set_record(ef_engine* e, int32_t on) {
+  EF_TRY({
+    if (on < 0 || on > 2) throw ValueError("record mode must be 0, 1 or 2");
+    if (on == 1) e->alloc_record();
+    e->cfg.record_routing = on;
   });
 }
 

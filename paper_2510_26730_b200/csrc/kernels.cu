@@ -234,7 +234,8 @@ __device__ float combine_row(int t, const float* h, float* vout, const float* __
   return block_sum(ss, red);
 }
 
-// h[t] += sum_r wts[t,r] * y[inv[t,r]] (rank order) + g_t * ys[t]; x[t] = rmsnorm(h[t]).
+// h[t] += sum_r wts[t,r] * y[inv[t,r]] (rank order) + g_t * ys[t]; x[t] = rmsnorm(h[t])
+// (x null: h only).
 __device__ void combine_token(int t, float* __restrict__ h, float* __restrict__ x,
                               const float* __restrict__ y, const int32_t* __restrict__ inv,
                               const float* __restrict__ wts, const float* __restrict__ ys,
@@ -242,6 +243,7 @@ __device__ void combine_token(int t, float* __restrict__ h, float* __restrict__ 
                               float* red) {
   float* hr = h + (int64_t)t * d;
   const float ss = combine_row(t, h, hr, y, inv, wts, ys, gate_logit, d, k, red);
+  if (!x) return;  // after the last layer: no next rmsnorm
   const float invn = 1.0f / sqrtf(ss / (float)d + eps);
   for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
     float4 v = *reinterpret_cast<const float4*>(hr + i);

@@ -11,13 +11,13 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-from dataclasses import dataclass, replace
 from typing import List, Optional, Sequence
 
 import numpy as np
 import torch
 
 from . import _lib as L
+from .configs import PRESETS, MoEConfig  # noqa: F401  (re-exported)
 from .core import HardwareSpec, ModelSpec, Seed, seconds_to_ns
 from .engine import PolicyConfig, SimMetrics, collect_metrics
 from .predictor import ForestModel
@@ -26,51 +26,6 @@ from .workload import EmbeddingTable
 
 DTYPES = {"f32": 0, "bf16": 1}
 ROUTE_MODES = {"mixtral": 0, "softmax_topk": 1}
-
-
-@dataclass(frozen=True)
-class MoEConfig:
-    """MoE layer-stack shape (public HF configs)."""
-    name: str
-    num_layers: int
-    num_experts: int
-    top_k: int
-    d_model: int
-    d_ff: int
-    dtype: str = "bf16"
-    route_mode: str = "mixtral"
-    shared_ff: int = 0
-    shared_gate: bool = False
-    embed_dim: int = 8
-    vocab_size: int = 32000
-
-    @property
-    def elem_bytes(self) -> int:
-        return 2 if self.dtype == "bf16" else 4
-
-    @property
-    def expert_bytes(self) -> int:
-        return 3 * self.d_model * self.d_ff * self.elem_bytes
-
-    @property
-    def total_experts(self) -> int:
-        return self.num_layers * self.num_experts
-
-    def model_spec(self) -> ModelSpec:
-        return ModelSpec(self.num_layers, self.num_experts, self.top_k, self.expert_bytes,
-                         self.embed_dim, self.vocab_size)
-
-
-PRESETS = {
-    "tiny": MoEConfig("tiny", 4, 8, 2, 256, 1024, dtype="f32"),
-    "tiny-bf16": MoEConfig("tiny-bf16", 4, 8, 2, 256, 1024, dtype="bf16"),
-    "mixtral-8x7b": MoEConfig("mixtral-8x7b", 32, 8, 2, 4096, 14336),
-    "qwen1.5-moe-a2.7b": MoEConfig("qwen1.5-moe-a2.7b", 24, 60, 4, 2048, 1408,
-                                   route_mode="softmax_topk", shared_ff=5632, shared_gate=True),
-    "deepseek-v2-lite": MoEConfig("deepseek-v2-lite", 26, 64, 6, 2048, 1408,
-                                  route_mode="softmax_topk", shared_ff=2816),
-    "mixtral-8x22b": MoEConfig("mixtral-8x22b", 56, 8, 2, 6144, 16384),
-}
 
 
 class MoEEngine:
@@ -162,6 +117,27 @@ class MoEEngine:
                                        C.byref(h)))
         self._h = L.Handle(h.value, L.lib.ef_engine_destroy)
         self._ec = ec
+        self._seed = seed
+        self._sim = sim
+
+    def reset(self, policy: PolicyConfig, routing_bias: float = 0.0) -> None:
+        """Start over with a fresh scheduler (``policy``) and routing bias on
+        the same slab, weights and pinned host store: the cache is emptied as
+        in a new engine, the routing log cleared; ``stats()`` counters keep
+        accumulating.  The prediction ladder's threshold and forest stay."""
+        model = self.cfg.model_spec()
+        policy.check(model)
+        if policy.predictor == "oracle":
+            raise ValueError("the oracle predictor needs future routing; use simulate()")
+        if policy.cum_threshold != self.policy.cum_threshold or \
+                (policy.predictor == "forest") != (self.policy.predictor == "forest"):
+            raise ValueError("reset keeps the engine's prediction ladder: same cum_threshold "
+                             "and forest use required")
+        sim = policy.to_c(model, self.hw, Seed(self._seed), self.emit_events)
+        L._pending_exc.clear()
+        L.check(L.lib.ef_engine_reset(self._h.ptr, C.byref(sim), float(routing_bias)))
+        self._sim = sim
+        self.policy = policy
 
     # ------------------------------------------------------------------ API
     def step(self, h: torch.Tensor, token_ids: Optional[Sequence[int]] = None) -> torch.Tensor:
@@ -258,7 +234,8 @@ class MoEEngine:
         keys = ["steps", "copies", "copy_bytes", "stall_ms", "phys_slots", "logical_capacity",
                 "staging_slots", "kernel_launches", "host_decision_ms", "ffn_ms", "step_ms",
                 "preload_copies", "d2h_bytes", "ffn_bytes", "ffn_launches", "gate_wait_ms",
-                "fast_layers", "peer_copies", "peer_bytes"]
+                "fast_layers", "peer_copies", "peer_bytes", "prefetch_admitted", "prefetch_used",
+                "prefetch_wasted"]
         out = (C.c_double * len(keys))()
         L.check(L.lib.ef_engine_stats(self._h.ptr, out, len(keys)))
         return dict(zip(keys, list(out)))
@@ -285,6 +262,11 @@ class MoEEngine:
             out.append((lg[:r * b * M].reshape(r, b, M).copy(), sel[:b * k].reshape(b, k).copy(),
                         lo.value | (hi.value << 64)))
         return out
+
+    def set_record_routing(self, mode) -> None:
+        """Routing-log recording: False/0 off, True/1 logits + selection +
+        router input x (routing_x), 2 logits + selection only."""
+        L.check(L.lib.ef_engine_set_record(self._h.ptr, int(mode)))
 
     def routing_x(self):
         """[(x[B, d] fp32, mask_tokens)] per executed layer, aligned with

@@ -520,3 +520,29 @@ def test_peer_pool_ipc_across_processes(monkeypatch):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ipc ok" in r.stdout, r.stdout + r.stderr
     owner.close()
+
+
+def test_reset_equals_fresh_engine():
+    """MoEEngine.reset(policy, bias) — the bench's grid / baselines reuse one
+    engine — behaves exactly like a new engine: same outputs, cache event
+    trace and scheduler metrics on the same inputs."""
+    cfg = PRESETS["tiny-bf16"]
+    kw = dict(budget_experts=12, link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2, seed=6,
+              emit_events=True)
+    a = MoEEngine(cfg, policy=ef.PolicyConfig("r", "reactive"), routing_bias=0.0, **kw)
+    for t in range(3):
+        a.step(synthetic_hidden(cfg, 6, 50 + t, 2, DEV))
+    pol = ef.PolicyConfig("a", "adaptive", predictor="pregate")
+    a.reset(pol, 1e4)
+    b = MoEEngine(cfg, policy=pol, routing_bias=1e4, **kw)
+    for t in range(5):
+        h1 = synthetic_hidden(cfg, 6, t, 2, DEV)
+        h2 = h1.clone()
+        a.step(h1)
+        b.step(h2)
+        torch.cuda.synchronize()
+        assert torch.equal(h1, h2), t
+    assert a.cache_events() == b.cache_events()
+    assert a.metrics() == b.metrics()
+    with pytest.raises(ValueError):
+        a.reset(ef.PolicyConfig("a", "adaptive", predictor="pregate", cum_threshold=0.5))
