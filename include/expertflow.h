@@ -263,6 +263,55 @@ int ef_grouped_gemm_bf16(void* stream, const void* A, int64_t a_rows, int K, con
                          int dual_off, void* out, int out_ld);
 
 /* ------------------------------------------------------------------ */
+/* Expert parallelism: collectives of the EP decode step */
+/* ------------------------------------------------------------------ */
+#define EF_COLL_ALLGATHER 0 /* recv[g*bytes..] = rank g's send[0..bytes) */
+#define EF_COLL_ALLTOALL 1  /* recv[g*bytes..] = rank g's send[me*bytes..) */
+/* host transport of the EP collectives (device buffers, ordered on `stream`;
+   return 0 on success).  The NCCL transport is built in; a callback lets G
+   processes share one GPU in tests (NCCL refuses two ranks on one device). */
+typedef int (*ef_collective_cb)(void* user, int op, void* dev_send, void* dev_recv,
+                                int64_t bytes, void* stream);
+/* 128-byte NCCL unique id for an EP group (rank 0 creates, all pass it) */
+int ef_ep_nccl_unique_id(void* out128);
+typedef struct ef_ep_comm ef_ep_comm;
+/* an EP group handle: nccl_id128 non-null -> NCCL; else cb (world 1: local copies) */
+int ef_ep_comm_create(int world, int rank, const void* nccl_id128, ef_collective_cb cb,
+                      void* user, ef_ep_comm** out);
+void ef_ep_comm_destroy(ef_ep_comm* c);
+/* dispatch (replaces the reference's single-process routing hand-off,
+   engine.py:573-581, for G ranks): pack this rank's routing block
+   [x B*d f32 | logits Rm*B*M f32 | sel B*k i32 | wts B*k f32] into `send`
+   (block_words 4-byte words, >= the block) and all-gather every rank's block
+   into recv[G][block_words]. */
+int ef_ep_dispatch(ef_ep_comm* c, void* stream, const float* x, const float* logits,
+                   const int32_t* sel, const float* wts, int B, int d, int Rm, int M, int k,
+                   int64_t block_words, float* send, float* recv);
+/* owner side: the (token, rank) slots of all G*B tokens routed to the Ms experts
+   [e0, e0+Ms) this rank owns, stable by (local expert, global slot) -> counts[Ms],
+   offsets[Ms+1], perm[<= G*B*k]; home_idx[B*k] = row of each local slot in the
+   all-to-all output (owner*B*k + t*k + r) */
+int ef_ep_owner(void* stream, const float* recv, int64_t block_words, int G, int B, int k, int M,
+                int d, int Rm, int rank, int e0, int Ms, int32_t* counts, int32_t* offsets,
+                int32_t* perm, int32_t* home_idx);
+/* combine: all-to-all of y rows in global slot order (y_slots [G*B*k][d] f32,
+   chunk g = rank g's slots) into y_recv, then the rank-order weighted combine
+   h[t] += sum_r wts[t,r]*y_recv[home_idx[t*k+r]] (+ g_t*ys[t]); x = rmsnorm(h)
+   (x nullable).  Same arithmetic and order as ef_combine. */
+int ef_ep_combine(ef_ep_comm* c, void* stream, const float* y_slots, float* y_recv,
+                  const int32_t* home_idx, const float* wts, const float* ys,
+                  const float* shared_gate_logit, int B, int d, int k, float* h, float* x);
+
+/* the shard's scheduler view of one layer's global routing (logits [GB][M] of all
+   G ranks' tokens, sel [GB][k]): gate[Ms] = the fp64 batch gate (bias 0, sequential
+   sums) restricted to the owned experts and renormalised; groups[GB][k] = each
+   token's owned experts as local ids ascending (-1 padded); actual[Ms] = their
+   ascending union (-1 padded, *n_actual entries).  The routing contract of
+   workload.py:161-179 per shard. */
+int ef_ep_shard_view(const float* logits, const int32_t* sel, int GB, int M, int k, int G,
+                     int rank, double* gate, int32_t* groups, int32_t* actual, int32_t* n_actual);
+
+/* ------------------------------------------------------------------ */
 /* MoE decode engine: slab + pinned host store + copy streams + stepper */
 /* ------------------------------------------------------------------ */
 typedef struct ef_engine ef_engine;
@@ -296,6 +345,19 @@ typedef struct ef_engine_cfg {
                                   process (one process per GPU) created and filled on
                                   peer_device (ef_engine_peer_pool_handle); opened, not
                                   allocated or filled */
+  /* Expert parallelism: ep_world > 0 makes this engine rank
+     ep_rank of an ep_world-rank group.  It owns experts [ep_rank*M/G, +M/G) of every
+     layer (G | M): its slab, pinned host store and scheduler (ef_sim_cfg with
+     M/G experts, top_k min(k, M/G), the shard's budget) cover only those; every step
+     routes its own B tokens, all-gathers the routing blocks, runs its experts for all
+     G*B tokens and all-to-alls the outputs back (ep_step).  Transport: ep_nccl_id
+     (NCCL), else ep_collective (callback), else (world 1) local copies.  Decode only,
+     routing_bias must be 0. */
+  int32_t ep_world;
+  int32_t ep_rank;
+  const void* ep_nccl_id;
+  ef_collective_cb ep_collective;
+  void* ep_user;
 } ef_engine_cfg;
 int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim, const ef_ladder_cfg* ladder,
                      ef_engine** out);

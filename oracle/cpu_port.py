@@ -161,11 +161,11 @@ class CpuDecodePort:
         return N.cast(x, self.dtype)
 
     # ------------------------------------------------------------ routing
-    def _mask(self, layer, ntok):
+    def _mask(self, layer, logits):
         if not self.bias:
             return 0
         res = [(layer, e) in self.st.cache for e in range(self.M)]
-        return N.routing_mask(res, self.M, self.k, self.budget, self.L, ntok)
+        return N.routing_mask(res, self.M, self.k, self.budget, self.L, logits.shape[0], logits)
 
     def _pregate(self, tt, layer, h):
         t0 = time.perf_counter()
@@ -175,7 +175,7 @@ class CpuDecodePort:
             lg = gemv(self.router[layer + h], self.M, self.d, self._x[layer])
             self._pg[key] = lg
         self._pg_s += time.perf_counter() - t0
-        return N.batch_gate(lg, self.bias, self._mask(layer + h, lg.shape[0]))
+        return N.batch_gate(lg, self.bias, self._mask(layer + h, lg))
 
     # ------------------------------------------------------------ one step
     def step(self, h: np.ndarray, token_ids: Optional[Sequence[int]] = None) -> np.ndarray:
@@ -198,7 +198,7 @@ class CpuDecodePort:
             self._x[layer] = x
             lg = gemv(self.router[layer], M, self.d, x)
             self._pg[(layer, 0)] = lg
-            mask = self._mask(layer, B)
+            mask = self._mask(layer, lg)
             sel = N.topk_select(lg, k, self.bias, N.mask_bits(mask, M) if self.bias else None)
             w = N.route_weights(lg, sel, self.mode).astype(np.float32)
             xe = self._x_in_dtype(x)

@@ -134,29 +134,38 @@ def router_logits(x: np.ndarray, wr: np.ndarray) -> np.ndarray:
     return np.asarray(x, np.float64) @ np.asarray(wr, np.float64).T
 
 
-def routing_mask(resident, M: int, k: int, budget_experts: int, L: int, ntok: int) -> int:
+def routing_mask(resident, M: int, k: int, budget_experts: int, L: int, ntok: int,
+                 logits: Optional[np.ndarray] = None) -> int:
     """Experts that get the cache-aware routing bias in one layer (engine.cu
-    ``residency_mask``): the layer's residents; when the batch could touch more
-    than the layer's share of the cache (ntok*k > U, U = max(k, budget // L))
-    and fewer than k experts are resident, topped up with the lowest-index
-    non-resident experts to U, so every token picks inside a set of at most U
-    experts and the per-layer unions fit the cache together (no cyclic-LRU
-    thrash at large batch).  Decode steps only: the engine's prefill passes
-    ntok = 0 (residents only).  No reference counterpart (routing bias is ours)."""
+    ``residency_mask`` + kernels.cu ``topup_mask``): the layer's residents;
+    when the batch could touch more than the layer's share of the cache
+    (ntok*k > U, U = max(k, budget // L)) and fewer than k experts are
+    resident, topped up to U experts by router votes over the layer's fp32
+    ``logits`` [B, M]: the non-resident experts in the most tokens' UNBIASED
+    top-k (value desc, index asc), then the largest logit over the batch,
+    then the lower index — the set that changes the fewest tokens'
+    selections.  Decode steps only: the engine's prefill passes ntok = 0
+    (residents only).  No reference counterpart (the reference's cache-aware
+    routing only reorders groups, engine.py:192-209)."""
     mask = 0
     n = 0
     for e in range(M):
         if resident[e]:
             mask |= 1 << e
             n += 1
-    U = max(k, budget_experts // L)
+    U = min(max(k, budget_experts // L), M)
     if ntok * k > U and n < k:
-        for e in range(M):
-            if n >= U:
-                break
-            if not (mask >> e) & 1:
-                mask |= 1 << e
-                n += 1
+        if logits is None:
+            raise ValueError("the top-up needs the layer's router logits")
+        lg = np.asarray(logits, dtype=np.float32)
+        votes = np.zeros(M, dtype=np.int64)
+        for row in topk_select(lg, k):
+            votes[row] += 1
+        mx = lg.max(axis=0)
+        order = sorted((e for e in range(M) if not (mask >> e) & 1),
+                       key=lambda e: (-int(votes[e]), -float(mx[e]), e))
+        for e in order[:max(0, U - n)]:
+            mask |= 1 << e
     return mask
 
 

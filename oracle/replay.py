@@ -52,7 +52,7 @@ def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, pol
         logits = log[i][0]
         cache = holder["st"].cache
         mask = N.routing_mask([(layer + h, e) in cache for e in range(M)], M, k, budget_experts,
-                              L, ntok(i)) if bias else 0
+                              L, ntok(i), logits[h]) if bias else 0
         return N.batch_gate(logits[h], bias, mask)
 
     st = OracleStepper(num_layers=L, experts_per_layer=M, top_k=k, expert_size_bytes=expert_bytes,
@@ -66,7 +66,7 @@ def replay(log, *, L, M, k, expert_bytes, link_bw, budget_experts, layer_ns, pol
         i = cur["t"] * L + layer
         logits, sel, mask = log[i]
         want = N.routing_mask([(layer, e) in resident for e in range(M)], M, k, budget_experts,
-                              L, ntok(i)) if bias else 0
+                              L, ntok(i), logits[0]) if bias else 0
         if mask != want:
             mask_bad.append((cur["t"], layer, mask, want))
         ref = N.topk_select(logits[0], k, bias, N.mask_bits(want, M) if bias else None)

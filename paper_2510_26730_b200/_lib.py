@@ -37,6 +37,7 @@ class StepStateC(C.Structure):
 
 
 PREGATE_CB = C.CFUNCTYPE(C.c_int, vp, i32, i32, P(f64))
+COLLECTIVE_CB = C.CFUNCTYPE(C.c_int, vp, C.c_int, vp, vp, i64, vp)
 FOREST_CB = C.CFUNCTYPE(C.c_int, vp, P(f64), i32, P(f64), P(f64))
 
 
@@ -64,7 +65,9 @@ class EngineCfg(C.Structure):
                 ("routing_bias", f32), ("seed", u64), ("device", i32), ("timing", i32),
                 ("record_routing", i32), ("max_prefill", i32), ("host_store_shm", C.c_char_p),
                 ("host_store_attach", i32), ("peer_device", i32), ("peer_pool_experts", i64),
-                ("peer_pool_ids", P(i32)), ("peer_ipc_handle", vp)]
+                ("peer_pool_ids", P(i32)), ("peer_ipc_handle", vp),
+                ("ep_world", i32), ("ep_rank", i32), ("ep_nccl_id", vp),
+                ("ep_collective", COLLECTIVE_CB), ("ep_user", vp)]
 
 
 _SIGS = {
@@ -144,6 +147,17 @@ _SIGS = {
     "ef_engine_routing_log": (C.c_int, [vp, i64, P(f32), i64, P(i32), i64, P(i32), P(i32), P(u64),
                                         P(u64), P(i64)]),
     "ef_engine_set_record": (C.c_int, [vp, i32]),
+    "ef_ep_nccl_unique_id": (C.c_int, [vp]),
+    "ef_ep_shard_view": (C.c_int, [P(f32), P(i32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   P(f64), P(i32), P(i32), P(i32)]),
+    "ef_ep_comm_create": (C.c_int, [C.c_int, C.c_int, vp, COLLECTIVE_CB, vp, P(vp)]),
+    "ef_ep_comm_destroy": (None, [vp]),
+    "ef_ep_dispatch": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                 C.c_int, i64, vp, vp]),
+    "ef_ep_owner": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                              C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),
+    "ef_ep_combine": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp,
+                                vp]),
     "ef_engine_reset": (C.c_int, [vp, P(SimCfg), f32]),
     "ef_engine_routing_x": (C.c_int, [vp, i64, P(f32), i64, P(i64), P(i32)]),
 }

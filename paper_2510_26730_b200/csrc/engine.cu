@@ -53,6 +53,7 @@
 #include "capi_util.h"
 #include "pipeline.h"
 #include "simcore.h"
+#include "transport.h"
 
 using namespace ef;
 
@@ -100,6 +101,40 @@ static void batch_gate(const float* logits, int B, int M, float bias, const uint
   for (int e = 0; e < M; ++e) out[e] = mixed[e] / s;
 }
 
+// Expert-parallel shard view of one layer's global routing:
+// the fp64 batch gate of all GB tokens (bias 0) restricted to the owned
+// experts [e0, e0+Ms) and renormalised by a sequential sum; one group per
+// global token holding its owned experts (local ids, ascending); the
+// ascending union.  oracle/ep_shard.py restates it.
+static void ep_shard_view(const float* lg, const int32_t* sel, int GB, int M, int k, int e0,
+                          int Ms, double* gate, std::vector<std::vector<int>>* groups,
+                          std::vector<int>* actual, std::vector<int>* cnt) {
+  std::vector<double> full(M);
+  const uint64_t none[2] = {0, 0};
+  batch_gate(lg, GB, M, 0.f, none, full.data());
+  double s = 0.0;
+  for (int j = 0; j < Ms; ++j) s += full[e0 + j];
+  for (int j = 0; j < Ms; ++j) gate[j] = full[e0 + j] / s;
+  if (!sel) return;
+  cnt->assign(Ms, 0);
+  groups->assign(GB, {});
+  for (int t = 0; t < GB; ++t) {
+    auto& g = (*groups)[t];
+    for (int j = 0; j < k; ++j) {
+      const int e = sel[t * k + j];
+      if (e < 0 || e >= M) throw RuntimeErr("route kernel produced an invalid expert id");
+      if (e >= e0 && e < e0 + Ms) {
+        g.push_back(e - e0);
+        (*cnt)[e - e0]++;
+      }
+    }
+    std::sort(g.begin(), g.end());
+  }
+  actual->clear();
+  for (int j = 0; j < Ms; ++j)
+    if ((*cnt)[j]) actual->push_back(j);
+}
+
 struct ef_engine {
   ef_engine_cfg cfg{};
   SimConfig simcfg;
@@ -119,6 +154,23 @@ struct ef_engine {
     return 1 + std::min(pol_max, cfg.L - 1);
   }
   void reset(const SimConfig& sc, float bias);
+  // ---- expert parallelism (ef_engine_cfg.ep_world > 0; kernels.cu
+  // "expert parallelism"): rank ep_rank of G owns experts [e0, e0 + Ms)
+  bool ep = false;
+  int G = 1, ep_rank = 0, Ms = 0, e0 = 0;
+  std::unique_ptr<Transport> xport;
+  int64_t ep_W = 0;  // routing block, 4-byte words (16-byte multiple)
+  float *ep_send = nullptr, *ep_recv = nullptr, *ep_yslots = nullptr, *ep_yrecv = nullptr;
+  int32_t *ep_counts = nullptr, *ep_offsets = nullptr, *ep_perm = nullptr, *ep_home = nullptr;
+  void* ep_act = nullptr;
+  char* ep_hout = nullptr;  // mapped: done word, then sel [G*B*k] i32, logits [L][G*B][M] f32
+  char* ep_hout_dev = nullptr;
+  int64_t ep_steps = 0, ep_collectives = 0, ep_bytes = 0;
+  void ep_alloc();
+  void ep_step_on(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
+  void shard_gate(const float* lg, int GB, double* out) const {
+    ep_shard_view(lg, nullptr, GB, cfg.M, cfg.top_k, e0, Ms, out, nullptr, nullptr, nullptr);
+  }
   // device
   char* slab = nullptr;
   void* router_w = nullptr;  // [L][M][d]
@@ -149,6 +201,8 @@ struct ef_engine {
   int stats_buf = 0, stats_pending = -1;
   int64_t stats_copies[2] = {0, 0}, copies_at_step = 0;
   void fold_stats(int i);
+  void timing_begin(cudaStream_t stream);
+  void timing_end(cudaStream_t stream);
   std::string dump_text;  // EF_STATS_DUMP timeline, printed on flush (not mid-step)
   void flush_stats() {
     if (stats_pending >= 0) fold_stats(stats_pending);
@@ -271,7 +325,10 @@ struct ef_engine {
     }
   } mirror;
 
-  int64_t idx(uint64_t key) const { return (int64_t)eid_layer(key) * cfg.M + eid_expert(key); }
+  // experts per layer in the scheduler's (and slab's) space: M, or M/G under
+  // expert parallelism (local ids of the owned experts)
+  int sM() const { return simcfg.M; }
+  int64_t idx(uint64_t key) const { return (int64_t)eid_layer(key) * sM() + eid_expert(key); }
   HostOut* out(int l) { return reinterpret_cast<HostOut*>(hout + (int64_t)l * out_stride); }
   int32_t* out_sel(int l) {
     return reinterpret_cast<int32_t*>(hout + (int64_t)l * out_stride + sizeof(HostOut));
@@ -327,13 +384,15 @@ struct ef_engine {
   // Experts that get the cache-aware routing bias in `layer` (oracle/numerics.py
   // routing_mask): its residents; when the batch could touch more than the
   // layer's share of the cache (tokens*k > U, U = max(k, capacity / L)) and
-  // fewer than k are resident, topped up with the lowest-index non-resident
-  // experts to U, so each layer's union stays within its share and the unions
-  // fit the cache together (without it, B=32 Qwen thrashes the global LRU).
-  int mask_tokens = 1;  // tokens of the current step / prefill
-  void residency_mask(int layer, uint64_t* m) const {
+  // fewer than k are resident, the mask is topped up to U experts by router
+  // votes (kernels.cu topup_mask: the experts most tokens' unbiased top-k
+  // picks), so each layer's union stays within its share and the unions fit
+  // the cache together (without it, B=32 Qwen thrashes the global LRU).
+  // Returns U when the route kernel must top up, else 0.
+  int mask_tokens = 1;  // tokens of the current step (0: prefill, residents only)
+  int residency_mask(int layer, uint64_t* m) const {
     m[0] = m[1] = 0;
-    if (cfg.routing_bias == 0.f || layer >= cfg.L) return;
+    if (cfg.routing_bias == 0.f || layer >= cfg.L) return 0;
     int n = 0;
     for (int e = 0; e < cfg.M; ++e)
       if (st->resident(layer, e)) {
@@ -341,14 +400,42 @@ struct ef_engine {
         ++n;
       }
     const int64_t U = std::max<int64_t>(cfg.top_k, st->cache().capacity() / cfg.L);
-    if ((int64_t)mask_tokens * cfg.top_k > U && n < cfg.top_k)
-      for (int e = 0; e < cfg.M && n < U; ++e)
-        if (!((m[e >> 6] >> (e & 63)) & 1ull)) {
-          m[e >> 6] |= 1ull << (e & 63);
-          ++n;
-        }
+    if ((int64_t)mask_tokens * cfg.top_k > U && n < cfg.top_k) return (int)std::min<int64_t>(U, cfg.M);
+    return 0;
+  }
+  // The same top-up on the host from B rows of fp32 logits (pre-gate rows:
+  // layer l+h's router applied to x_l) — the rule of kernels.cu topup_mask.
+  void scored_mask(int layer, const float* lg, int B, uint64_t* m) const {
+    const int U = residency_mask(layer, m);
+    if (U <= 0) return;
+    const int M = cfg.M, k = cfg.top_k;
+    std::vector<int> votes(M, 0), idx(M);
+    std::vector<float> mx(M, -INFINITY);
+    for (int t = 0; t < B; ++t) {
+      const float* r = lg + (int64_t)t * M;
+      for (int e = 0; e < M; ++e) {
+        idx[e] = e;
+        if (r[e] > mx[e]) mx[e] = r[e];
+      }
+      std::partial_sort(idx.begin(), idx.begin() + k, idx.end(), [&](int a, int b) {
+        return r[a] > r[b] || (r[a] == r[b] && a < b);
+      });
+      for (int j = 0; j < k; ++j) votes[idx[j]]++;
+    }
+    int n = __builtin_popcountll(m[0]) + __builtin_popcountll(m[1]);
+    for (; n < U; ++n) {
+      int be = -1;
+      for (int e = 0; e < M; ++e) {
+        if ((m[e >> 6] >> (e & 63)) & 1ull) continue;
+        if (be < 0 || votes[e] > votes[be] || (votes[e] == votes[be] && mx[e] > mx[be])) be = e;
+      }
+      if (be < 0) break;
+      m[be >> 6] |= 1ull << (be & 63);
+    }
   }
 
+  int cur_topup = 0;  // top-up target of the layer being enqueued (residency_mask)
+  uint64_t* fmask_d = nullptr;  // [L][2] final bias mask of each layer (route kernel)
   void enqueue_layer(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask);
   void enqueue_front(cudaStream_t stream, int l, int B, int R, const uint64_t* mask);
   std::vector<int> layer_R;  // router matrices scored at each layer this step
@@ -448,14 +535,17 @@ void ef_engine::init_weights() {
   }
   int64_t nff = (int64_t)ff * d;
   int it = 0;
+  // the store holds the scheduler's experts: all M, or the owned M/G under
+  // expert parallelism (weights keyed by the global expert id e0 + e)
   for (int l = 0; l < L; ++l) {
-    for (int e = 0; e < M; ++e, ++it) {
+    for (int e = 0; e < sM(); ++e, ++it) {
       char* sb = stage[it & 1];
+      const int ge = e0 + e;
       if (it >= 2) CK(cudaEventSynchronize(done[it & 1]));
-      CKS(ef_fill_uniform(s, sb, dt, nff, ef_stream_key(cfg.seed, l, e, 0), scale_for(d), 0));
-      CKS(ef_fill_uniform(s, sb + nff * esz, dt, nff, ef_stream_key(cfg.seed, l, e, 1),
+      CKS(ef_fill_uniform(s, sb, dt, nff, ef_stream_key(cfg.seed, l, ge, 0), scale_for(d), 0));
+      CKS(ef_fill_uniform(s, sb + nff * esz, dt, nff, ef_stream_key(cfg.seed, l, ge, 1),
                           scale_for(d), 0));
-      CKS(ef_fill_uniform(s, sb + 2 * nff * esz, dt, nff, ef_stream_key(cfg.seed, l, e, 2),
+      CKS(ef_fill_uniform(s, sb + 2 * nff * esz, dt, nff, ef_stream_key(cfg.seed, l, ge, 2),
                           scale_for(ff), 0));
       CK(cudaMemcpyAsync(store[l] + (int64_t)e * stride, sb, 3 * nff * esz,
                          cudaMemcpyDeviceToHost, s));
@@ -473,9 +563,9 @@ void ef_engine::init_weights() {
 // Fill the peer pool from the host store (once, at create).  Cross-device
 // pools need peer access in both directions; the copies then run over NVLink.
 void ef_engine::init_peer_pool() {
-  peer_n = std::min<int64_t>(cfg.peer_pool_experts, (int64_t)cfg.L * cfg.M);
+  peer_n = std::min<int64_t>(cfg.peer_pool_experts, (int64_t)cfg.L * sM());
   peer_dev = cfg.peer_device;
-  const int64_t LM = (int64_t)cfg.L * cfg.M;
+  const int64_t LM = (int64_t)cfg.L * sM();
   std::vector<int64_t> ids((size_t)peer_n);
   pool_slot_of.assign((size_t)LM, -1);
   for (int64_t i = 0; i < peer_n; ++i) {
@@ -515,7 +605,7 @@ void ef_engine::init_peer_pool() {
   CK(cudaSetDevice(peer_dev));
   CK(cudaMalloc(&peer_pool, (size_t)peer_n * stride));
   for (int64_t i = 0; i < peer_n; ++i)
-    CK(cudaMemcpy(peer_pool + i * stride, store[ids[i] / cfg.M] + (ids[i] % cfg.M) * stride,
+    CK(cudaMemcpy(peer_pool + i * stride, store[ids[i] / sM()] + (ids[i] % sM()) * stride,
                   stride, cudaMemcpyHostToDevice));
   CK(cudaSetDevice(cfg.device));
 }
@@ -539,7 +629,7 @@ ef_engine::~ef_engine() {
                   (void*)sgl_d, (void*)wts_d, (void*)y_d, (void*)ys_d, (void*)sel_d,
                   (void*)counts_d, (void*)offsets_d, (void*)perm_d, (void*)inv_d, act_d, acts_d,
                   (void*)dctrl, (void*)ready, (void*)stats_d, (void*)fuse_d, (void*)h_io_d,
-                  (void*)fast_words, (void*)px_d, (void*)plogits_d, (void*)pwts_d, (void*)py_d,
+                  (void*)fast_words, (void*)fmask_d, (void*)px_d, (void*)plogits_d, (void*)pwts_d, (void*)py_d,
                   (void*)pys_d, (void*)psgl_d, (void*)psel_d, (void*)pcounts_d, (void*)poffsets_d,
                   (void*)pperm_d, (void*)pinv_d, (void*)piota_d, pA_d, pact_d, pacts_d,
                   (void*)ptiles_d})
@@ -557,6 +647,11 @@ ef_engine::~ef_engine() {
       if (p) cudaFreeHost(p);
   }
   if (xrec_h) cudaFreeHost(xrec_h);
+  for (void* p : {(void*)ep_send, (void*)ep_recv, (void*)ep_yslots, (void*)ep_yrecv,
+                  (void*)ep_counts, (void*)ep_offsets, (void*)ep_perm, (void*)ep_home, ep_act})
+    if (p) cudaFree(p);
+  if (ep_hout) cudaFreeHost(ep_hout);
+  xport.reset();
   if (rec_stream) cudaStreamDestroy(rec_stream);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (compute_stream) cudaStreamDestroy(compute_stream);
@@ -589,7 +684,9 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
       for (int e = 0; e < M; ++e) rf.tab[e] = host_tab[(int64_t)l * M + e];
     CKS(router_route_fused(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
                            B, d, M, logits_d, stats_d + kStats * l + 7, k, cfg.route_mode,
-                           cfg.routing_bias, mask[0], mask[1], sel_d, wts_d, counts_d, offsets_d,
+                           cfg.routing_bias, mask[0], mask[1], cur_topup, fmask_d + 2 * l,
+                           fp ? nullptr : dev_of(&out(l)->mask[0]), sel_d, wts_d, counts_d,
+                           offsets_d,
                            perm_d, inv_d, dev_of(out_sel(l)), dev_of(out_logits(l)),
                            fp ? nullptr : const_cast<uint32_t*>(&dev_of(out(l))->done),
                            stats_d + kStats * l + 6, fuse_d,
@@ -610,8 +707,8 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
       ++launches;
     }
     CKS(launch_route_publish(stream, logits_d, B, M, k, cfg.route_mode, cfg.routing_bias, mask[0],
-                             mask[1], sel_d, wts_d, counts_d, offsets_d, perm_d, inv_d, nullptr,
-                             dev_of(out_sel(l)), dev_of(out_logits(l)),
+                             mask[1], cur_topup, sel_d, wts_d, counts_d, offsets_d, perm_d, inv_d,
+                             dev_of(&out(l)->mask[0]), dev_of(out_sel(l)), dev_of(out_logits(l)),
                              const_cast<uint32_t*>(&dev_of(out(l))->done),
                              stats_d + kStats * l + 6, R * B * M));
     ++launches;
@@ -634,7 +731,8 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
     if (fast_path()) {
       io = GateIO{fast_words + l, sel_d, logits_d, B * k, layer_R[l] * B * M,
                   dev_of(out_sel(l)), dev_of(out_logits(l)),
-                  const_cast<uint32_t*>(&dev_of(out(l))->done), M};
+                  const_cast<uint32_t*>(&dev_of(out(l))->done), M, fmask_d + 2 * l,
+                  dev_of(&out(l)->mask[0])};
     }
     CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
                          reinterpret_cast<volatile unsigned*>(fuse_d + 2), layer_seq[l], ready,
@@ -725,28 +823,23 @@ void ef_engine::step_host(cudaStream_t caller, const float* h_in, float* h_out, 
 
 void ef_engine::step_on(cudaStream_t stream, float* h, int B,
                         const std::vector<int64_t>& tokens_in) {
+  if (ep) {
+    ep_step_on(stream, h, B, tokens_in);
+    return;
+  }
   using clk = std::chrono::steady_clock;
   const int L = cfg.L, M = cfg.M, k = cfg.top_k;
   if (B < 1 || B > cfg.max_batch) throw ValueError("batch size outside [1, max_batch]");
   std::vector<int64_t> tokens = tokens_in;
-  if (tokens.empty()) tokens.push_back(-(int64_t)(steps + 1));  // unique prediction-cache key
-  if (cfg.timing) {
-    if (!stats_pin[0]) {
-      for (int i = 0; i < 2; ++i) {
-        CK(cudaHostAlloc(&stats_pin[i], sizeof(unsigned long long) * kStats * L,
-                         cudaHostAllocDefault));
-        for (int j = 0; j < 3; ++j) CK(cudaEventCreate(&tev[i][j]));
-      }
-    }
-    CK(cudaEventRecord(tev[stats_buf][0], stream));
-    copies_at_step = copies;
-  }
+  // unique prediction-cache key per scheduler token (restarts at reset())
+  if (tokens.empty()) tokens.push_back(-(int64_t)(st->tokens_run() + 1));
+  timing_begin(stream);
   cur_h = h;
   CKS(launch_init_stats(stream, stats_d, L));
   CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
   launches += 2;
   mask_tokens = B;
-  residency_mask(0, cur_mask);
+  cur_topup = residency_mask(0, cur_mask);
 
   std::vector<int64_t> gsizes(B, 1);
   double host_acc = 0;
@@ -794,6 +887,10 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       const int32_t* sel = out_sel(l);
       const float* lg0 = out_logits(l);
       const int R = layer_R[l];
+      if (cfg.routing_bias != 0.f) {  // the mask the route kernel selected on (after top-up)
+        cur_mask[0] = ho->mask[0];
+        cur_mask[1] = ho->mask[1];
+      }
       // ---- scheduler view of this layer's routing (workload.py:161-179 contract)
       LayerRouting r;
       r.gate.resize(M);
@@ -816,7 +913,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       hooks->pregate_fn = [&, R, lg0](int layer, int hz, double* o) {
         if (hz >= R) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
         uint64_t m[2];
-        residency_mask(layer + hz, m);
+        scored_mask(layer + hz, lg0 + (int64_t)hz * B * M, B, m);
         batch_gate(lg0 + (int64_t)hz * B * M, B, M, cfg.routing_bias, m, o);
       };
       if (cfg.record_routing) {
@@ -869,7 +966,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       host_acc += std::chrono::duration<double, std::milli>(clk::now() - h0).count();
       // enqueue layer l+1 while FFN(l) runs: its horizon and bias mask are final now
       if (l + 1 < L) {
-        residency_mask(l + 1, cur_mask);
+        cur_topup = residency_mask(l + 1, cur_mask);
         const int R1 = 1 + st->planned_horizon(l + 1);
         if (debug) {
           dbg_sync("copies", l);
@@ -900,17 +997,202 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
   }
   host_ms += host_acc;
   ++steps;
-  if (cfg.timing) {
-    const int i = stats_buf;
-    CK(cudaEventRecord(tev[i][1], stream));
-    CK(cudaMemcpyAsync(stats_pin[i], stats_d, sizeof(unsigned long long) * kStats * L,
-                       cudaMemcpyDeviceToHost, stream));
-    CK(cudaEventRecord(tev[i][2], stream));
-    stats_copies[i] = copies - copies_at_step;
-    if (stats_pending >= 0) fold_stats(stats_pending);  // (folded at step start normally)
-    stats_pending = i;
-    stats_buf ^= 1;
+  timing_end(stream);
+}
+
+void ef_engine::timing_begin(cudaStream_t stream) {
+  if (!cfg.timing) return;
+  if (!stats_pin[0]) {
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaHostAlloc(&stats_pin[i], sizeof(unsigned long long) * kStats * cfg.L,
+                       cudaHostAllocDefault));
+      for (int j = 0; j < 3; ++j) CK(cudaEventCreate(&tev[i][j]));
+    }
   }
+  CK(cudaEventRecord(tev[stats_buf][0], stream));
+  copies_at_step = copies;
+}
+
+void ef_engine::timing_end(cudaStream_t stream) {
+  if (!cfg.timing) return;
+  const int i = stats_buf;
+  CK(cudaEventRecord(tev[i][1], stream));
+  CK(cudaMemcpyAsync(stats_pin[i], stats_d, sizeof(unsigned long long) * kStats * cfg.L,
+                     cudaMemcpyDeviceToHost, stream));
+  CK(cudaEventRecord(tev[i][2], stream));
+  stats_copies[i] = copies - copies_at_step;
+  if (stats_pending >= 0) fold_stats(stats_pending);  // (folded at step start normally)
+  stats_pending = i;
+  stats_buf ^= 1;
+}
+
+
+// ---------------------------------------------------------------- expert parallelism
+void ef_engine::ep_alloc() {
+  const int B = cfg.max_batch, k = cfg.top_k, d = cfg.d, M = cfg.M, L = cfg.L;
+  const int64_t words = (int64_t)B * d + (int64_t)L * B * M + 2LL * B * k;
+  ep_W = (words + 3) / 4 * 4;
+  const int64_t GBk = (int64_t)G * B * k;
+  CK(cudaMalloc(&ep_send, sizeof(float) * ep_W));
+  CK(cudaMalloc(&ep_recv, sizeof(float) * ep_W * G));
+  CK(cudaMemset(ep_send, 0, sizeof(float) * ep_W));
+  CK(cudaMalloc(&ep_yslots, sizeof(float) * GBk * d));
+  CK(cudaMalloc(&ep_yrecv, sizeof(float) * GBk * d));
+  CK(cudaMalloc(&ep_counts, sizeof(int32_t) * Ms));
+  CK(cudaMalloc(&ep_offsets, sizeof(int32_t) * (Ms + 1)));
+  CK(cudaMalloc(&ep_perm, sizeof(int32_t) * GBk));
+  CK(cudaMalloc(&ep_home, sizeof(int32_t) * B * k));
+  CK(cudaMalloc(&ep_act, (size_t)GBk * cfg.ff * esz));
+  const size_t hbytes = 128 + sizeof(int32_t) * GBk + sizeof(float) * (size_t)L * G * B * M;
+  CK(cudaHostAlloc(&ep_hout, hbytes, cudaHostAllocMapped));
+  std::memset(ep_hout, 0, hbytes);
+  CK(cudaHostGetDevicePointer((void**)&ep_hout_dev, ep_hout, 0));
+}
+
+// One expert-parallel decode step: the reference's
+// per-layer loop (engine.py:566-659) runs per shard, over the owned experts'
+// access subsequence of all G*B tokens.  Synchronous per layer: the host
+// decides layer l from the gathered routing before its FFN is enqueued.
+void ef_engine::ep_step_on(cudaStream_t stream, float* h, int B,
+                           const std::vector<int64_t>& tokens_in) {
+  using clk = std::chrono::steady_clock;
+  const int L = cfg.L, M = cfg.M, k = cfg.top_k, d = cfg.d;
+  if (B != cfg.max_batch)
+    throw ValueError("expert-parallel steps run exactly max_batch tokens per rank");
+  std::vector<int64_t> tokens = tokens_in;
+  if (tokens.empty()) tokens.push_back(-(int64_t)(st->tokens_run() + 1));
+  const int GB = G * B;
+  const bool sgate = cfg.shared_ff && cfg.shared_gate;
+  volatile uint32_t* hdone = reinterpret_cast<volatile uint32_t*>(ep_hout);
+  const int32_t* hsel = reinterpret_cast<const int32_t*>(ep_hout + 128);
+  const float* hlog = reinterpret_cast<const float*>(ep_hout + 128 + sizeof(int32_t) * GB * k);
+  timing_begin(stream);
+  CKS(launch_init_stats(stream, stats_d, L));
+  CKS(ef_rmsnorm(stream, h, x_d, B, d, 1e-6f));
+  launches += 2;
+  std::vector<int64_t> gsizes(GB, 1);
+  double host_acc = 0;
+  int R = Rmax;
+  for (int l = 0; l < L; ++l) {
+    R = std::max(1, std::min(R, L - l));
+    layer_R[l] = R;
+    // ---- route this rank's tokens (router rows l .. l+R-1), shared expert
+    CKS(router_logits_stamped(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype,
+                              R, B, d, M, logits_d, stats_d + kStats * l + 7));
+    CKS(launch_route_publish(stream, logits_d, B, M, k, cfg.route_mode, 0.f, 0, 0, 0, sel_d, wts_d,
+                             counts_d, offsets_d, perm_d, inv_d, nullptr, nullptr, nullptr,
+                             nullptr, stats_d + kStats * l + 6, 0));
+    launches += 2;
+    if (cfg.shared_ff) {
+      if (sgate) {
+        CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B,
+                             d, 1, sgl_d));
+        ++launches;
+      }
+      const char* sw = shared_w + (int64_t)l * sstride;
+      int32_t z = 0, nb = B;
+      CKS(expert_ffn_ptrs(stream, x_d, perm_d, k, true, &sw, &z, &nb, 1, d, cfg.shared_ff,
+                          cfg.dtype, acts_d, ys_d));
+      launches += 2;
+    }
+    // ---- dispatch: every rank's routing block to every rank
+    CKS(ep_pack(stream, x_d, logits_d, sel_d, wts_d, B, d, L, M, k, ep_send));
+    xport->allgather(ep_send, ep_recv, sizeof(float) * ep_W, stream);
+    CKS(ep_owner(stream, ep_recv, ep_W, G, B, k, M, d, L, R, ep_rank, e0, Ms, ep_counts, ep_offsets,
+                 ep_perm, ep_home, reinterpret_cast<int32_t*>(ep_hout_dev + 128),
+                 reinterpret_cast<float*>(ep_hout_dev + 128 + sizeof(int32_t) * GB * k),
+                 reinterpret_cast<uint32_t*>(ep_hout_dev)));
+    launches += 2;
+    ++ep_collectives;
+    ep_bytes += (int64_t)sizeof(float) * ep_W * G;
+    auto w0 = clk::now();
+    unsigned spins = 0;
+    while (*hdone == 0u) {
+      _mm_pause();
+      if ((++spins & 0xffff) == 0 && std::chrono::duration<double>(clk::now() - w0).count() > 60.0)
+        throw RuntimeErr("expert-parallel routing exchange did not complete within 60 s");
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    *hdone = 0u;
+    auto h0 = clk::now();
+    // ---- the shard's view of the layer (workload.py:161-179 contract over
+    // the owned experts, local ids): one group per global token
+    LayerRouting r;
+    r.gate.resize(Ms);
+    std::vector<int> cnt;
+    ep_shard_view(hlog, hsel, GB, M, k, e0, Ms, r.gate.data(), &r.group_actual, &r.actual, &cnt);
+    hooks->pregate_fn = [&, R, hlog](int layer, int hz, double* o) {
+      if (hz >= R) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
+      shard_gate(hlog + (int64_t)hz * GB * M, GB, o);
+    };
+    if (cfg.record_routing) {
+      std::vector<float> lg(hlog, hlog + (int64_t)R * GB * M);
+      rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(hsel, hsel + GB * k), R, GB, 0,
+                                0,
+                                cfg.record_routing == 2 ? std::vector<float>()
+                                                        : record_x(x_d, (int64_t)B * d),
+                                B});
+    }
+    for (int j : r.actual)
+      if (pf_pending[(int64_t)l * Ms + j]) {
+        pf_pending[(int64_t)l * Ms + j] = 0;
+        ++pf_used;
+      }
+    if (l == 0) st->begin_token(tokens, gsizes, r);
+    std::fill(layer_use.begin(), layer_use.end(), -1);
+    st->begin_layer(l);
+    st->run_layer(l, r);
+    // ---- the owner's FFN over the gathered rows of its experts
+    HostCtrl& hc = hctrl[l];
+    int n = 0, run = 0, max_rows = 0;
+    for (int j = 0; j < Ms; ++j) {
+      if (cnt[j]) {
+        const int sl = layer_use[j];
+        if (sl < 0) throw RuntimeErr("routed expert has no resolved slot");
+        hc.ent[n++] = make_int4(sl, run, cnt[j], (int)slot_seq[sl]);
+        max_rows = std::max(max_rows, cnt[j]);
+      }
+      run += cnt[j];
+    }
+    if (n > kMaxActive) throw RuntimeErr("more active experts than the control block holds");
+    hc.n_active = n;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    host_acc += std::chrono::duration<double, std::milli>(clk::now() - h0).count();
+    if (n > 0) {
+      hc.go = 1u;
+      CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + kStats * l));
+      CKS(expert_ffn_ep(stream, ep_recv, ep_W, B, ep_perm, k, slab, stride, &dctrl[l], ready,
+                        stats_d + kStats * l, std::min(Ms, kMaxActive), max_rows, d, cfg.ff,
+                        cfg.dtype, ep_act, ep_yslots));
+      launches += 3;
+      ffn_bytes += (int64_t)n * stride;
+      ffn_launches += 2;
+    }
+    // ---- combine: every y row back to its token's rank, rank-order sum
+    xport->alltoall(ep_yslots, ep_yrecv, sizeof(float) * (size_t)B * k * d, stream);
+    ++ep_collectives;
+    ep_bytes += (int64_t)sizeof(float) * G * B * k * d;
+    CKS(combine_stamped(stream, h, l + 1 < L ? x_d : nullptr, ep_yrecv, ep_home, wts_d,
+                        cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, B, d, k, 1e-6f,
+                        stats_d + kStats * l + 5));
+    ++launches;
+    if (debug) {
+      CK(cudaStreamSynchronize(stream));
+      CK(cudaStreamSynchronize(copy_stream));
+    }
+    // slots read by FFN(l) are reusable once the next layer's exchange has
+    // completed (stream order: FFN(l) precedes it)
+    for (int s2 : pinned_list) pinned[s2] = 0;
+    pinned_list.clear();
+    for (int s2 : deferred_free) free_slots.push_back(s2);
+    deferred_free.clear();
+    if (l + 1 < L) R = 1 + st->planned_horizon(l + 1);
+  }
+  st->end_token();
+  host_ms += host_acc;
+  ++steps;
+  ++ep_steps;
+  timing_end(stream);
 }
 
 void ef_engine::fold_stats(int i) {
@@ -980,7 +1262,7 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
   if (max_prefill < 1) throw ValueError("engine created without prefill buffers (max_prefill)");
   if (T < 1 || T > max_prefill) throw ValueError("prefill length outside [1, max_prefill]");
   std::vector<int64_t> tokens = tokens_in;
-  if (tokens.empty()) tokens.push_back(-(steps + prefills + 1));
+  if (tokens.empty()) tokens.push_back(-(int64_t)(st->tokens_run() + 1));
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
   const int sff = cfg.shared_ff;
   std::vector<int64_t> gsizes(T, 1);
@@ -990,7 +1272,7 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
   // U-expert subset per layer would change the prompt's routing wholesale, and
   // the grouped GEMM streams each expert once whatever the union
   mask_tokens = 0;
-  residency_mask(0, cur_mask);
+  residency_mask(0, cur_mask);  // residents only: no top-up
   int R = Rmax;
   for (int l = 0; l < L; ++l) {
     R = std::max(1, std::min(R, L - l));
@@ -998,7 +1280,7 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
     CKS(ef_router_logits(stream, px_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R, T,
                          d, M, plogits_d));
     CKS(launch_route_publish(stream, plogits_d, T, M, k, cfg.route_mode, cfg.routing_bias,
-                             cur_mask[0], cur_mask[1], psel_d, pwts_d, pcounts_d, poffsets_d,
+                             cur_mask[0], cur_mask[1], 0, psel_d, pwts_d, pcounts_d, poffsets_d,
                              pperm_d, pinv_d, nullptr, nullptr, nullptr, nullptr, nullptr, 0));
     launches += 2;
     CK(cudaMemcpyAsync(plogits_h, plogits_d, sizeof(float) * R * T * M, cudaMemcpyDeviceToHost,
@@ -1027,7 +1309,7 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
     hooks->pregate_fn = [&, R, lg0](int layer, int hz, double* o) {
       if (hz >= R) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
       uint64_t m[2];
-      residency_mask(layer + hz, m);
+      residency_mask(layer + hz, m);  // mask_tokens = 0: residents only
       batch_gate(lg0 + (int64_t)hz * T * M, T, M, cfg.routing_bias, m, o);
     };
     if (cfg.record_routing) {
@@ -1126,7 +1408,7 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
 // starts from a cold cache exactly like a new engine (bench grids and
 // baselines reuse one engine instead of refilling a 90 GB host store).
 void ef_engine::reset(const SimConfig& sc, float bias) {
-  if (sc.L != cfg.L || sc.M != cfg.M || sc.top_k != cfg.top_k || sc.expert_size != stride)
+  if (sc.L != cfg.L || sc.M != simcfg.M || sc.top_k != simcfg.top_k || sc.expert_size != stride)
     throw ValueError("reset: scheduler shape differs from the engine's");
   if (sc.policy.predictor == 3)
     throw ValueError("the oracle predictor needs future routing; it exists only in simulate()");
@@ -1142,7 +1424,7 @@ void ef_engine::reset(const SimConfig& sc, float bias) {
   cfg.routing_bias = bias;
   Rmax = rows_for_policy();
   std::fill(phys_of.begin(), phys_of.end(), -1);
-  for (int64_t i = 0; i < (int64_t)cfg.L * cfg.M; ++i) host_tab[i] = make_int2(-1, 0);
+  for (int64_t i = 0; i < (int64_t)cfg.L * sM(); ++i) host_tab[i] = make_int2(-1, 0);
   std::fill(pf_pending.begin(), pf_pending.end(), 0);
   std::fill(pinned.begin(), pinned.end(), 0);
   pinned_list.clear();
@@ -1174,8 +1456,27 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->stride = 3LL * c.d * c.ff * e->esz;
     e->sstride = 3LL * c.d * c.shared_ff * e->esz;
     e->simcfg = sim_config_from(sim);
-    if (e->simcfg.L != c.L || e->simcfg.M != c.M || e->simcfg.top_k != c.top_k)
-      throw ValueError("scheduler and engine shapes differ");
+    if (c.ep_world < 0 || (c.ep_world > 0 && (c.ep_rank < 0 || c.ep_rank >= c.ep_world)))
+      throw ValueError("bad expert-parallel rank / world");
+    if (c.ep_world > 0) {
+      if (c.M % c.ep_world) throw ValueError("expert parallelism needs ep_world | M");
+      e->ep = true;
+      e->G = c.ep_world;
+      e->ep_rank = c.ep_rank;
+      e->Ms = c.M / c.ep_world;
+      e->e0 = c.ep_rank * e->Ms;
+      if (c.routing_bias != 0.f)
+        throw ValueError("expert-parallel steps take routing_bias 0 (the bias needs every "
+                         "shard's residency before routing)");
+      if (c.max_prefill > 0) throw ValueError("expert-parallel engines decode only");
+      if (c.ep_world > 1 && !c.ep_nccl_id && !c.ep_collective)
+        throw ValueError("ep_world > 1 needs ep_nccl_id or ep_collective");
+    }
+    const int wantM = e->ep ? e->Ms : c.M, wantK = e->ep ? std::min(c.top_k, e->Ms) : c.top_k;
+    if (e->simcfg.L != c.L || e->simcfg.M != wantM || e->simcfg.top_k != wantK)
+      throw ValueError(e->ep ? "an expert-parallel shard's scheduler has M/G experts and top_k "
+                               "min(k, M/G)"
+                             : "scheduler and engine shapes differ");
     if (e->simcfg.expert_size != e->stride)
       throw ValueError("scheduler expert_size_bytes must equal the expert blob size");
     if (e->simcfg.policy.predictor == 3)
@@ -1265,7 +1566,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     if (c.host_store_shm && c.host_store_shm[0]) {
       // one pinned host store shared by every process on the node (replica
       // ranks): POSIX shared memory, registered with CUDA in each process
-      const size_t bytes = (size_t)L * M * e->stride;
+      const size_t bytes = (size_t)L * e->sM() * e->stride;
       const bool create = !c.host_store_attach;
       int fd = shm_open(c.host_store_shm, create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
       if (fd < 0) throw RuntimeErr(std::string("shm_open failed for ") + c.host_store_shm);
@@ -1280,11 +1581,11 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       e->shm_bytes = bytes;
       if (create) e->shm_name = c.host_store_shm;
       CK(cudaHostRegister(base, bytes, cudaHostRegisterDefault));
-      for (int l = 0; l < L; ++l) e->store[l] = (char*)base + (size_t)l * M * e->stride;
+      for (int l = 0; l < L; ++l) e->store[l] = (char*)base + (size_t)l * e->sM() * e->stride;
       e->store_filled = !create;
     } else {
       for (int l = 0; l < L; ++l)
-        CK(cudaHostAlloc(&e->store[l], (size_t)M * e->stride, cudaHostAllocDefault));
+        CK(cudaHostAlloc(&e->store[l], (size_t)e->sM() * e->stride, cudaHostAllocDefault));
     }
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
@@ -1297,20 +1598,30 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     if (c.record_routing) e->alloc_record();
     e->slot_seq.assign(e->P, 0);
     e->pinned.assign(e->P, 0);
-    e->phys_of.assign((size_t)L * M, -1);
-    e->pf_pending.assign((size_t)L * M, 0);
+    e->phys_of.assign((size_t)L * e->sM(), -1);
+    e->pf_pending.assign((size_t)L * e->sM(), 0);
     e->layer_R.assign(L, 1);
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
     e->init_weights();
+    if (e->ep) {
+      if (c.ep_nccl_id)
+        e->xport = make_nccl_transport(c.ep_world, c.ep_rank, c.ep_nccl_id);
+      else if (c.ep_collective)
+        e->xport = make_callback_transport(c.ep_collective, c.ep_user);
+      else
+        e->xport = make_local_transport();
+      e->ep_alloc();
+    }
     if (c.peer_pool_experts < 0) throw ValueError("peer_pool_experts must be >= 0");
     if (c.peer_pool_experts > 0) e->init_peer_pool();
     if (preload_pipeline_kernels() < 30) throw CudaErr("could not load the pipeline kernels");
     const char* dbg = getenv("EF_PIPE_DEBUG");
     e->debug = dbg && dbg[0] == '1';
-    CK(cudaHostAlloc(&e->host_tab, sizeof(int2) * L * M, cudaHostAllocDefault));
-    for (int64_t i = 0; i < (int64_t)L * M; ++i) e->host_tab[i] = make_int2(-1, 0);
+    CK(cudaHostAlloc(&e->host_tab, sizeof(int2) * L * e->sM(), cudaHostAllocDefault));
+    for (int64_t i = 0; i < (int64_t)L * e->sM(); ++i) e->host_tab[i] = make_int2(-1, 0);
     CK(cudaMalloc(&e->fast_words, sizeof(unsigned) * L));
+    CK(cudaMalloc(&e->fmask_d, sizeof(uint64_t) * 2 * L));
     CK(cudaMemset(e->fast_words, 0, sizeof(unsigned) * L));
     e->layer_seq.assign(L, 0);
     CK(cudaMalloc(&e->fuse_d, sizeof(int) * 4));
@@ -1469,8 +1780,91 @@ extern "C" int ef_engine_routing_x(ef_engine* e, int64_t index, float* x, int64_
 
 extern "C" int ef_engine_slot_of(ef_engine* e, int32_t layer, int32_t expert, int32_t* slot) {
   EF_TRY({
-    if (layer < 0 || layer >= e->cfg.L || expert < 0 || expert >= e->cfg.M)
-      throw ValueError("expert id out of range");
-    *slot = e->phys_of[(int64_t)layer * e->cfg.M + expert];
+    if (layer < 0 || layer >= e->cfg.L || expert < 0 || expert >= e->sM())
+      throw ValueError("expert id out of range (local ids under expert parallelism)");
+    *slot = e->phys_of[(int64_t)layer * e->sM() + expert];
+  });
+}
+
+// ---------------------------------------------------------------- EP C ABI
+struct ef_ep_comm {
+  std::unique_ptr<Transport> t;
+  int world = 1, rank = 0;
+};
+
+extern "C" int ef_ep_comm_create(int world, int rank, const void* nccl_id128, ef_collective_cb cb,
+                                 void* user, ef_ep_comm** out) {
+  EF_TRY({
+    if (world < 1 || rank < 0 || rank >= world) throw ValueError("bad EP rank / world");
+    auto c = std::make_unique<ef_ep_comm>();
+    c->world = world;
+    c->rank = rank;
+    if (nccl_id128)
+      c->t = make_nccl_transport(world, rank, nccl_id128);
+    else if (cb)
+      c->t = make_callback_transport(cb, user);
+    else if (world == 1)
+      c->t = make_local_transport();
+    else
+      throw ValueError("world > 1 needs a NCCL id or a collective callback");
+    *out = c.release();
+  });
+}
+
+extern "C" void ef_ep_comm_destroy(ef_ep_comm* c) { delete c; }
+
+extern "C" int ef_ep_dispatch(ef_ep_comm* c, void* stream, const float* x, const float* logits,
+                              const int32_t* sel, const float* wts, int B, int d, int Rm, int M,
+                              int k, int64_t block_words, float* send, float* recv) {
+  EF_TRY({
+    if (block_words < (int64_t)B * d + (int64_t)Rm * B * M + 2LL * B * k)
+      throw ValueError("block_words smaller than the routing block");
+    auto st = reinterpret_cast<cudaStream_t>(stream);
+    CKS(ep_pack(st, x, logits, sel, wts, B, d, Rm, M, k, send));
+    c->t->allgather(send, recv, sizeof(float) * block_words, st);
+  });
+}
+
+extern "C" int ef_ep_owner(void* stream, const float* recv, int64_t block_words, int G, int B, int k,
+                           int M, int d, int Rm, int rank, int e0, int Ms, int32_t* counts,
+                           int32_t* offsets, int32_t* perm, int32_t* home_idx) {
+  EF_TRY({
+    // publish targets unused outside the engine: a scratch mapped word
+    static uint32_t* scratch = nullptr;
+    static uint32_t* scratch_dev = nullptr;
+    if (!scratch) {
+      CK(cudaHostAlloc(&scratch, 64, cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer((void**)&scratch_dev, scratch, 0));
+    }
+    CKS(ep_owner(reinterpret_cast<cudaStream_t>(stream), recv, block_words, G, B, k, M, d, Rm, 0,
+                 rank, e0, Ms, counts, offsets, perm, home_idx, nullptr, nullptr, scratch_dev));
+  });
+}
+
+extern "C" int ef_ep_combine(ef_ep_comm* c, void* stream, const float* y_slots, float* y_recv,
+                             const int32_t* home_idx, const float* wts, const float* ys,
+                             const float* shared_gate_logit, int B, int d, int k, float* h,
+                             float* x) {
+  EF_TRY({
+    auto st = reinterpret_cast<cudaStream_t>(stream);
+    c->t->alltoall(y_slots, y_recv, sizeof(float) * (size_t)B * k * d, st);
+    CKS(combine_stamped(st, h, x, y_recv, home_idx, wts, ys, shared_gate_logit, B, d, k, 1e-6f,
+                        nullptr));
+  });
+}
+
+extern "C" int ef_ep_shard_view(const float* logits, const int32_t* sel, int GB, int M, int k,
+                                int G, int rank, double* gate, int32_t* groups, int32_t* actual,
+                                int32_t* n_actual) {
+  EF_TRY({
+    if (G < 1 || M % G || rank < 0 || rank >= G) throw ValueError("bad EP shard");
+    const int Ms = M / G, e0 = rank * Ms;
+    std::vector<std::vector<int>> g;
+    std::vector<int> a, cnt;
+    ep_shard_view(logits, sel, GB, M, k, e0, Ms, gate, &g, &a, &cnt);
+    for (int t = 0; t < GB; ++t)
+      for (int j = 0; j < k; ++j) groups[t * k + j] = j < (int)g[t].size() ? g[t][j] : -1;
+    for (int j = 0; j < Ms; ++j) actual[j] = j < (int)a.size() ? a[j] : -1;
+    *n_actual = (int32_t)a.size();
   });
 }

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstddef>
 #include <cstdio>
 #include <string>
@@ -366,7 +367,6 @@ struct RouteSmem {
   int32_t warp_cnt[32][kMaxExperts];
   int32_t base[kMaxExperts];
   int32_t total[kMaxExperts];
-  uint64_t mask[2];
 };
 
 // Top-k of one token's logits by one warp (M <= 128), keyed on
@@ -465,25 +465,134 @@ __device__ void topk_token(const float* __restrict__ lg, int M, int k, int mode,
   }
 }
 
+// Cache-aware routing mask top-up (oracle/numerics.py routing_mask; the rule
+// is ours, the reference only reorders groups, engine.py:192-209).  When the
+// host asks for U > 0 experts, the residents in (mlo, mhi) are joined by the
+// best U - n non-resident experts by router votes: the number of tokens whose
+// UNBIASED top-k (raw fp32 logits, value desc / index asc) contains the
+// expert, then its largest logit over the batch, then the lower index — the
+// set that changes the fewest tokens' selections.  Whole CTA; every thread
+// gets the final mask.  All comparisons are exact (no arithmetic), so the
+// oracle reproduces it bit for bit.
+struct TopupSmem {
+  int votes[kMaxExperts];
+  int maxl[kMaxExperts];
+  uint64_t m[2];
+};
+__device__ __forceinline__ int float_order(float f) {
+  const int i = __float_as_int(__fadd_rn(f, 0.0f));  // -0 -> +0
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ bool mask_has(uint64_t lo, uint64_t hi, int e) {
+  return e < 64 ? ((lo >> e) & 1ull) : ((hi >> (e - 64)) & 1ull);
+}
+__device__ void topup_mask(TopupSmem& ts, const float* __restrict__ logits, int B, int M, int k,
+                           int U, uint64_t& mlo, uint64_t& mhi) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  for (int e = tid; e < kMaxExperts; e += blockDim.x) {
+    ts.votes[e] = 0;
+    ts.maxl[e] = INT_MIN;
+  }
+  __syncthreads();
+  for (int t = wid; t < B; t += nw) {
+    const float* lg = logits + (int64_t)t * M;
+    float v[4];
+    bool taken[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = lane + 32 * i;
+      v[i] = e < M ? __ldcg(lg + e) : -INFINITY;
+      taken[i] = e >= M;
+      if (e < M) atomicMax(&ts.maxl[e], float_order(v[i]));
+    }
+    for (int r = 0; r < k; ++r) {
+      float bk = 0.f;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (!taken[i] && (be == 0x7fffffff || v[i] > bk)) {
+          bk = v[i];
+          be = lane + 32 * i;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (oe != 0x7fffffff && (be == 0x7fffffff || ok > bk || (ok == bk && oe < be))) {
+          bk = ok;
+          be = oe;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (lane + 32 * i == be) taken[i] = true;
+      if (lane == 0 && be != 0x7fffffff) atomicAdd(&ts.votes[be], 1);
+    }
+  }
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t lo = mlo, hi = mhi;
+    int n = __popcll(lo) + __popcll(hi);
+    for (; n < U; ++n) {
+      int bv = -1, bm = INT_MIN, be = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = lane + 32 * i;
+        if (e < M && !mask_has(lo, hi, e)) {
+          const int cv = ts.votes[e], cm = ts.maxl[e];
+          if (be == 0x7fffffff || cv > bv || (cv == bv && cm > bm)) {
+            bv = cv;
+            bm = cm;
+            be = e;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int om = __shfl_xor_sync(0xffffffffu, bm, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (oe != 0x7fffffff &&
+            (be == 0x7fffffff || ov > bv || (ov == bv && (om > bm || (om == bm && oe < be))))) {
+          bv = ov;
+          bm = om;
+          be = oe;
+        }
+      }
+      if (be == 0x7fffffff) break;
+      if (be < 64)
+        lo |= 1ull << be;
+      else
+        hi |= 1ull << (be - 64);
+    }
+    if (lane == 0) {
+      ts.m[0] = lo;
+      ts.m[1] = hi;
+    }
+  }
+  __syncthreads();
+  mlo = ts.m[0];
+  mhi = ts.m[1];
+}
+
 // Route body, usable by any block size (the standalone kernel runs it with
 // 1024 threads, the fused router kernel with the last router CTA).
 __device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int B, int M, int k,
-                           int mode, float bias, uint64_t mlo, uint64_t mhi,
-                           int32_t* __restrict__ sel, float* __restrict__ wts,
+                           int mode, float bias, uint64_t mlo, uint64_t mhi, int topup_U,
+                           uint64_t* mask_out, int32_t* __restrict__ sel, float* __restrict__ wts,
                            int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
                            int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-                           const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
+                           uint64_t* host_mask, int32_t* host_sel, float* host_logits,
                            volatile uint32_t* host_done, unsigned long long* stamp, int n_pub) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (stamp && tid == 0) *stamp = gtimer();
-  if (mask_src) {  // mask in mapped host memory: one PCIe read, broadcast through smem
-    if (tid == 0) {
-      sm.mask[0] = mask_src[0];
-      sm.mask[1] = mask_src[1];
-    }
-    __syncthreads();
-    mlo = sm.mask[0];
-    mhi = sm.mask[1];
+  if (topup_U > 0) {
+    __shared__ TopupSmem ts;
+    topup_mask(ts, logits, B, M, k, topup_U, mlo, mhi);
+  }
+  if (mask_out && tid == 0) {
+    mask_out[0] = mlo;
+    mask_out[1] = mhi;
   }
 
   // ---- top-k and weights: one warp per token, logits in registers (M <= 128),
@@ -547,6 +656,10 @@ __device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int 
     // warp: a system-scope fence costs microseconds per warp that issues it
     for (int f = lane; f < N; f += 32) host_sel[f] = sel[f];
     for (int i = lane; i < n_pub; i += 32) host_logits[i] = __ldcg(logits + i);
+    if (host_mask && lane == 0) {
+      host_mask[0] = mlo;
+      host_mask[1] = mhi;
+    }
     __threadfence_system();
     __syncwarp();
     if (lane == 0) {
@@ -558,13 +671,13 @@ __device__ void route_body(RouteSmem& sm, const float* __restrict__ logits, int 
 
 __global__ void __launch_bounds__(kRouteThreads) route_permute_kernel(
     const float* __restrict__ logits, int B, int M, int k, int mode, float bias, uint64_t mlo,
-    uint64_t mhi, int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts,
-    int32_t* __restrict__ offsets, int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-    const volatile uint64_t* mask_src, int32_t* host_sel, float* host_logits,
+    uint64_t mhi, int topup_U, int32_t* __restrict__ sel, float* __restrict__ wts,
+    int32_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ perm,
+    int32_t* __restrict__ inv, uint64_t* host_mask, int32_t* host_sel, float* host_logits,
     volatile uint32_t* host_done, unsigned long long* stamp, int n_pub) {
   __shared__ RouteSmem sm;
-  route_body(sm, logits, B, M, k, mode, bias, mlo, mhi, sel, wts, counts, offsets, perm, inv,
-             mask_src, host_sel, host_logits, host_done, stamp, n_pub);
+  route_body(sm, logits, B, M, k, mode, bias, mlo, mhi, topup_U, nullptr, sel, wts, counts,
+             offsets, perm, inv, host_mask, host_sel, host_logits, host_done, stamp, n_pub);
 }
 
 // Engine decode path: router GEMV rows, then the last CTA to finish runs
@@ -574,6 +687,9 @@ struct RouteArgs {
   int B, M, k, mode;
   float bias;
   uint64_t mlo, mhi;
+  int topup_U;          // > 0: top the mask up to U experts by router votes
+  uint64_t* mask_out;   // device copy of the final mask (the fused gate publishes it)
+  uint64_t* host_mask;  // mapped host copy (configurations where the route publishes)
   int32_t *sel, *counts, *offsets, *perm, *inv, *host_sel;
   float *wts, *host_logits;
   uint32_t* host_done;  // null: the fused gate warp publishes instead
@@ -629,8 +745,17 @@ __device__ void route_small(const float* __restrict__ logits, const RouteArgs& r
   const int B = ra.B, M = ra.M, k = ra.k, N = B * k;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (stamp && threadIdx.x == 0) *stamp = gtimer();
+  uint64_t mlo = ra.mlo, mhi = ra.mhi;
+  if (ra.topup_U > 0) {
+    __shared__ TopupSmem ts;
+    topup_mask(ts, logits, B, M, k, ra.topup_U, mlo, mhi);
+  }
+  if (ra.mask_out && threadIdx.x == 0) {
+    ra.mask_out[0] = mlo;
+    ra.mask_out[1] = mhi;
+  }
   if (wid < B)
-    topk_token(logits + (int64_t)wid * M, M, k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.sel + wid * k,
+    topk_token(logits + (int64_t)wid * M, M, k, ra.mode, ra.bias, mlo, mhi, ra.sel + wid * k,
                ra.wts + wid * k, sel_sh + wid * k);
   __syncthreads();
   if (wid != 0) return;
@@ -689,6 +814,10 @@ __device__ void route_small(const float* __restrict__ logits, const RouteArgs& r
   }
   if (ra.host_done) {  // publish (non-fast configurations)
     if (lane < N) ra.host_sel[lane] = e;
+    if (ra.host_mask && lane == 0) {
+      ra.host_mask[0] = mlo;
+      ra.host_mask[1] = mhi;
+    }
     for (int i = lane; i < B * M; i += 32) ra.host_logits[i] = __ldcg(logits + i);
     __threadfence_system();
     __syncwarp();
@@ -875,9 +1004,9 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     route_small(logits, ra, tabv, ra.stamp_route);
     return;
   }
-  route_body(sm, logits, B, M, ra.k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.sel, ra.wts, ra.counts,
-             ra.offsets, ra.perm, ra.inv, nullptr, ra.host_sel, ra.host_logits, ra.host_done,
-             ra.stamp_route, rows * B);
+  route_body(sm, logits, B, M, ra.k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.topup_U, ra.mask_out,
+             ra.sel, ra.wts, ra.counts, ra.offsets, ra.perm, ra.inv, ra.host_mask, ra.host_sel,
+             ra.host_logits, ra.host_done, ra.stamp_route, rows * B);
   if (ra.rf.dc && (threadIdx.x >> 5) == 0)
     resolve_fast(ra.rf, ra.counts, ra.offsets, M, ra.stamp_route ? ra.stamp_route + 5 : nullptr);
 }
@@ -991,14 +1120,16 @@ __global__ void __launch_bounds__(256) router_route_row_kernel(const float* __re
 namespace ef {
 int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
                        int d, int M, float* logits, unsigned long long* stamp_router, int k,
-                       int mode, float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
+                       int mode, float bias, uint64_t mlo, uint64_t mhi, int topup_U,
+                       uint64_t* mask_out, uint64_t* host_mask, int32_t* sel, float* wts,
                        int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                        int32_t* host_sel, float* host_logits, uint32_t* host_done,
                        unsigned long long* stamp_route, int* counter, const CombineIn* ci,
                        const RouteFast* rf) {
   EF_CHECK_ARG(M <= 128 && k <= 16 && B >= 1, "bad fused route shape");
-  RouteArgs ra{B, M, k, mode, bias, mlo, mhi, sel, counts, offsets, perm, inv, host_sel, wts,
-               host_logits, host_done, stamp_route, counter, rf ? *rf : RouteFast{}};
+  RouteArgs ra{B, M, k, mode, bias, mlo, mhi, topup_U, mask_out, host_mask, sel, counts, offsets,
+               perm, inv, host_sel, wts, host_logits, host_done, stamp_route, counter,
+               rf ? *rf : RouteFast{}};
   CombArgs cb{};
   size_t smem = 0;
   if (ci) {
@@ -1048,9 +1179,9 @@ extern "C" int ef_route_permute(void* stream, const float* logits, int B, int M,
   EF_CHECK_ARG(M >= 1 && M <= 128 && k >= 1 && k <= 16 && k <= M && B >= 0, "bad route shape");
   EF_CHECK_ARG(mode == EF_ROUTE_MIXTRAL || mode == EF_ROUTE_SOFTMAX_TOPK, "bad routing mode");
   route_permute_kernel<<<1, kRouteThreads, 0, S(stream)>>>(logits, B, M, k, mode, bias, mlo, mhi,
-                                                           sel, wts, counts, offsets, perm, inv,
-                                                           nullptr, nullptr, nullptr, nullptr,
-                                                           nullptr, 0);
+                                                           0, sel, wts, counts, offsets, perm,
+                                                           inv, nullptr, nullptr, nullptr,
+                                                           nullptr, nullptr, 0);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -1073,8 +1204,13 @@ struct XGather {  // T(x[perm[p]/k]) — expert input, cast to the weight dtype
   int k, d;
   bool identity;  // shared expert: row p reads token p - id_base
   int id_base;
+  // expert parallelism: token t lives in rank t / tpr's block of the
+  // all-gathered routing buffer, rank_stride floats apart (tpr 0: contiguous)
+  int tpr = 0;
+  int64_t rank_stride = 0;
   __device__ inline const float* row(int p) const {
     int t = identity ? p - id_base : perm[p] / k;
+    if (tpr) return x + (int64_t)(t / tpr) * rank_stride + (int64_t)(t % tpr) * d;
     return x + (int64_t)t * d;
   }
   __device__ inline void load(const float* r, int c, float* out) const {
@@ -1176,6 +1312,7 @@ __device__ void gate_duty(volatile HostCtrl* hc, DevCtrl* dc, unsigned long long
   if (io.host_done) {  // selection + every scored logits row -> mapped host memory
     for (int f = lane; f < io.n_sel; f += 32) io.host_sel[f] = __ldcg(io.sel_src + f);
     for (int i = lane; i < io.n_pub; i += 32) io.host_logits[i] = __ldcg(io.logits_src + i);
+    if (io.host_mask && lane < 2) io.host_mask[lane] = __ldcg(io.mask_src + lane);
     __threadfence_system();
     __syncwarp();
     if (lane == 0) {
@@ -1472,6 +1609,153 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
   return EF_OK;
 }
 
+
+// ============================================================ expert parallelism
+// Decode step split over G ranks (engine.cu ep_step_on).  Per
+// layer each rank routes its own B tokens, then:
+//   dispatch  ep_pack_kernel writes the rank's routing block
+//             [x B*d | logits Rm*B*M | sel B*k | wts B*k] (4-byte words) and
+//             one all-gather gives every rank every block;
+//   owner     ep_owner_kernel selects the (token, rank) slots routed to the
+//             experts this rank owns, in (local expert, global slot) order —
+//             the stable permutation of the single-GPU route — publishes the
+//             global selection and logits rows to the host for the shard's
+//             scheduler, and builds the home combine index;
+//   FFN       the decode GEMV pair reads the owned slots' x rows straight
+//             from the gathered blocks and writes y in global slot order, which
+//             is already the all-to-all layout (chunk g = rank g's B*k slots);
+//   combine   after the all-to-all, rank-order combine of y rows from their
+//             owners: y[(owner * B + t) * k + r], owner = e * G / M.
+__global__ void ep_pack_kernel(const float* __restrict__ x, const float* __restrict__ logits,
+                               const int32_t* __restrict__ sel, const float* __restrict__ wts,
+                               int64_t nx, int64_t nl, int nk, float* __restrict__ out) {
+  const int64_t n = nx + nl + 2 * (int64_t)nk;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v;
+    if (i < nx) v = x[i];
+    else if (i < nx + nl) v = logits[i - nx];
+    else if (i < nx + nl + nk) v = __int_as_float(sel[i - nx - nl]);
+    else v = wts[i - nx - nl - nk];
+    out[i] = v;
+  }
+}
+
+struct EpOwnerArgs {
+  const float* recv;      // [G][W] gathered routing blocks
+  int64_t W;              // block stride (4-byte words)
+  int G, B, k, M, d, Rm, R, rank, e0, Ms;
+  int32_t* counts;        // [Ms]
+  int32_t* offsets;       // [Ms + 1]
+  int32_t* perm;          // [G*B*k] owned global slots, stable by (local expert, slot)
+  int32_t* home_idx;      // [B*k] y row of each local (token, rank) slot after the all-to-all
+  int32_t* host_sel;      // [G*B*k] mapped
+  float* host_logits;     // [R][G*B][M] mapped
+  volatile uint32_t* host_done;
+};
+
+__global__ void __launch_bounds__(1024) ep_owner_kernel(EpOwnerArgs a) {
+  __shared__ int cnt[kMaxExperts];
+  __shared__ int off[kMaxExperts + 1];
+  const int tid = threadIdx.x;
+  const int N = a.G * a.B * a.k;
+  const int64_t sel_off = (int64_t)a.B * a.d + (int64_t)a.Rm * a.B * a.M;
+  auto sel_of = [&](int f) {  // global slot f = (g*B + t)*k + r
+    const int g = f / (a.B * a.k), rem = f % (a.B * a.k);
+    return __float_as_int(__ldcg(a.recv + (int64_t)g * a.W + sel_off + rem));
+  };
+  for (int j = tid; j < a.Ms; j += blockDim.x) cnt[j] = 0;
+  __syncthreads();
+  for (int f = tid; f < N; f += blockDim.x) {
+    const int e = sel_of(f);
+    if (e >= a.e0 && e < a.e0 + a.Ms) atomicAdd(&cnt[e - a.e0], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int j = 0; j < a.Ms; ++j) {
+      off[j] = run;
+      a.counts[j] = cnt[j];
+      a.offsets[j] = run;
+      run += cnt[j];
+    }
+    a.offsets[a.Ms] = run;
+  }
+  __syncthreads();
+  for (int f = tid; f < N; f += blockDim.x) {
+    const int e = sel_of(f);
+    if (e < a.e0 || e >= a.e0 + a.Ms) continue;
+    int before = 0;  // stable: earlier slots of the same expert
+    for (int f2 = 0; f2 < f; ++f2) before += sel_of(f2) == e;
+    a.perm[off[e - a.e0] + before] = f;
+  }
+  for (int i = tid; i < a.B * a.k; i += blockDim.x) {
+    const int e = __float_as_int(__ldcg(a.recv + (int64_t)a.rank * a.W + sel_off + i));
+    const int o = e * a.G / a.M;
+    a.home_idx[i] = o * a.B * a.k + i;
+  }
+  // publish the global selection and the R scored logits rows of every token
+  if (a.host_sel)
+    for (int f = tid; f < N; f += blockDim.x) a.host_sel[f] = sel_of(f);
+  const int GB = a.G * a.B;
+  for (int64_t i = tid; a.host_logits && i < (int64_t)a.R * GB * a.M; i += blockDim.x) {
+    const int rr = (int)(i / ((int64_t)GB * a.M));
+    const int rem = (int)(i % ((int64_t)GB * a.M));
+    const int tg = rem / a.M, m = rem % a.M;
+    const int g = tg / a.B, t = tg % a.B;
+    a.host_logits[i] =
+        __ldcg(a.recv + (int64_t)g * a.W + (int64_t)a.B * a.d + ((int64_t)rr * a.B + t) * a.M + m);
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) *a.host_done = 1u;
+}
+
+int ep_pack(cudaStream_t st, const float* x, const float* logits, const int32_t* sel,
+            const float* wts, int B, int d, int Rm, int M, int k, float* out) {
+  const int64_t nx = (int64_t)B * d, nl = (int64_t)Rm * B * M;
+  const int64_t n = nx + nl + 2LL * B * k;
+  const int blocks = (int)std::min<int64_t>(148, (n + 255) / 256);
+  ep_pack_kernel<<<blocks, 256, 0, st>>>(x, logits, sel, wts, nx, nl, B * k, out);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+int ep_owner(cudaStream_t st, const float* recv, int64_t W, int G, int B, int k, int M, int d,
+             int Rm, int R, int rank, int e0, int Ms, int32_t* counts, int32_t* offsets,
+             int32_t* perm, int32_t* home_idx, int32_t* host_sel, float* host_logits,
+             uint32_t* host_done) {
+  EF_CHECK_ARG(Ms >= 1 && Ms <= kMaxExperts && M <= kMaxExperts, "bad expert-parallel shard");
+  EpOwnerArgs a{recv, W, G, B, k, M, d, Rm, R, rank, e0, Ms, counts, offsets, perm, home_idx,
+                host_sel, host_logits, host_done};
+  ep_owner_kernel<<<1, 1024, 0, st>>>(a);
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
+// owner-side routed FFN of the expert-parallel step: x rows from the
+// gathered blocks (row stride W floats per rank), y in global slot order
+int expert_ffn_ep(cudaStream_t st, const float* recv, int64_t W, int B, const int32_t* perm, int k,
+                  const char* slab, int64_t stride, const void* dctrl, const uint32_t* ready,
+                  unsigned long long* stats, int max_active, int max_rows, int d, int ff,
+                  int dtype, void* act, float* y) {
+  EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
+  ActiveList al{};
+  CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
+  FuseArgs fd{};
+  fd.y_perm = perm;
+  if (dtype == EF_BF16) {
+    XGather<__nv_bfloat16> xg{recv, perm, k, d, false, 0, B, W};
+    launch_ffn<__nv_bfloat16>(st, al, cs, max_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y,
+                              FuseArgs{}, fd);
+  } else {
+    XGather<float> xg{recv, perm, k, d, false, 0, B, W};
+    launch_ffn<float>(st, al, cs, max_active, max_rows, d, ff, xg, (float*)act, y, FuseArgs{}, fd);
+  }
+  EF_CUDA_RET(cudaGetLastError());
+  return EF_OK;
+}
+
 // Engine pipeline: slots / rows come from the gate-copied DevCtrl at run time.
 int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                     int64_t stride, const void* dctrl, const uint32_t* ready,
@@ -1554,14 +1838,13 @@ int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L) {
 }
 
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
-                         float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
-                         int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
-                         const void* mask_src, int32_t* host_sel, float* host_logits,
+                         float bias, uint64_t mlo, uint64_t mhi, int topup_U, int32_t* sel,
+                         float* wts, int32_t* counts, int32_t* offsets, int32_t* perm,
+                         int32_t* inv, uint64_t* host_mask, int32_t* host_sel, float* host_logits,
                          uint32_t* host_done, unsigned long long* stamp, int n_pub) {
   route_permute_kernel<<<1, kRouteThreads, 0, st>>>(
-      logits, B, M, k, mode, bias, mlo, mhi, sel, wts, counts, offsets, perm, inv,
-      reinterpret_cast<const volatile uint64_t*>(mask_src), host_sel, host_logits, host_done,
-      stamp, n_pub);
+      logits, B, M, k, mode, bias, mlo, mhi, topup_U, sel, wts, counts, offsets, perm, inv,
+      host_mask, host_sel, host_logits, host_done, stamp, n_pub);
   EF_CUDA_RET(cudaGetLastError());
   return EF_OK;
 }
@@ -1703,6 +1986,8 @@ int preload_pipeline_kernels() {
   preload(rmsnorm_kernel, n);
   preload(combine_kernel, n);
   preload(host_io_kernel, n);
+  preload(ep_pack_kernel, n);
+  preload(ep_owner_kernel, n);
   return n;
 }
 }  // namespace ef

@@ -49,10 +49,14 @@ struct GateIO {
   float* host_logits;
   uint32_t* host_done;
   int M;
+  const uint64_t* mask_src;  // the layer's final bias mask (route kernel, after top-up)
+  uint64_t* host_mask;
 };
 struct HostOut {  // followed by sel[B*k] int32 and logits[B*M] f32
   volatile uint32_t done;
-  uint32_t pad[15];
+  uint32_t pad0;
+  uint64_t mask[2];  // final cache-aware bias mask the route kernel selected on
+  uint32_t pad[10];
 };
 
 int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k, bool identity,
@@ -66,9 +70,9 @@ int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long
 int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L);
 int preload_pipeline_kernels();
 int launch_route_publish(cudaStream_t st, const float* logits, int B, int M, int k, int mode,
-                         float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
-                         int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
-                         const void* mask_src, int32_t* host_sel, float* host_logits,
+                         float bias, uint64_t mlo, uint64_t mhi, int topup_U, int32_t* sel,
+                         float* wts, int32_t* counts, int32_t* offsets, int32_t* perm,
+                         int32_t* inv, uint64_t* host_mask, int32_t* host_sel, float* host_logits,
                          uint32_t* host_done, unsigned long long* stamp, int n_pub);
 int router_logits_stamped(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
                           int d, int M, float* logits, unsigned long long* stamp);
@@ -93,7 +97,8 @@ struct CombineIn {
 int launch_host_io(cudaStream_t st, const float* src, float* dst, int64_t n, bool to_host);
 int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype, int R, int B,
                        int d, int M, float* logits, unsigned long long* stamp_router, int k,
-                       int mode, float bias, uint64_t mlo, uint64_t mhi, int32_t* sel, float* wts,
+                       int mode, float bias, uint64_t mlo, uint64_t mhi, int topup_U,
+                       uint64_t* mask_out, uint64_t* host_mask, int32_t* sel, float* wts,
                        int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                        int32_t* host_sel, float* host_logits, uint32_t* host_done,
                        unsigned long long* stamp_route, int* counter,
@@ -103,4 +108,15 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
                      int max_rows, int d, int ff, int dtype, void* act, float* y,
                      const GateIO* io = nullptr);
+// expert parallelism (kernels.cu "expert parallelism" section)
+int ep_pack(cudaStream_t st, const float* x, const float* logits, const int32_t* sel,
+            const float* wts, int B, int d, int Rm, int M, int k, float* out);
+int ep_owner(cudaStream_t st, const float* recv, int64_t W, int G, int B, int k, int M, int d,
+             int Rm, int R, int rank, int e0, int Ms, int32_t* counts, int32_t* offsets,
+             int32_t* perm, int32_t* home_idx, int32_t* host_sel, float* host_logits,
+             uint32_t* host_done);
+int expert_ffn_ep(cudaStream_t st, const float* recv, int64_t W, int B, const int32_t* perm, int k,
+                  const char* slab, int64_t stride, const void* dctrl, const uint32_t* ready,
+                  unsigned long long* stats, int max_active, int max_rows, int d, int ff,
+                  int dtype, void* act, float* y);
 }  // namespace ef

@@ -237,7 +237,11 @@ class Simulator:
 
     def __init__(self, model: ModelSpec, hw: HardwareSpec, policy: PolicyConfig, seed: Seed,
                  forest: Optional[ForestModel] = None, table: Optional[EmbeddingTable] = None,
-                 emit_events: bool = False):
+                 emit_events: bool = False, pregate=None):
+        """``pregate(layer, h) -> probs``: the pre-gate distribution of layer
+        layer + h (default: the reference's synthetic ``pregate_signal`` of the
+        current trace, engine.py:423-426; an expert-parallel shard passes its
+        real router rows, ep.shard_view)."""
         rep = validate(model, hw)
         if not rep.ok:
             raise ValueError("invalid specs: " + "; ".join(rep.violations))
@@ -246,8 +250,7 @@ class Simulator:
             raise ValueError("forest predictor needs a trained model and table")
         self.model, self.policy, self.seed, self.emit_events = model, policy, seed, emit_events
         self._trace: Optional[ActivationTrace] = None
-        pregate = None
-        if policy.predictor in ("pregate", "forest"):
+        if pregate is None and policy.predictor in ("pregate", "forest"):
             def pregate(layer, h):  # engine.py:423-426
                 return pregate_signal(self._trace, layer, h, policy.noise, seed).probs
         self._ladder = _Ladder(L_=model.num_layers, M=model.experts_per_layer, top_k=model.top_k,

@@ -1,28 +1,35 @@
-"""Expert parallelism: expert ownership, token dispatch/combine.
+"""Expert parallelism: ownership, shard shapes, and the
+host side of the expert-parallel decode step.
 
 Expert e of every layer lives on rank ``e * G // M`` (contiguous blocks; for
-Mixtral-8x22B at G=8 one expert per rank per layer).  Per layer each rank
-routes its own tokens, sends every (token, rank-r) row to the expert's owner
-(all-to-all), the owner runs the expert FFN on what it received, and the
-results come back the same way (all-to-all) to be combined in rank order —
-the same deterministic order as the single-GPU combine kernel.
+Mixtral-8x22B at G=8 one expert per rank per layer).  ``MoEEngine(...,
+ep_rank=r, ep_world=G)`` runs the step in C++/CUDA (engine.cu ``ep_step_on``):
+each rank routes its own B tokens, the routing blocks (x, logits, selection,
+weights) are all-gathered, every rank runs its owned experts for all G*B
+tokens from its own slab under its own scheduler, and the outputs return by
+an all-to-all to be combined in rank order — the single-GPU combine's order.
 
-Each rank keeps an independent ExpertCache over the experts it owns (E2), so
-the reference scheduler shards naturally: rank r's decisions equal the oracle
-fed with r's owned-expert access subsequence.
+The collectives are NCCL on the engine's stream (one process per GPU:
+``nccl_unique_id`` on rank 0, broadcast to the others), or a host transport
+(``TorchCollective``: any torch.distributed group, e.g. gloo) so G ranks can
+share one GPU in tests — NCCL refuses two ranks on one device.
 
-The exchange runs on ``torch.distributed`` all_to_all_single: NCCL over
-NVLink on GPUs, gloo on CPU for the multi-process tests.
+Each rank's scheduler sees only its owned experts (local ids 0..M/G-1): the
+batch gate of all G*B tokens restricted to them (``ef_ep_shard_view``), one
+routing group per global token.  The reference scheduler therefore shards
+naturally: rank r's decisions equal the oracle fed with r's view
+(oracle/ep_shard.py).
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-from typing import List, Optional, Sequence, Tuple
+import ctypes as C
+from typing import List, Sequence, Tuple
 
 import numpy as np
-import torch
-import torch.distributed as dist
+
+from . import _lib as L
+from .core import ModelSpec
 
 
 def owner(expert: int, M: int, G: int) -> int:
@@ -34,6 +41,22 @@ def owned_experts(rank: int, M: int, G: int) -> List[int]:
     return [e for e in range(M) if owner(e, M, G) == rank]
 
 
+def shard_model(model: ModelSpec, G: int) -> ModelSpec:
+    """The scheduler shape of one rank: M/G experts per layer, top_k
+    min(k, M/G) (its ladder predicts over its own experts)."""
+    if model.experts_per_layer % G:
+        raise ValueError(f"expert parallelism needs G | M (M={model.experts_per_layer}, G={G})")
+    ms = model.experts_per_layer // G
+    return ModelSpec(model.num_layers, ms, min(model.top_k, ms), model.expert_size_bytes,
+                     model.embed_dim, model.vocab_size)
+
+
+def shard_budget(total_budget: int, M: int, G: int, L: int) -> int:
+    """Per-rank expert-cache capacity for a global budget (E4): the budget
+    split in proportion to the experts each rank owns (equal for G | M)."""
+    return max(1, total_budget * len(owned_experts(0, M, G)) // M)
+
+
 def home_pool_rank(rank: int, G: int) -> int:
     """GPU whose spare HBM holds the home copies of ``rank``'s owned experts
     (the peer-HBM miss tier): the next rank, so a miss never
@@ -43,91 +66,79 @@ def home_pool_rank(rank: int, G: int) -> int:
 
 def peer_pool_ids(rank: int, L: int, M: int, G: int) -> List[int]:
     """Flat expert ids (l*M + e) of every layer's experts owned by ``rank``,
-    in (layer, expert) order: the pool that ``home_pool_rank(rank, G)`` fills
-    and exports, and the ``peer_pool_ids`` the owner's engine opens it with."""
+    in (layer, expert) order: the home copies a single-GPU engine's peer pool
+    holds for that rank's experts.  An expert-parallel engine's own pool uses
+    its local ids (l * M/G + j)."""
     own = owned_experts(rank, M, G)
     return [l * M + e for l in range(L) for e in own]
 
 
-@dataclass
-class DispatchPlan:
-    """Where each (token, rank) row goes, in a canonical order.
-
-    ``order`` lists flat slots f = t*k + r grouped by destination rank, and
-    by f inside a destination, so the exchange is deterministic.
-    """
-    order: np.ndarray          # [B*k] flat slots sorted by (dest, f)
-    send_counts: List[int]     # rows to each rank
-    recv_counts: List[int]     # rows from each rank
-    recv_experts: np.ndarray   # [sum(recv)] global expert id of every received row
-
-
-def plan_dispatch(sel: np.ndarray, M: int, G: int) -> Tuple[np.ndarray, List[int]]:
-    sel = np.asarray(sel)
-    flat = sel.reshape(-1)
-    dest = np.array([owner(int(e), M, G) for e in flat], dtype=np.int64)
-    order = np.lexsort((np.arange(flat.size), dest)).astype(np.int64)
-    counts = [int((dest == r).sum()) for r in range(G)]
-    return order, counts
+def shard_view(logits: np.ndarray, sel: np.ndarray, M: int, k: int, G: int, rank: int
+               ) -> Tuple[np.ndarray, Tuple[Tuple[int, ...], ...], Tuple[int, ...]]:
+    """The shard's view of one layer (ef_ep_shard_view): (gate [M/G] fp64,
+    per-token owned experts as local ids, ascending union)."""
+    lg = np.ascontiguousarray(logits, dtype=np.float32)
+    sl = np.ascontiguousarray(sel, dtype=np.int32)
+    GB = lg.shape[0]
+    ms = M // G
+    gate = np.empty(ms, dtype=np.float64)
+    groups = np.empty((GB, k), dtype=np.int32)
+    actual = np.empty(ms, dtype=np.int32)
+    n = C.c_int32()
+    L.check(L.lib.ef_ep_shard_view(L.as_ptr(lg, C.c_float), L.as_ptr(sl, C.c_int32), GB, M, k, G,
+                                   rank, L.as_ptr(gate, C.c_double), L.as_ptr(groups, C.c_int32),
+                                   L.as_ptr(actual, C.c_int32), C.byref(n)))
+    g = tuple(tuple(int(e) for e in row if e >= 0) for row in groups)
+    return gate, g, tuple(int(e) for e in actual[:n.value])
 
 
-class EPExchange:
-    """all-to-all dispatch / combine of token rows for one process group."""
-
-    def __init__(self, M: int, group=None):
-        self.M = M
-        self.group = group
-        self.G = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-
-    def _a2a(self, t: torch.Tensor, send: List[int], recv: List[int]) -> torch.Tensor:
-        out = torch.empty((sum(recv),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.all_to_all_single(out, t.contiguous(), recv, send, group=self.group)
-        return out
-
-    def dispatch(self, x: torch.Tensor, sel: np.ndarray) -> Tuple[torch.Tensor, DispatchPlan]:
-        """x [B, d] local tokens, sel [B, k] global expert ids ->
-        (rows received for my experts [R, d], plan)."""
-        B, k = np.asarray(sel).shape
-        order, send = plan_dispatch(sel, self.M, self.G)
-        dev = x.device
-        send_t = torch.tensor(send, dtype=torch.int64, device=dev)
-        recv_t = torch.empty_like(send_t)
-        dist.all_to_all_single(recv_t, send_t, group=self.group)
-        recv = [int(v) for v in recv_t.tolist()]
-        rows = x[torch.as_tensor(order // k, device=dev)]
-        experts = torch.as_tensor(np.asarray(sel).reshape(-1)[order], dtype=torch.int64,
-                                  device=dev).reshape(-1, 1)
-        got = self._a2a(rows, send, recv)
-        got_e = self._a2a(experts, send, recv).reshape(-1).cpu().numpy()
-        return got, DispatchPlan(order, send, recv, got_e)
-
-    def combine(self, y_recv: torch.Tensor, plan: DispatchPlan, wts: torch.Tensor,
-                residual: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """Return every processed row to its token's rank and sum in rank
-        order: out[t] = residual[t] + sum_r wts[t, r] * y[t, r]."""
-        back = self._a2a(y_recv, plan.recv_counts, plan.send_counts)
-        B, k = wts.shape
-        y = torch.empty((B * k,) + tuple(back.shape[1:]), dtype=back.dtype, device=back.device)
-        y[torch.as_tensor(plan.order, device=back.device)] = back
-        y = y.reshape(B, k, -1)
-        out = residual.clone() if residual is not None else torch.zeros(
-            B, y.shape[-1], dtype=y.dtype, device=y.device)
-        for r in range(k):  # rank order, like ef_combine
-            out += wts[:, r:r + 1].to(y.dtype) * y[:, r]
-        return out
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id of a new EP group (call on rank 0 only)."""
+    buf = C.create_string_buffer(128)
+    L.check(L.lib.ef_ep_nccl_unique_id(buf))
+    return buf.raw
 
 
-def local_groups(recv_experts: np.ndarray) -> List[Tuple[int, np.ndarray]]:
-    """(expert, row indices) for the rows a rank received, experts ascending,
-    rows in arrival order (stable)."""
-    out = []
-    for e in sorted(set(int(v) for v in recv_experts)):
-        out.append((e, np.nonzero(recv_experts == e)[0]))
-    return out
+def nccl_group_id(group=None) -> bytes:
+    """The NCCL id of an EP group, agreed over a torch.distributed group."""
+    import torch.distributed as dist
+    box = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return box[0]
 
 
-def shard_budget(total_budget: int, M: int, G: int, L: int) -> int:
-    """Per-rank expert-cache capacity for a global budget (E4): the budget
-    split in proportion to the experts each rank owns (equal for G | M)."""
-    return max(1, total_budget * len(owned_experts(0, M, G)) // M)
+class TorchCollective:
+    """Host transport of the EP collectives over a torch.distributed group
+    (``MoEEngine(..., ep_collective=TorchCollective(group))``): the device
+    buffers are staged through host memory and exchanged with the group's
+    backend (gloo in the multi-process tests, several ranks per GPU)."""
+
+    def __init__(self, group=None, device=0):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.world = dist.get_world_size(group)
+        self.device = torch.device("cuda", device)
+        self.calls = 0
+
+    def _view(self, ptr: int, nbytes: int):
+        from .runtime import _raw_device_view
+        return _raw_device_view(ptr, nbytes, self.device)
+
+    def __call__(self, op: int, send: int, recv: int, nbytes: int, stream: int) -> None:
+        torch, dist = self.torch, self.dist
+        torch.cuda.synchronize(self.device)  # the engine's stream has produced `send`
+        G = self.world
+        if op == 0:  # all-gather: recv[g] = rank g's send
+            src = self._view(send, nbytes).cpu()
+            out = torch.empty(G * nbytes, dtype=torch.uint8)
+            dist.all_gather(list(out.view(G, nbytes).unbind(0)), src, group=self.group)
+        elif op == 1:  # all-to-all: recv[g] = rank g's send[me]
+            src = self._view(send, G * nbytes).cpu()
+            out = torch.empty(G * nbytes, dtype=torch.uint8)
+            dist.all_to_all_single(out, src, group=self.group)
+        else:
+            raise ValueError(f"unknown collective op {op}")
+        self._view(recv, G * nbytes).copy_(out)
+        torch.cuda.synchronize(self.device)
+        self.calls += 1

@@ -45,7 +45,9 @@ class MoEEngine:
                  device: int = 0, max_prefill: int = 0, host_store_shm: Optional[str] = None,
                  host_store_attach: bool = False, peer_device: Optional[int] = None,
                  peer_pool_experts: int = 0, peer_ipc_handle: Optional[bytes] = None,
-                 peer_pool_ids: Optional[Sequence[int]] = None):
+                 peer_pool_ids: Optional[Sequence[int]] = None, ep_rank: int = 0,
+                 ep_world: int = 0, ep_nccl_id: Optional[bytes] = None,
+                 ep_collective=None):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
@@ -53,7 +55,16 @@ class MoEEngine:
         self.max_prefill = max_prefill
         self.emit_events = emit_events
         self.device = torch.device("cuda", device)
-        model = cfg.model_spec()
+        # expert parallelism: this engine is rank ep_rank of
+        # ep_world and schedules only its owned experts (ep.shard_model);
+        # budget_experts is the shard's budget (ep.shard_budget)
+        self.ep_world, self.ep_rank = int(ep_world), int(ep_rank)
+        if self.ep_world:
+            from .ep import shard_model
+            model = shard_model(cfg.model_spec(), self.ep_world)
+        else:
+            model = cfg.model_spec()
+        self.sched_model = model
         hw = HardwareSpec(int(link_bw), int(budget_experts) * cfg.expert_bytes, float(layer_time_s))
         policy.check(model)
         if policy.predictor == "oracle":
@@ -61,7 +72,7 @@ class MoEEngine:
         if policy.predictor == "forest" and (forest is None or table is None):
             raise ValueError("forest predictor needs a trained model and table")
         self.hw = hw
-        self._ladder = _Ladder(L_=cfg.num_layers, M=cfg.num_experts, top_k=cfg.top_k,
+        self._ladder = _Ladder(L_=cfg.num_layers, M=model.experts_per_layer, top_k=model.top_k,
                                cum_threshold=policy.cum_threshold,
                                forest=forest if policy.predictor == "forest" else None,
                                table=table if policy.predictor == "forest" else None)
@@ -76,7 +87,8 @@ class MoEEngine:
         # landing slot for the one in-flight transfer + slots pinned by the
         # current layer after an in-layer eviction
         ec.staging_slots = staging_slots or (
-            2 + min(max(max_batch, max_prefill) * cfg.top_k, cfg.num_experts))
+            2 + min(max(max_batch, max_prefill) * cfg.top_k * max(1, self.ep_world),
+                    model.experts_per_layer))
         ec.routing_bias = routing_bias
         ec.seed = seed
         ec.device = device
@@ -109,6 +121,26 @@ class MoEEngine:
                 raise ValueError("peer_ipc_handle must be the 64-byte handle of peer_pool_handle()")
             self._peer_ipc = C.create_string_buffer(bytes(peer_ipc_handle), 64)
             ec.peer_ipc_handle = C.cast(self._peer_ipc, L.vp)
+        ec.ep_world, ec.ep_rank = self.ep_world, self.ep_rank
+        self._ep_id = None
+        if ep_nccl_id is not None:
+            if len(ep_nccl_id) != 128:
+                raise ValueError("ep_nccl_id must be the 128-byte id of ep.nccl_unique_id()")
+            self._ep_id = C.create_string_buffer(bytes(ep_nccl_id), 128)
+            ec.ep_nccl_id = C.cast(self._ep_id, L.vp)
+        self._ep_cb = None
+        if ep_collective is not None:
+            # ep_collective(op, send_ptr, recv_ptr, nbytes, stream_ptr): a host
+            # transport (ep.TorchCollective); exceptions surface from step()
+            def _cb(user, op, send, recv, nbytes, stream):
+                try:
+                    ep_collective(int(op), send or 0, recv or 0, int(nbytes), stream or 0)
+                    return 0
+                except BaseException as exc:  # noqa: BLE001 - re-raised after the C call
+                    L._pending_exc.append(exc)
+                    return -1
+            self._ep_cb = L.COLLECTIVE_CB(_cb)
+            ec.ep_collective = self._ep_cb
         torch.cuda.set_device(device)
         torch.cuda.init()
         h = L.vp()
@@ -125,7 +157,7 @@ class MoEEngine:
         the same slab, weights and pinned host store: the cache is emptied as
         in a new engine, the routing log cleared; ``stats()`` counters keep
         accumulating.  The prediction ladder's threshold and forest stay."""
-        model = self.cfg.model_spec()
+        model = self.sched_model
         policy.check(model)
         if policy.predictor == "oracle":
             raise ValueError("the oracle predictor needs future routing; use simulate()")

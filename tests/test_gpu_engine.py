@@ -114,7 +114,7 @@ def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feat
         i = cur["t"] * L + layer
         lg = log[i][0]
         mask = N.routing_mask([(layer + h, e) in cache for e in range(M)], M, cfg.top_k, budget,
-                              L, mask_tokens[i]) if bias else 0
+                              L, mask_tokens[i], lg[h]) if bias else 0
         return N.batch_gate(lg[h], bias, mask)
 
     st = OracleStepper(num_layers=L, experts_per_layer=cfg.num_experts, top_k=cfg.top_k,
@@ -130,7 +130,7 @@ def _replay(log, cfg, budget, link_bw, layer_s, policy, toks, bias, forest, feat
         i = cur["t"] * L + layer
         logits, sel, mask = log[i]
         want = N.routing_mask([(layer, e) in resident for e in range(M)], M, cfg.top_k, budget, L,
-                              mask_tokens[i]) if bias else 0
+                              mask_tokens[i], logits[0]) if bias else 0
         if mask != want:
             mask_bad.append((cur["t"], layer))
         res = N.mask_bits(want, M)
@@ -161,9 +161,22 @@ def test_tiny_f32_engine_parity(policy):
                   layer_s=0.0002)
 
 
-def test_tiny_bf16_batch32_engine_parity():
+@pytest.mark.parametrize("bias", [0.0, 1e4])
+def test_tiny_bf16_batch32_engine_parity(bias):
+    """B = 32 (the general route kernel and counting sort); with the
+    residency bias the mask is topped up by router votes on the device."""
     run_and_check(PRESETS["tiny-bf16"], ef.PolicyConfig("a", "adaptive", predictor="pregate"),
-                  B=32, steps=2, budget=12, link_bw=ef.GB, layer_s=0.0003)
+                  B=32, steps=3, budget=12, link_bw=ef.GB, layer_s=0.0003, bias=bias)
+
+
+def test_qwen_shape_batch32_topup_parity():
+    """Qwen expert shape at B = 32 with the residency bias: the top-up by
+    router votes (kernels.cu topup_mask) is bit-exact with the oracle's rule,
+    including the pre-gate rows' masks on the host (engine.cu scored_mask)."""
+    cfg = MoEConfig("qwen-3l", 3, 60, 4, 2048, 1408, route_mode="softmax_topk", shared_ff=5632,
+                    shared_gate=True)
+    run_and_check(cfg, ef.PolicyConfig("a", "adaptive", predictor="pregate"), B=32, steps=3,
+                  budget=72, link_bw=50 * ef.GB, layer_s=5e-5, bias=1e4)
 
 
 def test_cache_aware_bias_engine_parity():

@@ -29,20 +29,24 @@ def test_compare_engines_validates_policies():
 
 
 def test_engine_cfg_struct_matches_header():
-    """ef_engine_cfg in include/expertflow.h and the ctypes mirror agree on
-    field order (the last fields were appended for prefill and the shared
-    host store)."""
-    names = [f[0] for f in L.EngineCfg._fields_]
-    assert names[-7:] == ["max_prefill", "host_store_shm", "host_store_attach", "peer_device",
-                          "peer_pool_experts", "peer_pool_ids", "peer_ipc_handle"]
-    hdr = open(__import__("os").path.join(__import__("os").path.dirname(__file__), "..",
-                                          "include", "expertflow.h")).read()
-    body = hdr[hdr.index("typedef struct ef_engine_cfg"):hdr.index("} ef_engine_cfg;")]
-    pos = [body.index(n) for n in ("record_routing", "max_prefill", "host_store_shm",
-                                   "host_store_attach", "peer_device", "peer_pool_experts",
-                                   "peer_pool_ids", "peer_ipc_handle")]
-    assert pos == sorted(pos)
-    assert C.sizeof(L.EngineCfg) >= 96
+    """ef_engine_cfg in include/expertflow.h and the ctypes mirror declare the
+    same fields in the same order."""
+    import os
+    import re
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "expertflow.h")).read()
+    body = hdr[hdr.index("typedef struct ef_engine_cfg {") + len("typedef struct ef_engine_cfg {"):
+               hdr.index("} ef_engine_cfg;")]
+    body = re.sub(r"/\*.*?\*/", " ", body, flags=re.S)
+    names = []
+    for stmt in body.split(";"):
+        stmt = stmt.replace("*", " ").strip()
+        if not stmt:
+            continue
+        chunks = stmt.split(",")
+        names.append(chunks[0].split()[-1])
+        names += [c.strip() for c in chunks[1:]]
+    assert names == [f[0] for f in L.EngineCfg._fields_]
+    assert names[-5:] == ["ep_world", "ep_rank", "ep_nccl_id", "ep_collective", "ep_user"]
 
 
 def test_new_entry_points_exported():
@@ -58,9 +62,14 @@ def test_bench_reference_arm_contract():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
-                          "--config", "tiny", "--steps", "1", "--warmup", "0"],
-                         capture_output=True, text=True, timeout=300, cwd=root)
+    # run the arm in-process of a child that reports whether the product
+    # library was ever mapped (the reference arm must not load it)
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', "
+            "'tiny', '--steps', '2', '--warmup', '1']; runpy.run_path('bench.py', "
+            "run_name='__main__'); print('MAPPED', any('libexpertflow' in l "
+            "for l in open('/proc/self/maps')), 'TORCH', 'torch' in sys.modules)")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=300, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
@@ -70,19 +79,30 @@ def test_bench_reference_arm_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["reference_scheduler_us_per_layer"] > 0
+    assert "MAPPED False TORCH False" in out.stdout, out.stdout[-500:]
 
 
 def test_routing_mask_top_up_rule():
     """Cache-aware routing mask (oracle/numerics.py routing_mask, engine.cu
-    residency_mask): residents only, unless the batch could exceed the layer's
-    cache share (ntok*k > U) and fewer than k experts are resident; then the
-    lowest-index non-resident experts top it up to U = max(k, budget // L)."""
+    residency_mask + kernels.cu topup_mask): residents only, unless the batch
+    could exceed the layer's cache share (ntok*k > U) and fewer than k experts
+    are resident; then the non-residents with the most unbiased top-k votes
+    (ties: larger max logit, then lower index) top it up to U = max(k, budget // L)."""
+    import numpy as np
     from oracle import numerics as N
     M, k, L, budget = 8, 2, 4, 12  # U = 3
+    lg = np.array([[0.1, 0.9, 0.0, 0.8, 0.2, 0.0, 0.0, 0.0],
+                   [0.0, 0.7, 0.0, 0.1, 0.0, 0.0, 0.6, 0.0]], dtype=np.float32)
+    # votes: e1 = 2, e3 = 1, e6 = 1 (max logit 0.8 vs 0.6)
     res = [False, False, True, False, False, False, False, False]
-    assert N.routing_mask(res, M, k, budget, L, 1) == 1 << 2          # 1*2 <= 3: residents only
-    assert N.routing_mask(res, M, k, budget, L, 2) == 0b111           # top up to 3 experts
+    assert N.routing_mask(res, M, k, budget, L, 1, lg[:1]) == 1 << 2          # 1*2 <= 3
+    assert N.routing_mask(res, M, k, budget, L, 2, lg) == (1 << 2) | (1 << 1) | (1 << 3)
+    none = [False] * M
+    assert N.routing_mask(none, M, k, budget, L, 2, lg) == (1 << 1) | (1 << 3) | (1 << 6)
     two = [True, False, False, True, False, False, False, False]
-    assert N.routing_mask(two, M, k, budget, L, 32) == 0b1001         # k resident: no top-up
-    assert N.routing_mask([False] * M, M, k, 0, L, 32) == 0b11        # U = k when budget < L
+    assert N.routing_mask(two, M, k, budget, L, 32, lg) == 0b1001         # k resident: no top-up
+    assert N.routing_mask(none, M, k, 0, L, 32, lg) == (1 << 1) | (1 << 3)  # U = k
+    tie = np.zeros((2, M), dtype=np.float32)                              # all equal: index order
+    assert N.routing_mask(none, M, k, budget, L, 2, tie) == 0b111
     assert N.mask_bits(0b101, 4).tolist() == [True, False, True, False]
