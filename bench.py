@@ -540,6 +540,12 @@ def run_ours(args, cfg, bias):
             "hit_rate": _rate(m1.hits - m0.hits, m1.misses - m0.misses),
             "copies_per_step": (st1["copies"] - st0["copies"]) / K,
             "h2d_GBps": h2d_GBps,
+            "bandwidth_estimate_GBps": {"logical": m1.bandwidth_estimate / 1e9,
+                                        "physical": st1["bw_physical_Bps"] / 1e9,
+                                        "physical_transfers": int(st1["bw_physical_transfers"]),
+                                        "what": "EWMA (alpha 0.25) of the scheduler's logical "
+                                                "transfers / of the copy engine's measured "
+                                                "expert copies (copy-stream events)"},
             "host_decision_us_per_layer": 1e3 * (st1["host_decision_ms"] - st0["host_decision_ms"])
             / (K * cfg.num_layers),
             "gate_wait_us_per_layer": 1e3 * (st1["gate_wait_ms"] - st0["gate_wait_ms"])

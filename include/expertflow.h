@@ -189,6 +189,11 @@ typedef struct ef_sim_cfg {
   int32_t prediction_cache_capacity;
   int32_t emit_events;
   uint64_t seed;
+  /* 1: bandwidth feedback into S: each adaptive boundary re-bases
+     the step on the current bandwidth estimate — the logical EWMA in ef_sim, the
+     copy engine's measured transfer times in ef_engine.  0 (parity mode): S is
+     computed once, as the reference does (engine.py:545-556). */
+  int32_t bw_feedback;
 } ef_sim_cfg;
 int ef_sim_create(const ef_sim_cfg* cfg, const ef_ladder_cfg* ladder, ef_sim** out);
 void ef_sim_destroy(ef_sim* s);
@@ -387,7 +392,9 @@ int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len, int64_t* n
    fast_layers (layers whose routed FFN started from the device-side slot table,
    without waiting for the host), peer_copies, peer_bytes (swap-ins served by the
    peer-HBM tier), prefetch_admitted / prefetch_used / prefetch_wasted (experts admitted
-   by a PREFETCH transfer; routed to by a later layer before eviction; evicted unused) */
+   by a PREFETCH transfer; routed to by a later layer before eviction; evicted unused),
+   bw_physical_Bps (EWMA, alpha 0.25, of the measured expert-copy rates; copy-stream
+   events), bw_physical_transfers (copies folded into it) */
 int ef_engine_stats(ef_engine* e, double* out, int n);
 /* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
    6 perm, 7 inv, 8 y, 9 x */

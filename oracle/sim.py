@@ -121,7 +121,8 @@ class OracleStepper:
     def __init__(self, *, num_layers, experts_per_layer, top_k, expert_size_bytes,
                  link_bw, device_memory_bytes, layer_compute_ns, policy: Policy,
                  seed_value: int = 0, emit_events=False, forest=None,
-                 features_fn=None, pregate_fn: Optional[Callable] = None):
+                 features_fn=None, pregate_fn: Optional[Callable] = None,
+                 bandwidth_feedback: bool = False):
         self.L, self.M, self.k = num_layers, experts_per_layer, top_k
         self.E_s = expert_size_bytes
         self.bw = link_bw
@@ -133,6 +134,7 @@ class OracleStepper:
         # pregate_fn(token_trace, layer, h) -> fp64 probs; None -> the
         # reference's synthetic pregate_signal (engine.py:423-426).
         self.pregate_fn = pregate_fn
+        self.bandwidth_feedback = bandwidth_feedback
         self.layer_ns = layer_compute_ns                       # engine.py:263
         if self.layer_ns < 1:
             raise ValueError("layer compute time rounds below 1 ns")
@@ -295,6 +297,14 @@ class OracleStepper:
             if layer % self.policy.interval == 0:
                 self._issue_horizon(tt, layer, self.policy.interval)
         elif layer == self.next_boundary:
+            if self.bandwidth_feedback and self.state is not None:
+                # flagged feedback (not in the reference, whose S is
+                # computed once, engine.py:545-556): re-base S on the current
+                # estimate at every adaptive boundary
+                pol = self.policy
+                n_e = D.expected_expert_count(tt.gates[layer], pol.cum_threshold)
+                self.state.current = D.compute_step(n_e, self.E_s, self.estimator.estimate,
+                                                    self.layer_ns, pol.min_step, self.max_step)
             step = self.state.current
             self._issue_horizon(tt, layer, step)
             self.next_boundary = layer + step

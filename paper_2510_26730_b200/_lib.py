@@ -55,7 +55,8 @@ class SimCfg(C.Structure):
                 ("cache_aware_routing", i32), ("cold_start_preload", i32),
                 ("cum_threshold", f64), ("stall_threshold", i32), ("overfetch_threshold", i32),
                 ("min_step", i32), ("max_step", i32), ("recent_window", i32),
-                ("prediction_cache_capacity", i32), ("emit_events", i32), ("seed", u64)]
+                ("prediction_cache_capacity", i32), ("emit_events", i32), ("seed", u64),
+                ("bw_feedback", i32)]
 
 
 class EngineCfg(C.Structure):

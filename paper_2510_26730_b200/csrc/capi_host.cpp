@@ -402,6 +402,7 @@ SimConfig sim_config_from(const ef_sim_cfg* c) {
   s.device_memory = c->device_memory_bytes;
   s.layer_ns = c->layer_ns;
   s.emit_events = c->emit_events != 0;
+  s.bw_feedback = c->bw_feedback != 0;
   Policy& p = s.policy;
   p.strategy = c->strategy;
   p.predictor = c->predictor;
@@ -429,6 +430,10 @@ extern "C" int ef_sim_create(const ef_sim_cfg* cfg, const ef_ladder_cfg* ladder,
     if (sc.policy.predictor == 2 && (!s->hooks->has_forest() || !ladder->table))
       throw ValueError("forest predictor needs a trained model and table");
     s->st = std::make_unique<Stepper>(sc, s->hooks.get());
+    if (sc.bw_feedback) {
+      Stepper* st = s->st.get();
+      st->set_bw_feedback([st] { return st->logical_bw_estimate(); });
+    }
     s->L = cfg->L;
     s->M = cfg->M;
     *out = s.release();

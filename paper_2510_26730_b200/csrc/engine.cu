@@ -154,6 +154,9 @@ struct ef_engine {
     return 1 + std::min(pol_max, cfg.L - 1);
   }
   void reset(const SimConfig& sc, float bias);
+  void install_bw_feedback() {
+    if (simcfg.bw_feedback) st->set_bw_feedback([this] { return phys_bw->estimate(); });
+  }
   // ---- expert parallelism (ef_engine_cfg.ep_world > 0; kernels.cu
   // "expert parallelism"): rank ep_rank of G owns experts [e0, e0 + Ms)
   bool ep = false;
@@ -342,6 +345,47 @@ struct ef_engine {
     return reinterpret_cast<T*>(hout_dev + (reinterpret_cast<char*>(host_mapped) - hout));
   }
 
+  // Physical bandwidth of the copy engine: every blob copy is
+  // bracketed by two events on the copy stream; completed pairs are folded
+  // into an EWMA (alpha 0.25, memory.py:205-236) at each layer decision.  With
+  // ef_sim_cfg.bw_feedback the adaptive controller re-bases S on it
+  // (PAPER.md:307); otherwise it is reported only.
+  struct CopyTiming {
+    cudaEvent_t a, b;
+    int64_t bytes;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  std::deque<CopyTiming> ev_pending;
+  std::unique_ptr<BandwidthEstimator> phys_bw;
+  int64_t phys_observed = 0;
+  cudaEvent_t take_event() {
+    if (ev_pool.empty()) {
+      cudaEvent_t ev;
+      CK(cudaEventCreate(&ev));
+      return ev;
+    }
+    cudaEvent_t ev = ev_pool.back();
+    ev_pool.pop_back();
+    return ev;
+  }
+  void poll_copy_times() {
+    while (!ev_pending.empty()) {
+      CopyTiming& c = ev_pending.front();
+      if (cudaEventQuery(c.b) != cudaSuccess) {
+        cudaGetLastError();
+        break;
+      }
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, c.a, c.b) == cudaSuccess && ms > 0.f) {
+        phys_bw->observe(c.bytes, std::max<int64_t>(1, (int64_t)std::llround(ms * 1e6)));
+        ++phys_observed;
+      }
+      ev_pool.push_back(c.a);
+      ev_pool.push_back(c.b);
+      ev_pending.pop_front();
+    }
+  }
+
   void issue_copy(uint64_t key, bool preload) {
     // A free slot's previous readers have all completed (see the header).
     if (free_slots.empty())
@@ -349,6 +393,12 @@ struct ef_engine {
     int s = free_slots.front();
     free_slots.pop_front();
     const int64_t flat = idx(key);
+    CopyTiming ct{nullptr, nullptr, stride};
+    if (ev_pending.size() < 4096) {
+      ct.a = take_event();
+      ct.b = take_event();
+      CK(cudaEventRecord(ct.a, copy_stream));
+    }
     const int64_t ps = peer_n ? pool_slot_of[flat] : -1;
     if (ps >= 0) {
       // miss served from the peer's HBM over NVLink (copy engine, same stream,
@@ -361,6 +411,10 @@ struct ef_engine {
       const char* src = store[eid_layer(key)] + (int64_t)eid_expert(key) * stride;
       CK(cudaMemcpyAsync(slab + (int64_t)s * stride, src, stride, cudaMemcpyHostToDevice,
                          copy_stream));
+    }
+    if (ct.a) {
+      CK(cudaEventRecord(ct.b, copy_stream));
+      ev_pending.push_back(ct);
     }
     uint32_t seq = ++copy_seq;
     // Publish the fill sequence with the copy engine (a 4-byte H2D copy from a
@@ -647,6 +701,8 @@ ef_engine::~ef_engine() {
       if (p) cudaFreeHost(p);
   }
   if (xrec_h) cudaFreeHost(xrec_h);
+  for (auto& c : ev_pending) ev_pool.insert(ev_pool.end(), {c.a, c.b});
+  for (cudaEvent_t ev : ev_pool) cudaEventDestroy(ev);
   for (void* p : {(void*)ep_send, (void*)ep_recv, (void*)ep_yslots, (void*)ep_yrecv,
                   (void*)ep_counts, (void*)ep_offsets, (void*)ep_perm, (void*)ep_home, ep_act})
     if (p) cudaFree(p);
@@ -941,6 +997,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
           pf_pending[(int64_t)l * M + e] = 0;
           ++pf_used;
         }
+      poll_copy_times();
       if (l == 0) st->begin_token(tokens, gsizes, r);
       std::fill(layer_use.begin(), layer_use.end(), -1);
       st->begin_layer(l);
@@ -1138,6 +1195,7 @@ void ef_engine::ep_step_on(cudaStream_t stream, float* h, int B,
         pf_pending[(int64_t)l * Ms + j] = 0;
         ++pf_used;
       }
+    poll_copy_times();
     if (l == 0) st->begin_token(tokens, gsizes, r);
     std::fill(layer_use.begin(), layer_use.end(), -1);
     st->begin_layer(l);
@@ -1318,6 +1376,7 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
                                 cur_mask[0], cur_mask[1], record_x(px_d, (int64_t)T * d),
                                 mask_tokens});
     }
+    poll_copy_times();
     if (l == 0) st->begin_token(tokens, gsizes, r);
     std::fill(layer_use.begin(), layer_use.end(), -1);
     st->begin_layer(l);
@@ -1419,6 +1478,7 @@ void ef_engine::reset(const SimConfig& sc, float bias) {
   simcfg = sc;
   st = std::make_unique<Stepper>(simcfg, hooks.get());
   st->set_observer(&mirror);
+  install_bw_feedback();
   if ((int64_t)P < st->cache().capacity() + 1)
     throw ValueError("reset: the new budget exceeds the engine's physical slots");
   cfg.routing_bias = bias;
@@ -1485,6 +1545,8 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->st = std::make_unique<Stepper>(e->simcfg, e->hooks.get());
     e->mirror.e = e.get();
     e->st->set_observer(&e->mirror);
+    e->phys_bw = std::make_unique<BandwidthEstimator>(true, (double)e->simcfg.link_bw, 0.25);
+    e->install_bw_feedback();
     int64_t cap = e->st->cache().capacity();
     e->P = (int)(cap + c.staging_slots);
     e->Rmax = e->rows_for_policy();
@@ -1698,7 +1760,8 @@ extern "C" int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len,
 extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   EF_TRY({
     e->flush_stats();
-    double v[22] = {(double)e->steps,         (double)e->copies,
+    e->poll_copy_times();
+    double v[24] = {(double)e->steps,         (double)e->copies,
                     (double)e->copy_bytes,    e->stall_ms,
                     (double)e->P,             (double)e->st->cache().capacity(),
                     (double)e->cfg.staging_slots, (double)e->launches,
@@ -1708,8 +1771,9 @@ extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
                     (double)e->ffn_launches,  e->bubble_ms,
                     (double)e->fast_layers,   (double)e->peer_copies,
                     (double)e->peer_bytes,    (double)e->pf_admitted,
-                    (double)e->pf_used,       (double)e->pf_wasted};
-    for (int i = 0; i < n && i < 22; ++i) out[i] = v[i];
+                    (double)e->pf_used,       (double)e->pf_wasted,
+                    e->phys_bw->estimate(),   (double)e->phys_observed};
+    for (int i = 0; i < n && i < 24; ++i) out[i] = v[i];
   });
 }
 

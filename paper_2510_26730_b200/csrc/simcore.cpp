@@ -720,6 +720,12 @@ void Stepper::boundary(int layer) {
   } else if (p.strategy == 2) {
     if (layer % p.interval == 0) issue_horizon(layer, p.interval);
   } else if (layer == next_boundary_) {
+    if (bw_src_ && has_state_) {
+      const Policy& pp = cfg_.policy;
+      const int n_e = expected_expert_count(seen_[layer].gate.data(), cfg_.M, pp.cum_threshold);
+      state_.current = compute_step_float(n_e, cfg_.expert_size, bw_src_(), cfg_.layer_ns,
+                                          pp.min_step, max_step_);
+    }
     int step = state_.current;
     issue_horizon(layer, step);
     next_boundary_ = layer + step;  // unclipped (Appendix A Q7)

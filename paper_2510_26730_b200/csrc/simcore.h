@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <deque>
+#include <functional>
 #include <list>
 #include <map>
 #include <memory>
@@ -24,6 +25,7 @@
 #include <string>
 #include <unordered_map>
 #include <utility>
+#include <functional>
 #include <vector>
 
 namespace ef {
@@ -218,6 +220,7 @@ struct SimConfig {
   int L = 1, M = 1, top_k = 1;
   int64_t expert_size = 1, link_bw = 1, device_memory = 1, layer_ns = 1;
   bool emit_events = false;
+  bool bw_feedback = false;  // ef_sim_cfg.bw_feedback
   Policy policy;
 };
 
@@ -304,6 +307,15 @@ class Stepper {
   const std::vector<SampleRec>& samples() const { return samples_; }
   std::vector<SimEventRec> sorted_events() const;
   void set_observer(Observer* o) { obs_ = o; }
+  // Bandwidth feedback into S ("observed transfer times update
+  // the bandwidth estimate C_s, informing subsequent skip-distance
+  // calculations"; the reference computes S once, engine.py:545-556, and never
+  // feeds its EWMA back — SURVEY Appendix A Q2).  When a source is set, every
+  // adaptive boundary re-bases the step: S = compute_step(N_e(this layer's
+  // gate), E_s, source(), T_l, min, max), then stall / overfetch feedback
+  // continues from it.  Off by default (parity mode).
+  void set_bw_feedback(std::function<double()> src) { bw_src_ = std::move(src); }
+  double logical_bw_estimate() const { return estimator_.estimate(); }
   void set_oracle_future(const std::vector<LayerRouting>* f) { oracle_future_ = f; }
   int64_t clock() const { return clock_; }
   int64_t per_expert_ns() const { return per_expert_ns_; }
@@ -313,6 +325,7 @@ class Stepper {
 
  private:
   std::vector<uint64_t> hot_scratch_;
+  std::function<double()> bw_src_;
   struct Inflight {
     uint64_t key;
     int prio;

@@ -237,7 +237,7 @@ class Simulator:
 
     def __init__(self, model: ModelSpec, hw: HardwareSpec, policy: PolicyConfig, seed: Seed,
                  forest: Optional[ForestModel] = None, table: Optional[EmbeddingTable] = None,
-                 emit_events: bool = False, pregate=None):
+                 emit_events: bool = False, pregate=None, bandwidth_feedback: bool = False):
         """``pregate(layer, h) -> probs``: the pre-gate distribution of layer
         layer + h (default: the reference's synthetic ``pregate_signal`` of the
         current trace, engine.py:423-426; an expert-parallel shard passes its
@@ -260,6 +260,9 @@ class Simulator:
                                pregate=pregate)
         h = L.vp()
         self._cfg = policy.to_c(model, hw, seed, emit_events)
+        # bandwidth feedback into S from the logical EWMA; the
+        # reference computes S once (engine.py:545-556): off = parity
+        self._cfg.bw_feedback = int(bandwidth_feedback)
         L.check(L.lib.ef_sim_create(C.byref(self._cfg), C.byref(self._ladder.cfg), C.byref(h)))
         self._h = L.Handle(h.value, L.lib.ef_sim_destroy)
 

@@ -47,7 +47,7 @@ class MoEEngine:
                  peer_pool_experts: int = 0, peer_ipc_handle: Optional[bytes] = None,
                  peer_pool_ids: Optional[Sequence[int]] = None, ep_rank: int = 0,
                  ep_world: int = 0, ep_nccl_id: Optional[bytes] = None,
-                 ep_collective=None):
+                 ep_collective=None, bandwidth_feedback: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
@@ -77,6 +77,9 @@ class MoEEngine:
                                forest=forest if policy.predictor == "forest" else None,
                                table=table if policy.predictor == "forest" else None)
         sim = policy.to_c(model, hw, Seed(seed), emit_events)
+        # physical bandwidth feedback into S; off = parity mode
+        self.bandwidth_feedback = bool(bandwidth_feedback)
+        sim.bw_feedback = int(self.bandwidth_feedback)
         ec = L.EngineCfg()
         ec.L, ec.M, ec.top_k = cfg.num_layers, cfg.num_experts, cfg.top_k
         ec.d, ec.ff, ec.dtype = cfg.d_model, cfg.d_ff, DTYPES[cfg.dtype]
@@ -166,6 +169,7 @@ class MoEEngine:
             raise ValueError("reset keeps the engine's prediction ladder: same cum_threshold "
                              "and forest use required")
         sim = policy.to_c(model, self.hw, Seed(self._seed), self.emit_events)
+        sim.bw_feedback = int(self.bandwidth_feedback)
         L._pending_exc.clear()
         L.check(L.lib.ef_engine_reset(self._h.ptr, C.byref(sim), float(routing_bias)))
         self._sim = sim
@@ -267,7 +271,7 @@ class MoEEngine:
                 "staging_slots", "kernel_launches", "host_decision_ms", "ffn_ms", "step_ms",
                 "preload_copies", "d2h_bytes", "ffn_bytes", "ffn_launches", "gate_wait_ms",
                 "fast_layers", "peer_copies", "peer_bytes", "prefetch_admitted", "prefetch_used",
-                "prefetch_wasted"]
+                "prefetch_wasted", "bw_physical_Bps", "bw_physical_transfers"]
         out = (C.c_double * len(keys))()
         L.check(L.lib.ef_engine_stats(self._h.ptr, out, len(keys)))
         return dict(zip(keys, list(out)))

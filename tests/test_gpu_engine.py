@@ -559,3 +559,23 @@ def test_reset_equals_fresh_engine():
     assert a.metrics() == b.metrics()
     with pytest.raises(ValueError):
         a.reset(ef.PolicyConfig("a", "adaptive", predictor="pregate", cum_threshold=0.5))
+
+
+def test_physical_bandwidth_estimate_and_feedback():
+    """A13: the copy engine's measured transfer rates feed an EWMA next to the
+    logical one; with bandwidth_feedback the adaptive controller re-bases S
+    on it.  Off (default) keeps the reference's decisions."""
+    cfg = PRESETS["tiny-bf16"]
+    kw = dict(budget_experts=12, policy=ef.PolicyConfig("a", "adaptive", predictor="pregate"),
+              link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2, seed=8)
+    a = MoEEngine(cfg, **kw)
+    b = MoEEngine(cfg, bandwidth_feedback=True, **kw)
+    for t in range(6):
+        a.step(synthetic_hidden(cfg, 8, t, 2, DEV))
+        b.step(synthetic_hidden(cfg, 8, t, 2, DEV))
+    torch.cuda.synchronize()
+    sa, sb = a.stats(), b.stats()
+    assert sa["bw_physical_transfers"] > 0 and sb["bw_physical_transfers"] > 0
+    # 1.5 MB blobs over PCIe: well above 1 GB/s, below the 64 GB/s link
+    assert 1e9 < sa["bw_physical_Bps"] < 80e9, sa["bw_physical_Bps"]
+    assert abs(a.metrics().bandwidth_estimate - 2 * ef.GB) < 0.01 * ef.GB  # logical clock's EWMA

@@ -239,6 +239,40 @@ def test_multi_token_stepper_matches_oracle():
         assert R.diff_dicts(got, want) == [], c["policy"]["name"]
 
 
+def test_bandwidth_feedback_matches_oracle():
+    """Flagged bandwidth feedback into S: every
+    adaptive boundary re-bases the step on the current estimate.  The product
+    stepper and the oracle agree with the flag on, and the flag changes the
+    step history on some case (it is off — the reference's behaviour — by
+    default)."""
+    cases = [c for c in G.load("simulate.json") if c["model"]["num_layers"] == 8
+             and c["policy"]["strategy"] == "adaptive" and not c.get("forest")][:30]
+    assert cases
+    changed = 0
+    for c in cases:
+        model, hw = ef.ModelSpec(**c["model"]), ef.HardwareSpec(**c["hw"])
+        pol = to_policy(c["policy"])
+        traces = [to_trace(x["trace"]) for x in cases[:3]]
+        sim = ef.Simulator(model, hw, pol, ef.Seed(c["seed"]), emit_events=True,
+                           bandwidth_feedback=True)
+        base = ef.Simulator(model, hw, pol, ef.Seed(c["seed"]))
+        st = S.OracleStepper(num_layers=model.num_layers, experts_per_layer=model.experts_per_layer,
+                             top_k=model.top_k, expert_size_bytes=model.expert_size_bytes,
+                             link_bw=hw.link_bandwidth_bytes_per_sec,
+                             device_memory_bytes=hw.device_memory_bytes,
+                             layer_compute_ns=ef.seconds_to_ns(hw.layer_compute_time_sec),
+                             policy=S.Policy(**c["policy"]), seed_value=c["seed"],
+                             emit_events=True, bandwidth_feedback=True)
+        for tr, x in zip(traces, cases[:3]):
+            sim.run_token(tr)
+            base.run_token(tr)
+            st.run_token(G.token_trace(x["trace"]))
+        got = R.product_metrics_dict(sim.metrics(), sim.cache_events())
+        assert R.diff_dicts(got, R.oracle_metrics_dict(st)) == [], c["policy"]["name"]
+        changed += sim.metrics().step_history != base.metrics().step_history
+    assert changed > 0
+
+
 def test_forest_inference_matches_reference():
     for c in G.load("forest.json"):
         fo = ef.model_from_json(c["forest"])
