@@ -489,6 +489,10 @@ struct ef_engine {
   }
 
   int cur_topup = 0;  // top-up target of the layer being enqueued (residency_mask)
+  bool ffn_mma = false;  // tensor-core decode FFN (bf16), shared experts in its launches
+  // shared-gate logits, double-buffered by layer parity: router(l) writes
+  // layer l's while its CTAs still combine layer l-1 with the other buffer
+  float* sgl_of(int l) { return sgl_d + (l & 1) * cfg.max_batch; }
   uint64_t* fmask_d = nullptr;  // [L][2] final bias mask of each layer (route kernel)
   void enqueue_layer(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask);
   void enqueue_front(cudaStream_t stream, int l, int B, int R, const uint64_t* mask);
@@ -732,7 +736,7 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
   const bool sgate = cfg.shared_ff && cfg.shared_gate;
   layer_seq[l] = ++gate_seq;
   if ((fuse & 1) && M <= 128) {
-    CombineIn ci{cur_h, y_d, cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_d : nullptr, 1e-6f,
+    CombineIn ci{cur_h, y_d, cfg.shared_ff ? ys_d : nullptr, sgate ? sgl_of(l - 1) : nullptr, 1e-6f,
                  l > 0 ? stats_d + kStats * (l - 1) + 5 : nullptr, fused_gate()};
     const bool fp = fast_path();
     RouteFast rf{&dctrl[l], fast_words + l, layer_seq[l], {}};
@@ -746,20 +750,17 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
                            perm_d, inv_d, dev_of(out_sel(l)), dev_of(out_logits(l)),
                            fp ? nullptr : const_cast<uint32_t*>(&dev_of(out(l))->done),
                            stats_d + kStats * l + 6, fuse_d,
-                           comb_in_router(l, B) ? &ci : nullptr, fp ? &rf : nullptr));
+                           comb_in_router(l, B) ? &ci : nullptr, fp ? &rf : nullptr,
+                           sgate ? (char*)sgate_w + (int64_t)l * d * esz : nullptr,
+                           sgate ? sgl_of(l) : nullptr));  // shared gate = one more router row
     ++launches;
-    if (sgate) {
-      CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
-                           1, sgl_d));
-      ++launches;
-    }
   } else {
     CKS(router_logits_stamped(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype,
                               R, B, d, M, logits_d, stats_d + kStats * l + 7));
     ++launches;
     if (sgate) {
       CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
-                           1, sgl_d));
+                           1, sgl_of(l)));
       ++launches;
     }
     CKS(launch_route_publish(stream, logits_d, B, M, k, cfg.route_mode, cfg.routing_bias, mask[0],
@@ -769,7 +770,7 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
                              stats_d + kStats * l + 6, R * B * M));
     ++launches;
   }
-  if (cfg.shared_ff) {  // always resident: runs while the host decides the layer
+  if (cfg.shared_ff && !ffn_mma) {  // always resident: runs while the host decides the layer
     const char* sw = shared_w + (int64_t)l * sstride;
     int32_t z = 0, nb = B;
     CKS(expert_ffn_ptrs(stream, x_d, perm_d, k, true, &sw, &z, &nb, 1, d, cfg.shared_ff,
@@ -790,29 +791,34 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
                   const_cast<uint32_t*>(&dev_of(out(l))->done), M, fmask_d + 2 * l,
                   dev_of(&out(l)->mask[0])};
     }
+    // the tensor-core FFN carries the layer's shared expert(s) in the same launches
+    SharedFfn sh{shared_w + (int64_t)l * sstride, cfg.shared_ff, B, acts_d, ys_d};
+    const SharedFfn* shp = ffn_mma && cfg.shared_ff ? &sh : nullptr;
     CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
                          reinterpret_cast<volatile unsigned*>(fuse_d + 2), layer_seq[l], ready,
                          stats_d + kStats * l, std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d,
-                         y_d, &io));
+                         y_d, &io, shp));
     launches += 2;
     if (!comb_next) {  // y is in slot order after the fused FFN: no inv
       // after the last layer there is no next rmsnorm: x_d keeps x_{L-1},
       // which the host may still be reading (record_routing) on the fast path
       CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_d : nullptr, y_d, nullptr, wts_d,
                           cfg.shared_ff ? ys_d : nullptr,
-                          sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
+                          sgate ? sgl_of(l) : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
       ++launches;
     }
     return;
   }
   CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + kStats * l));
   ++launches;
+  SharedFfn sh{shared_w + (int64_t)l * sstride, cfg.shared_ff, B, acts_d, ys_d};
   CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
-                      std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d));
+                      std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d,
+                      ffn_mma && cfg.shared_ff ? &sh : nullptr));
   launches += 2;
   if (comb_next) return;
   CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_d : nullptr, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
-                      sgate ? sgl_d : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
+                      sgate ? sgl_of(l) : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
   ++launches;
 }
 
@@ -1599,7 +1605,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       CK(cudaEventCreateWithFlags(&e->copy_mark, cudaEventDisableTiming));
     }
     CK(cudaMalloc(&e->logits_d, (size_t)L * B * M * 4));
-    CK(cudaMalloc(&e->sgl_d, (size_t)B * 4));
+    CK(cudaMalloc(&e->sgl_d, (size_t)2 * B * 4));
     CK(cudaMalloc(&e->wts_d, (size_t)B * k * 4));
     CK(cudaMalloc(&e->sel_d, (size_t)B * k * 4));
     CK(cudaMalloc(&e->counts_d, (size_t)M * 4));
@@ -1665,6 +1671,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->layer_R.assign(L, 1);
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
+    e->ffn_mma = ffn_mma_enabled(c.dtype, c.d, c.ff, c.shared_ff);
     e->init_weights();
     if (e->ep) {
       if (c.ep_nccl_id)

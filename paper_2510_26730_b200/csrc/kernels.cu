@@ -696,6 +696,11 @@ struct RouteArgs {
   unsigned long long* stamp_route;
   int* counter;
   ef::RouteFast rf;  // device-side slot resolution (rf.dc null: off)
+  // Qwen's sigmoid-gated shared expert: its gate logit x.w_sg rides as one
+  // extra router row (row index rows_main) written to sgl_out[t]
+  const void* sgate_w;
+  float* sgl_out;
+  int rows_main;
 };
 
 __device__ __forceinline__ int2 ld_volatile_v2(const void* p) {
@@ -863,10 +868,12 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   // is loaded before waiting on the previous kernel, so its HBM latency
   // overlaps the tail of the previous layer's FFN
   uint4 wv0[UN];
+  const bool sg_row = ra.sgate_w && warp == ra.rows_main;
+  const WT* wrow = sg_row ? reinterpret_cast<const WT*>(ra.sgate_w) : w + (int64_t)warp * d;
   if (warp < rows) {
 #pragma unroll
     for (int u = 0; u < UN; ++u)
-      if (lane * V + u * 32 * V < d) wv0[u] = ld_stream16(w + (int64_t)warp * d + lane * V + u * 32 * V);
+      if (lane * V + u * 32 * V < d) wv0[u] = ld_stream16(wrow + lane * V + u * 32 * V);
   }
   // this layer's slot-table row is final once the previous kernel has started
   // (written by the previous layer's gate warp, two kernels back)
@@ -902,7 +909,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
   }
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) stamp[5] = clock64();
   if (warp < rows) {
-    const WT* wr = w + (int64_t)warp * d;
+    const WT* wr = wrow;
     float acc[MAXB];
 #pragma unroll
     for (int t = 0; t < MAXB; ++t) acc[t] = 0.f;
@@ -969,7 +976,12 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     for (int t = 0; t < MAXB; ++t) {
       if (t < nb) {
         float sum = warp_sum(acc[t]);
-        if (lane == 0) logits[((int64_t)r * B + t0 + t) * M + m] = sum;
+        if (lane == 0) {
+          if (sg_row)
+            ra.sgl_out[t0 + t] = sum;
+          else
+            logits[((int64_t)r * B + t0 + t) * M + m] = sum;
+        }
       }
     }
   }
@@ -1000,13 +1012,13 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     if (cb.stamp && threadIdx.x == 0) *cb.stamp = gtimer();
   }
   if (threadIdx.x == 0) *ra.counter = 0;  // ready for the next launch
-  if (B * ra.k <= 32 && B <= (int)(blockDim.x >> 5) && (!ra.host_done || rows == M)) {
+  if (B * ra.k <= 32 && B <= (int)(blockDim.x >> 5) && (!ra.host_done || ra.rows_main == M)) {
     route_small(logits, ra, tabv, ra.stamp_route);
     return;
   }
   route_body(sm, logits, B, M, ra.k, ra.mode, ra.bias, ra.mlo, ra.mhi, ra.topup_U, ra.mask_out,
              ra.sel, ra.wts, ra.counts, ra.offsets, ra.perm, ra.inv, ra.host_mask, ra.host_sel,
-             ra.host_logits, ra.host_done, ra.stamp_route, rows * B);
+             ra.host_logits, ra.host_done, ra.stamp_route, ra.rows_main * B);
   if (ra.rf.dc && (threadIdx.x >> 5) == 0)
     resolve_fast(ra.rf, ra.counts, ra.offsets, M, ra.stamp_route ? ra.stamp_route + 5 : nullptr);
 }
@@ -1028,7 +1040,8 @@ __global__ void __launch_bounds__(256) router_route_row_kernel(const float* __re
   const int row = blockIdx.x;
   const int span = d / 8;  // 8 warps split the row
   const int cb0 = wid * span + lane * V;
-  const WT* wr = w + (int64_t)row * d;
+  const bool sg_row = ra.sgate_w && row == ra.rows_main;
+  const WT* wr = sg_row ? reinterpret_cast<const WT*>(ra.sgate_w) : w + (int64_t)row * d;
   uint4 wv0[UQ];
 #pragma unroll
   for (int u = 0; u < UQ; ++u)
@@ -1096,8 +1109,12 @@ __global__ void __launch_bounds__(256) router_route_row_kernel(const float* __re
   if (lane == 0) part[wid] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    logits[row] = ((part[0] + part[1]) + (part[2] + part[3])) +
-                  ((part[4] + part[5]) + (part[6] + part[7]));  // B = 1: [r][0][m] = row
+    const float v = ((part[0] + part[1]) + (part[2] + part[3])) +
+                    ((part[4] + part[5]) + (part[6] + part[7]));
+    if (sg_row)
+      ra.sgl_out[0] = v;
+    else
+      logits[row] = v;  // B = 1: [r][0][m] = row
     if (stamp && blockIdx.x == 0) stamp[6] = clock64();
     __threadfence();
     last = atomicAdd(ra.counter, 1) == (int)gridDim.x - 1;
@@ -1125,11 +1142,11 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
                        int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                        int32_t* host_sel, float* host_logits, uint32_t* host_done,
                        unsigned long long* stamp_route, int* counter, const CombineIn* ci,
-                       const RouteFast* rf) {
+                       const RouteFast* rf, const void* sgate_w, float* sgl_out) {
   EF_CHECK_ARG(M <= 128 && k <= 16 && B >= 1, "bad fused route shape");
   RouteArgs ra{B, M, k, mode, bias, mlo, mhi, topup_U, mask_out, host_mask, sel, counts, offsets,
                perm, inv, host_sel, wts, host_logits, host_done, stamp_route, counter,
-               rf ? *rf : RouteFast{}};
+               rf ? *rf : RouteFast{}, sgate_w, sgl_out, R * M};
   CombArgs cb{};
   size_t smem = 0;
   if (ci) {
@@ -1141,7 +1158,7 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
                   ci->ys, ci->gate_logit, k, ci->eps, ci->stamp};
     smem = (size_t)B * d * 4;
   }
-  const int rows = R * M, threads = 256;
+  const int rows = R * M + (sgate_w ? 1 : 0), threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
   const int vq = dtype == EF_BF16 ? 8 : 4;
   if (B == 1 && d % (8 * 32 * vq) == 0 && k <= 32 && (!host_done || R == 1)) {
@@ -1505,6 +1522,268 @@ __global__ void __launch_bounds__(128, NT <= 2 ? (DUAL ? 8 : 16) : 1) ffn_gemv_k
   if (DUAL) pdl_trigger();
 }
 
+// ------------------------------------------------------------ (d) decode FFN on mma.sync
+// Tensor-core decode FFN (bf16): one warp owns 16 output rows of one expert
+// and streams them ONCE for all of the expert's tokens (8-token n-tiles,
+// mma.sync.m16n8k16, fp32 accumulators in registers) — the GEMV kernel above
+// re-streams an expert per 8-token chunk and runs out of FMA throughput past
+// a few tokens.  The shared expert(s) ride in the same launch as extra work
+// units (identity token map), so a layer's whole FFN is one gate/up launch
+// and one down launch.  Weights: 16-byte L1-bypassing evict-first loads; k
+// is permuted inside each 32-wide block (thread tq holds k 8tq..8tq+7 of its
+// rows and of its token's x/act row) so every load is 16 B and A and B use
+// the same permutation.
+struct FfnMmaArgs {
+  // routed entries: DevCtrl (engine) or an explicit list (tests / bench)
+  const DevCtrl* ctrl;
+  ActiveList al;
+  int n_list;  // entries in `al` when ctrl is null
+  const char* slab;
+  int64_t stride;
+  const volatile uint32_t* ready;
+  unsigned long long* stats;
+  bool wait_ready;
+  // shared expert blob [W1 sff x d | W3 sff x d | W2 d x sff] (null: none),
+  // its tokens are rows 0..B-1 of x / act_s
+  const __nv_bfloat16* shared_w;
+  int sff, B;
+  // tensors
+  const float* x;          // [B, d] fp32 (up)
+  int tpr;                 // expert parallelism: tokens per rank block of x (0: contiguous)
+  int64_t rank_stride;     //   floats between rank blocks
+  const int32_t* perm;     // permuted row -> flat (token, rank) slot
+  int k, d, ff;
+  __nv_bfloat16* act;      // [rows, ff]  routed act (up out / down in)
+  __nv_bfloat16* act_s;    // [B, sff]    shared act
+  float* y;                // [slots, d]  routed out, row y_perm[p] (slot order) or p
+  float* ys;               // [B, d]      shared out
+  const int32_t* y_perm;
+  int max_active, routed_units, shared_units;  // units = 16-row warp tiles
+};
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1,
+                                               uint32_t a2, uint32_t a3, uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// 8 consecutive fp32 -> 4 bf16x2 (RNE): the expert input T(x)
+__device__ __forceinline__ uint4 ld_x8_bf16(const float* p) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  return make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+                    pack_bf16x2(b.z, b.w));
+}
+
+constexpr int kMmaWarps = 4;
+constexpr int kMmaTiles = 4;  // 8-token tiles per pass (32 tokens); more tokens loop
+
+// One warp: rows [r0, r0+16) of matrix A (and B when UP: W3 at +ff rows) of
+// one expert over K columns, tokens n (rows p0.. of the permuted order or the
+// shared expert's identity rows).
+template <bool UP>
+__device__ void mma_unit(const FfnMmaArgs& a, const __nv_bfloat16* W, int rows_total, int K,
+                         int r0, int p0, int n, bool shared, uint64_t pol) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const __nv_bfloat16* A0 = W + (int64_t)(r0 + g) * K + 8 * tq;
+  const __nv_bfloat16* A1 = A0 + (int64_t)8 * K;
+  const int64_t offB = (int64_t)rows_total * K;  // W3 behind W1 (UP)
+  for (int t0 = 0; t0 < n; t0 += 8 * kMmaTiles) {
+    const int nt = min(kMmaTiles, (n - t0 + 7) / 8);
+    // the token rows this thread feeds as column g of each n-tile
+    const float* xr[kMmaTiles];
+    const __nv_bfloat16* br[kMmaTiles];
+    bool ok[kMmaTiles];
+#pragma unroll
+    for (int j = 0; j < kMmaTiles; ++j) {
+      const int p = t0 + 8 * j + g;
+      ok[j] = j < nt && p < n;
+      const int pp = ok[j] ? p : 0;
+      if (UP) {
+        const int tok = shared ? pp : __ldg(a.perm + p0 + pp) / a.k;
+        xr[j] = (a.tpr ? a.x + (int64_t)(tok / a.tpr) * a.rank_stride + (int64_t)(tok % a.tpr) * a.d
+                       : a.x + (int64_t)tok * a.d) + 8 * tq;
+        br[j] = nullptr;
+      } else {
+        br[j] = (shared ? a.act_s + (int64_t)pp * a.sff : a.act + (int64_t)(p0 + pp) * a.ff) +
+                8 * tq;
+        xr[j] = nullptr;
+      }
+    }
+    float c1[kMmaTiles][4], c3[kMmaTiles][4];
+#pragma unroll
+    for (int j = 0; j < kMmaTiles; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c1[j][q] = c3[j][q] = 0.f;
+    constexpr int U = UP ? 2 : 4;  // 32-wide k blocks per iteration
+    for (int kb = 0; kb < K; kb += 32 * U) {
+      uint4 w1[U][2], w3[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = kb + 32 * u;
+        if (kk < K) {
+          w1[u][0] = ld_stream16_ef(A0 + kk, pol);
+          w1[u][1] = ld_stream16_ef(A1 + kk, pol);
+          if (UP) {
+            w3[u][0] = ld_stream16_ef(A0 + offB + kk, pol);
+            w3[u][1] = ld_stream16_ef(A1 + offB + kk, pol);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = kb + 32 * u;
+        if (kk >= K) break;
+#pragma unroll
+        for (int j = 0; j < kMmaTiles; ++j) {
+          if (j >= nt) break;
+          uint4 bv = make_uint4(0, 0, 0, 0);
+          if (ok[j]) bv = UP ? ld_x8_bf16(xr[j] + kk) : __ldg(reinterpret_cast<const uint4*>(br[j] + kk));
+          mma_bf16_16816(c1[j], w1[u][0].x, w1[u][1].x, w1[u][0].y, w1[u][1].y, bv.x, bv.y);
+          mma_bf16_16816(c1[j], w1[u][0].z, w1[u][1].z, w1[u][0].w, w1[u][1].w, bv.z, bv.w);
+          if (UP) {
+            mma_bf16_16816(c3[j], w3[u][0].x, w3[u][1].x, w3[u][0].y, w3[u][1].y, bv.x, bv.y);
+            mma_bf16_16816(c3[j], w3[u][0].z, w3[u][1].z, w3[u][0].w, w3[u][1].w, bv.z, bv.w);
+          }
+        }
+      }
+    }
+    // epilogue: c[q] = (row g + 8*(q>>1), token 2tq + (q&1)) of each n-tile
+#pragma unroll
+    for (int j = 0; j < kMmaTiles; ++j) {
+      if (j >= nt) break;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = t0 + 8 * j + 2 * tq + (q & 1);
+        if (p >= n) continue;
+        const int row = r0 + g + 8 * (q >> 1);
+        if (UP) {
+          const float gg = c1[j][q], uu = c3[j][q];
+          const float s = gg / (1.0f + expf(-gg)) * uu;
+          if (shared)
+            a.act_s[(int64_t)p * a.sff + row] = __float2bfloat16_rn(s);
+          else
+            a.act[(int64_t)(p0 + p) * a.ff + row] = __float2bfloat16_rn(s);
+        } else {
+          if (shared)
+            a.ys[(int64_t)p * a.d + row] = c1[j][q];
+          else
+            a.y[(a.y_perm ? (int64_t)__ldg(a.y_perm + p0 + p) : (int64_t)(p0 + p)) * a.d + row] =
+                c1[j][q];
+        }
+      }
+    }
+  }
+}
+
+template <bool UP>
+__global__ void __launch_bounds__(kMmaWarps * 32) ffn_mma_kernel(FfnMmaArgs a, FuseArgs fz) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  pdl_wait();
+  if (!UP) pdl_trigger();  // the next kernel is the small router grid
+  if (fz.hc && blockIdx.x == 0) {  // fused gate: CTA 0 is the gate (see ffn_gemv_kernel)
+    if (wid == 0) gate_duty(fz.hc, fz.dc, a.stats, fz.dflag, fz.seq, fz.io);
+    return;
+  }
+  const int u = (blockIdx.x - (fz.hc ? 1 : 0)) * kMmaWarps + wid;
+  const uint64_t pol = l2_evict_first_policy();
+  if (u < a.shared_units) {  // shared expert: always resident, needs no decision
+    const int rows = UP ? a.sff : a.d;
+    const __nv_bfloat16* W = a.shared_w + (UP ? 0 : 2LL * a.sff * a.d);
+    mma_unit<UP>(a, W, rows, UP ? a.d : a.sff, u * 16, 0, a.B, true, pol);
+    if (UP) pdl_trigger();
+    return;
+  }
+  if (fz.hc && lane == 0) {  // routed work waits for the layer's decision
+    const bool fast = fz.io.fast_word &&
+                      *reinterpret_cast<const volatile unsigned*>(fz.io.fast_word) == fz.seq;
+    const long long c0 = clock64();
+    while (!fast && ld_acquire_gpu(fz.dflag) < fz.seq) {
+      __nanosleep(64);
+      if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+    }
+  }
+  __syncwarp();
+  const int ru = u - a.shared_units;
+  const int ei = ru / a.routed_units, sub = ru % a.routed_units;
+  int4 e = make_int4(0, 0, 0, 0);
+  const char* wbase = nullptr;
+  if (a.ctrl) {
+    if (ei < a.max_active && ei < __ldcg(&a.ctrl->n_active)) e = __ldcg(&a.ctrl->ent[ei]);
+    wbase = a.slab + (int64_t)e.x * a.stride;
+  } else if (ei < a.n_list) {
+    e = make_int4(0, a.al.p0[ei], a.al.n[ei], 0);
+    wbase = a.al.w[ei];
+  }
+  if (e.z <= 0) {
+    if (UP) pdl_trigger();
+    return;
+  }
+  if (a.ctrl && a.wait_ready && lane == 0) {
+    const bool early = blockIdx.x < 4;
+    if (a.stats && early) atomicMin(&a.stats[10], globaltimer());
+    const unsigned need = (unsigned)e.w;
+    if (a.ready[e.x] < need) {
+      const unsigned long long t0 = globaltimer();
+      const long long c0 = clock64();
+      while (a.ready[e.x] < need) {
+        __nanosleep(256);
+        if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+      }
+      const unsigned long long t1 = globaltimer();
+      if (a.stats && t1 > t0) atomicMax(&a.stats[2], t1 - t0);
+    }
+    if (a.stats && early) atomicMin(&a.stats[3], globaltimer());
+  }
+  __syncwarp();
+  const __nv_bfloat16* W =
+      reinterpret_cast<const __nv_bfloat16*>(wbase) + (UP ? 0 : 2LL * a.ff * a.d);
+  mma_unit<UP>(a, W, UP ? a.ff : a.d, UP ? a.d : a.ff, sub * 16, e.y, e.z, false, pol);
+  if (!UP && a.ctrl && a.stats && lane == 0) atomicMax(&a.stats[4], globaltimer());
+  if (UP) pdl_trigger();
+}
+
+// Launch the pair (gate/up + SiLU, then down) for up to max_active routed
+// entries (+ the shared expert when a.shared_w).  Shapes: d, ff, sff % 16 == 0
+// and % 32 == 0 on the reduction side (checked by the callers).
+static int launch_ffn_mma(cudaStream_t st, FfnMmaArgs a, const FuseArgs& fz_up,
+                          const FuseArgs& fz_dn) {
+  a.routed_units = a.ff / 16;
+  a.shared_units = a.shared_w ? a.sff / 16 : 0;
+  const int n_ent = a.ctrl ? a.max_active : a.n_list;
+  const int up_units = a.shared_units + n_ent * a.routed_units;
+  const int up_ctas = (up_units + kMmaWarps - 1) / kMmaWarps + (fz_up.hc ? 1 : 0);
+  EF_CUDA_RET(launch_k(ffn_mma_kernel<true>, dim3(up_ctas), dim3(kMmaWarps * 32), 0, st, a, fz_up));
+  FfnMmaArgs b = a;
+  b.wait_ready = false;
+  b.routed_units = a.d / 16;
+  b.shared_units = a.shared_w ? a.d / 16 : 0;
+  const int dn_units = b.shared_units + n_ent * b.routed_units;
+  EF_CUDA_RET(launch_k(ffn_mma_kernel<false>, dim3((dn_units + kMmaWarps - 1) / kMmaWarps),
+                       dim3(kMmaWarps * 32), 0, st, b, fz_dn));
+  return EF_OK;
+}
+
+// The tensor-core decode FFN serves bf16 experts whose dimensions are
+// multiples of 32 (every SURVEY §8 shape); EF_FFN_MMA=0 selects the GEMV pair
+// (A/B comparisons, fp32 engines always use it).
+namespace ef {
+bool ffn_mma_enabled(int dtype, int d, int ff, int sff) {
+  static const int env = [] {
+    const char* v = getenv("EF_FFN_MMA");
+    return v ? atoi(v) : 1;
+  }();
+  return env != 0 && dtype == EF_BF16 && d % 32 == 0 && ff % 32 == 0 && sff % 32 == 0;
+}
+}  // namespace ef
+
 // Decode GEMV tilings (tools/ffn_lab.cu sweep on B200, Mixtral shapes):
 // gate/up: 2 rows x 2 column chunks per warp (8 x 16 B in flight per lane,
 // few distinct DRAM rows per warp) ran at 6.5 TB/s vs 5.5 TB/s for 4 x 1;
@@ -1571,6 +1850,19 @@ int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k,
     max_rows = std::max(max_rows, nrows[i]);
   }
   if (max_rows == 0) return EF_OK;
+  if (!identity && ffn_mma_enabled(dtype, d, ff, 0)) {
+    FfnMmaArgs a{};
+    a.al = al;
+    a.n_list = n_active;
+    a.x = x;
+    a.perm = perm;
+    a.k = k;
+    a.d = d;
+    a.ff = ff;
+    a.act = (__nv_bfloat16*)act;
+    a.y = y;
+    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{});
+  }
   CtrlSrc cs{};
   if (dtype == EF_BF16) {
     XGather<__nv_bfloat16> xg{x, perm, k, d, identity, identity ? p0[0] : 0};
@@ -1589,7 +1881,7 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
                      int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
                      int max_rows, int d, int ff, int dtype, void* act, float* y,
-                     const GateIO* io) {
+                     const GateIO* io, const SharedFfn* sh) {
   EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
   ActiveList al{};
   CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
@@ -1597,6 +1889,33 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
               dflag, seq, io ? *io : GateIO{}, nullptr};
   FuseArgs fd{};
   fd.y_perm = perm;  // y in slot order (the engine's combine reads it without inv)
+  if (ffn_mma_enabled(dtype, d, ff, sh ? sh->sff : 0)) {
+    FfnMmaArgs a{};
+    a.ctrl = reinterpret_cast<const DevCtrl*>(dctrl);
+    a.slab = slab;
+    a.stride = stride;
+    a.ready = ready;
+    a.stats = stats;
+    a.wait_ready = true;
+    if (sh) {
+      a.shared_w = reinterpret_cast<const __nv_bfloat16*>(sh->w);
+      a.sff = sh->sff;
+      a.B = sh->B;
+      a.act_s = reinterpret_cast<__nv_bfloat16*>(sh->act);
+      a.ys = sh->y;
+    }
+    a.x = x;
+    a.perm = perm;
+    a.k = k;
+    a.d = d;
+    a.ff = ff;
+    a.act = (__nv_bfloat16*)act;
+    a.y = y;
+    a.y_perm = perm;
+    a.max_active = max_active;
+    return launch_ffn_mma(st, a, fu, FuseArgs{});
+  }
+  EF_CHECK_ARG(!sh, "the shared expert rides in the tensor-core FFN launch only");
   if (dtype == EF_BF16) {
     XGather<__nv_bfloat16> xg{x, perm, k, d, false, 0};
     launch_ffn<__nv_bfloat16>(st, al, cs, max_active, max_rows, d, ff, xg, (__nv_bfloat16*)act, y,
@@ -1740,6 +2059,27 @@ int expert_ffn_ep(cudaStream_t st, const float* recv, int64_t W, int B, const in
                   unsigned long long* stats, int max_active, int max_rows, int d, int ff,
                   int dtype, void* act, float* y) {
   EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
+  if (ffn_mma_enabled(dtype, d, ff, 0)) {
+    FfnMmaArgs a{};
+    a.ctrl = reinterpret_cast<const DevCtrl*>(dctrl);
+    a.slab = slab;
+    a.stride = stride;
+    a.ready = ready;
+    a.stats = stats;
+    a.wait_ready = true;
+    a.x = recv;
+    a.tpr = B;
+    a.rank_stride = W;
+    a.perm = perm;
+    a.k = k;
+    a.d = d;
+    a.ff = ff;
+    a.act = (__nv_bfloat16*)act;
+    a.y = y;
+    a.y_perm = perm;
+    a.max_active = max_active;
+    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{});
+  }
   ActiveList al{};
   CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
   FuseArgs fd{};
@@ -1760,8 +2100,34 @@ int expert_ffn_ep(cudaStream_t st, const float* recv, int64_t W, int B, const in
 int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                     int64_t stride, const void* dctrl, const uint32_t* ready,
                     unsigned long long* stats, int max_active, int max_rows, int d, int ff,
-                    int dtype, void* act, float* y) {
+                    int dtype, void* act, float* y, const SharedFfn* sh) {
   EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
+  if (ffn_mma_enabled(dtype, d, ff, sh ? sh->sff : 0)) {
+    FfnMmaArgs a{};
+    a.ctrl = reinterpret_cast<const DevCtrl*>(dctrl);
+    a.slab = slab;
+    a.stride = stride;
+    a.ready = ready;
+    a.stats = stats;
+    a.wait_ready = true;
+    if (sh) {
+      a.shared_w = reinterpret_cast<const __nv_bfloat16*>(sh->w);
+      a.sff = sh->sff;
+      a.B = sh->B;
+      a.act_s = reinterpret_cast<__nv_bfloat16*>(sh->act);
+      a.ys = sh->y;
+    }
+    a.x = x;
+    a.perm = perm;
+    a.k = k;
+    a.d = d;
+    a.ff = ff;
+    a.act = (__nv_bfloat16*)act;
+    a.y = y;
+    a.max_active = max_active;
+    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{});
+  }
+  EF_CHECK_ARG(!sh, "the shared expert rides in the tensor-core FFN launch only");
   ActiveList al{};
   CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
   if (dtype == EF_BF16) {
@@ -1987,6 +2353,8 @@ int preload_pipeline_kernels() {
   preload(combine_kernel, n);
   preload(host_io_kernel, n);
   preload(ep_pack_kernel, n);
+  preload(ffn_mma_kernel<true>, n);
+  preload(ffn_mma_kernel<false>, n);
   preload(ep_owner_kernel, n);
   return n;
 }

@@ -59,13 +59,21 @@ struct HostOut {  // followed by sel[B*k] int32 and logits[B*M] f32
   uint32_t pad[10];
 };
 
+// shared expert(s) of a layer riding in the routed FFN launch (tensor-core path)
+struct SharedFfn {
+  const char* w;  // [W1 sff x d | W3 sff x d | W2 d x sff] bf16
+  int sff, B;
+  void* act;      // [B, sff] bf16
+  float* y;       // [B, d]
+};
+bool ffn_mma_enabled(int dtype, int d, int ff, int sff);
 int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k, bool identity,
                     const char* const* wbase, const int32_t* p0, const int32_t* nrows,
                     int n_active, int d, int ff, int dtype, void* act, float* y);
 int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                     int64_t stride, const void* dctrl, const uint32_t* ready,
                     unsigned long long* stats, int max_active, int max_rows, int d, int ff,
-                    int dtype, void* act, float* y);
+                    int dtype, void* act, float* y, const SharedFfn* sh = nullptr);
 int launch_gate(cudaStream_t st, void* host_ctrl_dev, void* dctrl, unsigned long long* stats);
 int launch_init_stats(cudaStream_t st, unsigned long long* stats, int L);
 int preload_pipeline_kernels();
@@ -102,12 +110,13 @@ int router_route_fused(cudaStream_t st, const float* x, const void* w, int dtype
                        int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
                        int32_t* host_sel, float* host_logits, uint32_t* host_done,
                        unsigned long long* stamp_route, int* counter,
-                       const CombineIn* comb = nullptr, const RouteFast* rf = nullptr);
+                       const CombineIn* comb = nullptr, const RouteFast* rf = nullptr,
+                       const void* sgate_w = nullptr, float* sgl_out = nullptr);
 int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k, const char* slab,
                      int64_t stride, void* hctrl_dev, void* dctrl, volatile unsigned* dflag,
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
                      int max_rows, int d, int ff, int dtype, void* act, float* y,
-                     const GateIO* io = nullptr);
+                     const GateIO* io = nullptr, const SharedFfn* sh = nullptr);
 // expert parallelism (kernels.cu "expert parallelism" section)
 int ep_pack(cudaStream_t st, const float* x, const float* logits, const int32_t* sel,
             const float* wts, int B, int d, int Rm, int M, int k, float* out);

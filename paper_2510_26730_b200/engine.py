@@ -152,10 +152,26 @@ class SimMetrics:
 
 def route_batch(groups: Sequence[Tuple[int, Tuple[ExpertId, ...]]],
                 resident: Set[ExpertId]) -> Tuple[Tuple[int, ...], Tuple[int, ...]]:
-    """Stable ready-first partition of routing groups (engine.py:192-209)."""
-    ready = [gid for gid, dem in groups if all(e in resident for e in dem)]
-    late = [gid for gid, dem in groups if not all(e in resident for e in dem)]
-    return tuple(ready + late), tuple(late)
+    """Stable ready-first partition of routing groups (engine.py:192-209),
+    computed by the C++ runtime (ef_route_batch) over a dense index of the
+    demanded experts."""
+    groups = list(groups)
+    if not groups:
+        return (), ()
+    ids = {}
+    recs = []
+    for gid, dem in groups:
+        dem = tuple(dem)
+        recs += [int(gid), len(dem)] + [ids.setdefault(e, len(ids)) for e in dem]
+    mask = np.array([1 if e in resident else 0 for e in ids] or [0], dtype=np.uint8)
+    rec = L.i32arr(recs)
+    order = np.empty(len(groups), dtype=np.int32)
+    deferred = np.empty(len(groups), dtype=np.int32)
+    n, nd = C.c_int32(), C.c_int32()
+    L.check(L.lib.ef_route_batch(L.as_ptr(rec, C.c_int32), rec.size, L.as_ptr(mask, C.c_uint8),
+                                 max(1, len(ids)), L.as_ptr(order, C.c_int32),
+                                 L.as_ptr(deferred, C.c_int32), C.byref(n), C.byref(nd)))
+    return (tuple(int(g) for g in order[:n.value]), tuple(int(g) for g in deferred[:nd.value]))
 
 
 # --------------------------------------------------------------- C outputs
