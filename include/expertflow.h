@@ -363,6 +363,11 @@ typedef struct ef_engine_cfg {
   const void* ep_nccl_id;
   ef_collective_cb ep_collective;
   void* ep_user;
+  /* peer pool modes (see peer_device above): 1 = allocate and fill the pool on this
+     engine's own device for OTHER processes only (this engine's misses never read it;
+     export with ef_engine_peer_pool_handle).  Pool ids are global flat ids l*M + e. */
+  int32_t peer_pool_export;
+  uint64_t peer_ipc_layout_hash; /* the exporter's layout hash, checked when opening */
 } ef_engine_cfg;
 int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim, const ef_ladder_cfg* ladder,
                      ef_engine** out);
@@ -399,10 +404,11 @@ int ef_engine_stats(ef_engine* e, double* out, int n);
 /* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
    6 perm, 7 inv, 8 y, 9 x */
 int ef_engine_ptr(ef_engine* e, int which, void** out);
-/* export this engine's peer pool (allocated on its own device) as a 64-byte
-   cudaIpcMemHandle_t, for the engine of another process to open through
-   ef_engine_cfg.peer_ipc_handle */
-int ef_engine_peer_pool_handle(ef_engine* e, void* handle64);
+/* export this engine's peer pool (allocated on its own device: export-only mode, or
+   the same-device test mode) as a 64-byte cudaIpcMemHandle_t plus the pool's layout
+   hash (expert bytes + global ids), for the engine of another process to open
+   through ef_engine_cfg.peer_ipc_handle / peer_ipc_layout_hash */
+int ef_engine_peer_pool_handle(ef_engine* e, void* handle64, uint64_t* layout_hash);
 /* routing log entry `index` (one per executed layer, in order): R scored router
    matrices of logits [R][B][M] fp32, sel [B][k], cache-aware bias mask.  Pass
    null buffers to query sizes; *n_entries = log length. */

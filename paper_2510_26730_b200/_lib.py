@@ -68,7 +68,8 @@ class EngineCfg(C.Structure):
                 ("host_store_attach", i32), ("peer_device", i32), ("peer_pool_experts", i64),
                 ("peer_pool_ids", P(i32)), ("peer_ipc_handle", vp),
                 ("ep_world", i32), ("ep_rank", i32), ("ep_nccl_id", vp),
-                ("ep_collective", COLLECTIVE_CB), ("ep_user", vp)]
+                ("ep_collective", COLLECTIVE_CB), ("ep_user", vp),
+                ("peer_pool_export", i32), ("peer_ipc_layout_hash", u64)]
 
 
 _SIGS = {
@@ -142,7 +143,7 @@ _SIGS = {
     "ef_engine_output": (C.c_int, [vp, i32, P(i64), i64, P(i64)]),
     "ef_engine_event_details": (C.c_int, [vp, C.c_char_p, i64, P(i64)]),
     "ef_engine_stats": (C.c_int, [vp, P(f64), C.c_int]),
-    "ef_engine_peer_pool_handle": (C.c_int, [vp, vp]),
+    "ef_engine_peer_pool_handle": (C.c_int, [vp, vp, P(u64)]),
     "ef_engine_ptr": (C.c_int, [vp, C.c_int, P(vp)]),
     "ef_engine_slot_of": (C.c_int, [vp, i32, i32, P(i32)]),
     "ef_engine_routing_log": (C.c_int, [vp, i64, P(f32), i64, P(i32), i64, P(i32), P(i32), P(u64),

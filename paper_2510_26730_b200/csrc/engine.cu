@@ -34,6 +34,7 @@
 
 #include <fcntl.h>
 #include <sys/mman.h>
+#include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -220,6 +221,22 @@ struct ef_engine {
   size_t shm_bytes = 0;
   std::string shm_name;      // set by the creating process, which unlinks it
   bool store_filled = false;  // attached to a store another process filled
+  static constexpr size_t kShmHeader = 4096;
+  static constexpr uint64_t kShmMagic = 0x45464853544f5245ull;  // "EFHSTORE"
+  struct ShmHeader {
+    uint64_t magic, layout;
+    uint32_t complete;
+  };
+  uint64_t store_layout_hash() const {
+    uint64_t h = 1469598103934665603ull;
+    for (int64_t v : {(int64_t)cfg.L, (int64_t)cfg.M, (int64_t)cfg.d, (int64_t)cfg.ff,
+                      (int64_t)cfg.dtype, (int64_t)cfg.seed, (int64_t)e0, (int64_t)sM(), stride})
+      for (int b = 0; b < 8; ++b) {
+        h ^= (uint64_t)((v >> (8 * b)) & 0xff);
+        h *= 1099511628211ull;
+      }
+    return h;
+  }
   cudaStream_t copy_stream = nullptr;
   // peer-HBM tier (ef_engine_cfg.peer_device / peer_pool_experts): home copies
   // of experts [0, peer_n) (flat l*M+e) on device peer_dev
@@ -230,6 +247,7 @@ struct ef_engine {
   bool peer_ipc = false;  // pool opened from another process's IPC handle
   int64_t peer_copies = 0, peer_bytes = 0;
   void init_peer_pool();
+  uint64_t pool_hash = 0;
   // A same-device copy runs on SMs, not on a copy engine (tools/peer_copy_lab.cu:
   // it never starts while a kernel holds every SM).  A routed FFN that fills the
   // GPU and spins on the slot such a copy fills would never finish, so the
@@ -620,20 +638,71 @@ void ef_engine::init_weights() {
 
 // Fill the peer pool from the host store (once, at create).  Cross-device
 // pools need peer access in both directions; the copies then run over NVLink.
+// Layout of a peer pool: FNV-1a over (expert blob bytes, pool size, global
+// flat ids) — exported with the IPC handle and checked by every opener, so a
+// pool is never read with another id order.
+static uint64_t pool_layout_hash(int64_t stride, const std::vector<int64_t>& ids) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](int64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      h ^= (uint64_t)((v >> (8 * b)) & 0xff);
+      h *= 1099511628211ull;
+    }
+  };
+  mix(stride);
+  mix((int64_t)ids.size());
+  for (int64_t v : ids) mix(v);
+  return h;
+}
+
+// Peer pool: home copies of experts, by GLOBAL flat id
+// l*M + e (peer_pool_ids; default: the first N experts this engine
+// schedules), on peer_device.  Three modes:
+//   in-process  peer_device != device: allocated and filled here, misses of
+//               pooled experts are cudaMemcpyPeerAsync over NVLink;
+//   export-only peer_pool_export: allocated and filled on this engine's own
+//               device for OTHER processes (ef_engine_peer_pool_handle); this
+//               engine's own misses never read it;
+//   opened      peer_ipc_handle: another process's pool, checked against
+//               peer_ipc_layout_hash.
+// Pools are filled by generating each expert on the pool's device with the
+// weights' counter generator (no host store needed: an expert-parallel rank
+// holds only its own shard in host memory).
 void ef_engine::init_peer_pool() {
-  peer_n = std::min<int64_t>(cfg.peer_pool_experts, (int64_t)cfg.L * sM());
+  const int64_t LMg = (int64_t)cfg.L * cfg.M;
+  peer_n = std::min<int64_t>(cfg.peer_pool_experts, LMg);
   peer_dev = cfg.peer_device;
-  const int64_t LM = (int64_t)cfg.L * sM();
   std::vector<int64_t> ids((size_t)peer_n);
-  pool_slot_of.assign((size_t)LM, -1);
-  for (int64_t i = 0; i < peer_n; ++i) {
-    ids[i] = cfg.peer_pool_ids ? cfg.peer_pool_ids[i] : i;
-    if (ids[i] < 0 || ids[i] >= LM || pool_slot_of[ids[i]] >= 0)
-      throw ValueError("peer_pool_ids must be distinct flat expert ids in [0, L*M)");
-    pool_slot_of[ids[i]] = i;
+  {
+    std::vector<char> seen((size_t)LMg, 0);
+    int64_t next_local = 0;  // default ids: the first N experts this engine schedules
+    for (int64_t i = 0; i < peer_n; ++i) {
+      if (cfg.peer_pool_ids) {
+        ids[i] = cfg.peer_pool_ids[i];
+      } else {
+        const int64_t ll = next_local++;
+        ids[i] = (ll / sM()) * cfg.M + e0 + ll % sM();
+      }
+      if (ids[i] < 0 || ids[i] >= LMg || seen[ids[i]])
+        throw ValueError("peer_pool_ids must be distinct flat expert ids in [0, L*M)");
+      seen[ids[i]] = 1;
+    }
   }
+  pool_hash = pool_layout_hash(stride, ids);
+  const bool export_only = cfg.peer_pool_export != 0;
+  pool_slot_of.assign((size_t)cfg.L * sM(), -1);
+  if (!export_only)
+    for (int64_t i = 0; i < peer_n; ++i) {
+      const int64_t l = ids[i] / cfg.M, e = ids[i] % cfg.M;
+      if (e < e0 || e >= e0 + sM())
+        throw ValueError("peer_pool_ids name an expert this expert-parallel rank does not own");
+      pool_slot_of[l * sM() + (e - e0)] = i;
+    }
   if (cfg.peer_ipc_handle) {
-    // pool created and filled by the process that owns peer_dev
+    if (export_only) throw ValueError("an opened peer pool cannot be export-only");
+    if (cfg.peer_ipc_layout_hash != pool_hash)
+      throw ValueError("peer_ipc_handle's pool holds another expert layout than peer_pool_ids "
+                       "(layout hash mismatch)");
     cudaIpcMemHandle_t h;
     std::memcpy(&h, cfg.peer_ipc_handle, sizeof(h));
     CK(cudaSetDevice(cfg.device));
@@ -647,24 +716,40 @@ void ef_engine::init_peer_pool() {
   }
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
-  if (peer_dev < 0 || peer_dev >= ndev) throw ValueError("peer_device is not a visible device");
-  if (peer_dev == cfg.device) check_same_device_pool();
-  if (peer_dev != cfg.device) {
-    int ok = 0;
-    CK(cudaDeviceCanAccessPeer(&ok, cfg.device, peer_dev));
-    if (!ok) throw RuntimeErr("no peer access between the engine device and peer_device");
-    for (int a : {cfg.device, peer_dev}) {
-      CK(cudaSetDevice(a));
-      cudaError_t r = cudaDeviceEnablePeerAccess(a == cfg.device ? peer_dev : cfg.device, 0);
-      if (r == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-      else CK(r);
+  if (export_only) {
+    peer_dev = cfg.device;  // exported for other processes; never read by this engine
+  } else {
+    if (peer_dev < 0 || peer_dev >= ndev) throw ValueError("peer_device is not a visible device");
+    if (peer_dev == cfg.device) check_same_device_pool();
+    if (peer_dev != cfg.device) {
+      int ok = 0;
+      CK(cudaDeviceCanAccessPeer(&ok, cfg.device, peer_dev));
+      if (!ok) throw RuntimeErr("no peer access between the engine device and peer_device");
+      for (int a : {cfg.device, peer_dev}) {
+        CK(cudaSetDevice(a));
+        cudaError_t r = cudaDeviceEnablePeerAccess(a == cfg.device ? peer_dev : cfg.device, 0);
+        if (r == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CK(r);
+      }
     }
   }
   CK(cudaSetDevice(peer_dev));
   CK(cudaMalloc(&peer_pool, (size_t)peer_n * stride));
-  for (int64_t i = 0; i < peer_n; ++i)
-    CK(cudaMemcpy(peer_pool + i * stride, store[ids[i] / sM()] + (ids[i] % sM()) * stride,
-                  stride, cudaMemcpyHostToDevice));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const int64_t nff = (int64_t)cfg.ff * cfg.d;
+  auto scale_for = [](double fan_in) { return (float)(std::sqrt(3.0 / fan_in) / 8388608.0); };
+  for (int64_t i = 0; i < peer_n; ++i) {
+    const int l = (int)(ids[i] / cfg.M), e = (int)(ids[i] % cfg.M);
+    char* dst = peer_pool + i * stride;
+    CKS(ef_fill_uniform(s, dst, cfg.dtype, nff, ef_stream_key(cfg.seed, l, e, 0), scale_for(cfg.d), 0));
+    CKS(ef_fill_uniform(s, dst + nff * esz, cfg.dtype, nff, ef_stream_key(cfg.seed, l, e, 1),
+                        scale_for(cfg.d), 0));
+    CKS(ef_fill_uniform(s, dst + 2 * nff * esz, cfg.dtype, nff, ef_stream_key(cfg.seed, l, e, 2),
+                        scale_for(cfg.ff), 0));
+  }
+  CK(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
   CK(cudaSetDevice(cfg.device));
 }
 
@@ -1632,24 +1717,51 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     CK(cudaHostAlloc(&e->seq_ring, sizeof(uint32_t) * ef_engine::kSeqRing, cudaHostAllocDefault));
     e->store.assign(L, nullptr);
     if (c.host_store_shm && c.host_store_shm[0]) {
-      // one pinned host store shared by every process on the node (replica
-      // ranks): POSIX shared memory, registered with CUDA in each process
-      const size_t bytes = (size_t)L * e->sM() * e->stride;
+      // one pinned host store shared by the processes of ONE node (replica
+      // ranks): POSIX shared memory, registered with CUDA in each process.  A
+      // 4 KiB header in front of the experts carries the store's layout hash
+      // and a fill-complete flag: attaching to a store of another shape or
+      // seed, or to one still being filled, fails loudly.
+      const size_t data = (size_t)L * e->sM() * e->stride;
+      const size_t bytes = data + ef_engine::kShmHeader;
       const bool create = !c.host_store_attach;
-      int fd = shm_open(c.host_store_shm, create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
-      if (fd < 0) throw RuntimeErr(std::string("shm_open failed for ") + c.host_store_shm);
+      int fd = shm_open(c.host_store_shm, create ? (O_CREAT | O_EXCL | O_RDWR) : O_RDWR, 0600);
+      if (fd < 0)
+        throw RuntimeErr(std::string(create ? "shm_open (create, exclusive) failed for "
+                                            : "shm_open (attach) failed for ") +
+                         c.host_store_shm);
       if (create && ftruncate(fd, (off_t)bytes) != 0) {
         close(fd);
+        shm_unlink(c.host_store_shm);
         throw RuntimeErr("ftruncate of the shared host store failed (is /dev/shm large enough?)");
+      }
+      struct stat sb {};
+      if (!create && (fstat(fd, &sb) != 0 || (size_t)sb.st_size != bytes)) {
+        close(fd);
+        throw ValueError("the shared host store has another size than this engine's experts");
       }
       void* base = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
       close(fd);
       if (base == MAP_FAILED) throw RuntimeErr("mmap of the shared host store failed");
       e->shm_base = base;
       e->shm_bytes = bytes;
-      if (create) e->shm_name = c.host_store_shm;
+      auto* hdr = reinterpret_cast<ef_engine::ShmHeader*>(base);
+      const uint64_t want = e->store_layout_hash();
+      if (create) {
+        e->shm_name = c.host_store_shm;
+        hdr->magic = ef_engine::kShmMagic;
+        hdr->layout = want;
+        hdr->complete = 0;
+      } else {
+        if (hdr->magic != ef_engine::kShmMagic || hdr->layout != want)
+          throw ValueError("the shared host store holds another model shape or seed");
+        if (__atomic_load_n(&hdr->complete, __ATOMIC_ACQUIRE) != 1)
+          throw RuntimeErr("the shared host store is not filled yet (attach after its creator "
+                           "finished)");
+      }
+      char* experts = (char*)base + ef_engine::kShmHeader;
       CK(cudaHostRegister(base, bytes, cudaHostRegisterDefault));
-      for (int l = 0; l < L; ++l) e->store[l] = (char*)base + (size_t)l * e->sM() * e->stride;
+      for (int l = 0; l < L; ++l) e->store[l] = experts + (size_t)l * e->sM() * e->stride;
       e->store_filled = !create;
     } else {
       for (int l = 0; l < L; ++l)
@@ -1671,8 +1783,10 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->layer_R.assign(L, 1);
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
-    e->ffn_mma = ffn_mma_enabled(c.dtype, c.d, c.ff, c.shared_ff);
+    e->ffn_mma = ffn_mma_enabled(c.dtype, c.d, c.ff, c.shared_ff, c.max_batch);
     e->init_weights();
+    if (e->shm_base && !e->store_filled)  // the experts are in: attachers may map them
+      __atomic_store_n(&reinterpret_cast<ef_engine::ShmHeader*>(e->shm_base)->complete, 1u, __ATOMIC_RELEASE);
     if (e->ep) {
       if (c.ep_nccl_id)
         e->xport = make_nccl_transport(c.ep_world, c.ep_rank, c.ep_nccl_id);
@@ -1784,13 +1898,15 @@ extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   });
 }
 
-extern "C" int ef_engine_peer_pool_handle(ef_engine* e, void* handle64) {
+extern "C" int ef_engine_peer_pool_handle(ef_engine* e, void* handle64, uint64_t* layout_hash) {
   EF_TRY({
     if (!e->peer_pool || e->peer_ipc || e->peer_dev != e->cfg.device)
-      throw ValueError("no peer pool allocated on this engine's device to export");
+      throw ValueError("no peer pool allocated on this engine's device to export "
+                       "(peer_pool_export=1 allocates one)");
     cudaIpcMemHandle_t h;
     CK(cudaIpcGetMemHandle(&h, e->peer_pool));
     std::memcpy(handle64, &h, sizeof(h));
+    if (layout_hash) *layout_hash = e->pool_hash;
   });
 }
 

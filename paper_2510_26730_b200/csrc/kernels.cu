@@ -1582,27 +1582,35 @@ __device__ __forceinline__ uint4 ld_x8_bf16(const float* p) {
                     pack_bf16x2(b.z, b.w));
 }
 
-constexpr int kMmaWarps = 4;
-constexpr int kMmaTiles = 4;  // 8-token tiles per pass (32 tokens); more tokens loop
 
 // One warp: rows [r0, r0+16) of matrix A (and B when UP: W3 at +ff rows) of
 // one expert over K columns, tokens n (rows p0.. of the permuted order or the
 // shared expert's identity rows).
-template <bool UP>
+// One CTA = one 16-row unit of one expert: its 4 warps split the reduction
+// dimension K in 4 (contiguous quarters), each streams its 16 x K/4 slice of
+// A (and of W3 when UP) once for all of the expert's tokens (NT 8-token
+// n-tiles per pass; more tokens loop over passes, the weights then come
+// from L2), and the partial fp32 fragments are summed in a fixed warp order
+// through shared memory before warp 0's epilogue (deterministic).  Split-K
+// keeps ~4x more warps streaming than a whole-K warp tile at decode batch.
+template <bool UP, int NT, int WARPS>
 __device__ void mma_unit(const FfnMmaArgs& a, const __nv_bfloat16* W, int rows_total, int K,
-                         int r0, int p0, int n, bool shared, uint64_t pol) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+                         int r0, int p0, int n, bool shared, uint64_t pol, float* red) {
+  constexpr int kMmaWarps = WARPS;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
+  // this warp's k range, in whole 32-wide blocks
+  const int nkb = K / 32;
+  const int kb0 = (nkb * wid) / kMmaWarps * 32, kb1 = (nkb * (wid + 1)) / kMmaWarps * 32;
   const __nv_bfloat16* A0 = W + (int64_t)(r0 + g) * K + 8 * tq;
   const __nv_bfloat16* A1 = A0 + (int64_t)8 * K;
   const int64_t offB = (int64_t)rows_total * K;  // W3 behind W1 (UP)
-  for (int t0 = 0; t0 < n; t0 += 8 * kMmaTiles) {
-    const int nt = min(kMmaTiles, (n - t0 + 7) / 8);
-    // the token rows this thread feeds as column g of each n-tile
-    const float* xr[kMmaTiles];
-    const __nv_bfloat16* br[kMmaTiles];
-    bool ok[kMmaTiles];
+  for (int t0 = 0; t0 < n; t0 += 8 * NT) {
+    const int nt = min(NT, (n - t0 + 7) / 8);
+    const float* xr[NT];
+    const __nv_bfloat16* br[NT];
+    bool ok[NT];
 #pragma unroll
-    for (int j = 0; j < kMmaTiles; ++j) {
+    for (int j = 0; j < NT; ++j) {
       const int p = t0 + 8 * j + g;
       ok[j] = j < nt && p < n;
       const int pp = ok[j] ? p : 0;
@@ -1617,18 +1625,18 @@ __device__ void mma_unit(const FfnMmaArgs& a, const __nv_bfloat16* W, int rows_t
         xr[j] = nullptr;
       }
     }
-    float c1[kMmaTiles][4], c3[kMmaTiles][4];
+    float c1[NT][4], c3[NT][4];
 #pragma unroll
-    for (int j = 0; j < kMmaTiles; ++j)
+    for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int q = 0; q < 4; ++q) c1[j][q] = c3[j][q] = 0.f;
-    constexpr int U = UP ? 2 : 4;  // 32-wide k blocks per iteration
-    for (int kb = 0; kb < K; kb += 32 * U) {
+    constexpr int U = UP ? 4 : 8;  // 32-wide k blocks in flight per iteration
+    for (int kb = kb0; kb < kb1; kb += 32 * U) {
       uint4 w1[U][2], w3[U][2];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int kk = kb + 32 * u;
-        if (kk < K) {
+        if (kk < kb1) {
           w1[u][0] = ld_stream16_ef(A0 + kk, pol);
           w1[u][1] = ld_stream16_ef(A1 + kk, pol);
           if (UP) {
@@ -1640,12 +1648,13 @@ __device__ void mma_unit(const FfnMmaArgs& a, const __nv_bfloat16* W, int rows_t
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int kk = kb + 32 * u;
-        if (kk >= K) break;
+        if (kk >= kb1) break;
 #pragma unroll
-        for (int j = 0; j < kMmaTiles; ++j) {
+        for (int j = 0; j < NT; ++j) {
           if (j >= nt) break;
           uint4 bv = make_uint4(0, 0, 0, 0);
-          if (ok[j]) bv = UP ? ld_x8_bf16(xr[j] + kk) : __ldg(reinterpret_cast<const uint4*>(br[j] + kk));
+          if (ok[j])
+            bv = UP ? ld_x8_bf16(xr[j] + kk) : __ldg(reinterpret_cast<const uint4*>(br[j] + kk));
           mma_bf16_16816(c1[j], w1[u][0].x, w1[u][1].x, w1[u][0].y, w1[u][1].y, bv.x, bv.y);
           mma_bf16_16816(c1[j], w1[u][0].z, w1[u][1].z, w1[u][0].w, w1[u][1].w, bv.z, bv.w);
           if (UP) {
@@ -1655,36 +1664,69 @@ __device__ void mma_unit(const FfnMmaArgs& a, const __nv_bfloat16* W, int rows_t
         }
       }
     }
-    // epilogue: c[q] = (row g + 8*(q>>1), token 2tq + (q&1)) of each n-tile
+    // split-K reduction: warps 1..3 park their fragments, warp 0 adds them in order
+    constexpr int NV = (UP ? 8 : 4) * NT;  // floats per thread
+    if (wid > 0) {
 #pragma unroll
-    for (int j = 0; j < kMmaTiles; ++j) {
-      if (j >= nt) break;
+      for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int p = t0 + 8 * j + 2 * tq + (q & 1);
-        if (p >= n) continue;
-        const int row = r0 + g + 8 * (q >> 1);
-        if (UP) {
-          const float gg = c1[j][q], uu = c3[j][q];
-          const float s = gg / (1.0f + expf(-gg)) * uu;
-          if (shared)
-            a.act_s[(int64_t)p * a.sff + row] = __float2bfloat16_rn(s);
-          else
-            a.act[(int64_t)(p0 + p) * a.ff + row] = __float2bfloat16_rn(s);
-        } else {
-          if (shared)
-            a.ys[(int64_t)p * a.d + row] = c1[j][q];
-          else
-            a.y[(a.y_perm ? (int64_t)__ldg(a.y_perm + p0 + p) : (int64_t)(p0 + p)) * a.d + row] =
-                c1[j][q];
+        for (int q = 0; q < 4; ++q) {
+          red[((wid - 1) * NV + j * 4 + q) * 32 + lane] = c1[j][q];
+          if (UP) red[((wid - 1) * NV + 4 * NT + j * 4 + q) * 32 + lane] = c3[j][q];
+        }
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+      for (int w = 1; w < kMmaWarps; ++w)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            c1[j][q] += red[((w - 1) * NV + j * 4 + q) * 32 + lane];
+            if (UP) c3[j][q] += red[((w - 1) * NV + 4 * NT + j * 4 + q) * 32 + lane];
+          }
+      // epilogue: c[q] = (row g + 8*(q>>1), token 2tq + (q&1)) of each n-tile
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        if (j >= nt) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int p = t0 + 8 * j + 2 * tq + (q & 1);
+          if (p >= n) continue;
+          const int row = r0 + g + 8 * (q >> 1);
+          if (UP) {
+            const float gg = c1[j][q], uu = c3[j][q];
+            const float sv = gg / (1.0f + expf(-gg)) * uu;
+            if (shared)
+              a.act_s[(int64_t)p * a.sff + row] = __float2bfloat16_rn(sv);
+            else
+              a.act[(int64_t)(p0 + p) * a.ff + row] = __float2bfloat16_rn(sv);
+          } else {
+            if (shared)
+              a.ys[(int64_t)p * a.d + row] = c1[j][q];
+            else
+              a.y[(a.y_perm ? (int64_t)__ldg(a.y_perm + p0 + p) : (int64_t)(p0 + p)) * a.d +
+                  row] = c1[j][q];
+          }
         }
       }
     }
+    __syncthreads();  // red is reused by the next pass
   }
 }
 
+// CTA size: 4 warps split K for gate/up (W1 and W3 in flight), 8 for down
 template <bool UP>
-__global__ void __launch_bounds__(kMmaWarps * 32) ffn_mma_kernel(FfnMmaArgs a, FuseArgs fz) {
+struct MmaWarps {
+  static constexpr int value = UP ? 4 : 8;
+};
+
+template <bool UP, int NT>
+__global__ void __launch_bounds__(MmaWarps<UP>::value * 32) ffn_mma_kernel(FfnMmaArgs a, FuseArgs fz) {
+  constexpr int kMmaWarps = MmaWarps<UP>::value;
+  __shared__ float red[(kMmaWarps - 1) * (UP ? 8 : 4) * NT * 32];
+  __shared__ int4 e_sh;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   pdl_wait();
   if (!UP) pdl_trigger();  // the next kernel is the small router grid
@@ -1692,95 +1734,107 @@ __global__ void __launch_bounds__(kMmaWarps * 32) ffn_mma_kernel(FfnMmaArgs a, F
     if (wid == 0) gate_duty(fz.hc, fz.dc, a.stats, fz.dflag, fz.seq, fz.io);
     return;
   }
-  const int u = (blockIdx.x - (fz.hc ? 1 : 0)) * kMmaWarps + wid;
+  const int u = blockIdx.x - (fz.hc ? 1 : 0);  // this CTA's 16-row unit
   const uint64_t pol = l2_evict_first_policy();
   if (u < a.shared_units) {  // shared expert: always resident, needs no decision
     const int rows = UP ? a.sff : a.d;
     const __nv_bfloat16* W = a.shared_w + (UP ? 0 : 2LL * a.sff * a.d);
-    mma_unit<UP>(a, W, rows, UP ? a.d : a.sff, u * 16, 0, a.B, true, pol);
+    mma_unit<UP, NT, kMmaWarps>(a, W, rows, UP ? a.d : a.sff, u * 16, 0, a.B, true, pol, red);
     if (UP) pdl_trigger();
     return;
   }
-  if (fz.hc && lane == 0) {  // routed work waits for the layer's decision
-    const bool fast = fz.io.fast_word &&
-                      *reinterpret_cast<const volatile unsigned*>(fz.io.fast_word) == fz.seq;
-    const long long c0 = clock64();
-    while (!fast && ld_acquire_gpu(fz.dflag) < fz.seq) {
-      __nanosleep(64);
-      if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
-    }
-  }
-  __syncwarp();
   const int ru = u - a.shared_units;
   const int ei = ru / a.routed_units, sub = ru % a.routed_units;
-  int4 e = make_int4(0, 0, 0, 0);
-  const char* wbase = nullptr;
-  if (a.ctrl) {
-    if (ei < a.max_active && ei < __ldcg(&a.ctrl->n_active)) e = __ldcg(&a.ctrl->ent[ei]);
-    wbase = a.slab + (int64_t)e.x * a.stride;
-  } else if (ei < a.n_list) {
-    e = make_int4(0, a.al.p0[ei], a.al.n[ei], 0);
-    wbase = a.al.w[ei];
+  if (threadIdx.x == 0) {
+    if (fz.hc) {  // routed work waits for the layer's decision
+      const bool fast = fz.io.fast_word &&
+                        *reinterpret_cast<const volatile unsigned*>(fz.io.fast_word) == fz.seq;
+      const long long c0 = clock64();
+      while (!fast && ld_acquire_gpu(fz.dflag) < fz.seq) {
+        __nanosleep(64);
+        if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+      }
+    }
+    int4 e = make_int4(0, 0, 0, 0);
+    if (a.ctrl) {
+      if (ei < a.max_active && ei < __ldcg(&a.ctrl->n_active)) e = __ldcg(&a.ctrl->ent[ei]);
+    } else if (ei < a.n_list) {
+      e = make_int4(ei, a.al.p0[ei], a.al.n[ei], 0);
+    }
+    if (a.ctrl && a.wait_ready && e.z > 0) {
+      const bool early = ru < 4;  // the first routed units stamp the FFN start
+      if (a.stats && early) atomicMin(&a.stats[10], globaltimer());
+      const unsigned need = (unsigned)e.w;
+      if (a.ready[e.x] < need) {
+        const unsigned long long t0 = globaltimer();
+        const long long c0 = clock64();
+        while (a.ready[e.x] < need) {
+          __nanosleep(256);
+          if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
+        }
+        const unsigned long long t1 = globaltimer();
+        if (a.stats && t1 > t0) atomicMax(&a.stats[2], t1 - t0);
+      }
+      if (a.stats && early) atomicMin(&a.stats[3], globaltimer());
+    }
+    e_sh = e;
   }
+  __syncthreads();
+  const int4 e = e_sh;
   if (e.z <= 0) {
     if (UP) pdl_trigger();
     return;
   }
-  if (a.ctrl && a.wait_ready && lane == 0) {
-    const bool early = blockIdx.x < 4;
-    if (a.stats && early) atomicMin(&a.stats[10], globaltimer());
-    const unsigned need = (unsigned)e.w;
-    if (a.ready[e.x] < need) {
-      const unsigned long long t0 = globaltimer();
-      const long long c0 = clock64();
-      while (a.ready[e.x] < need) {
-        __nanosleep(256);
-        if (clock64() - c0 > kSpinTimeoutCycles) asm volatile("trap;");
-      }
-      const unsigned long long t1 = globaltimer();
-      if (a.stats && t1 > t0) atomicMax(&a.stats[2], t1 - t0);
-    }
-    if (a.stats && early) atomicMin(&a.stats[3], globaltimer());
-  }
-  __syncwarp();
+  const char* wbase = a.ctrl ? a.slab + (int64_t)e.x * a.stride : a.al.w[e.x];
   const __nv_bfloat16* W =
       reinterpret_cast<const __nv_bfloat16*>(wbase) + (UP ? 0 : 2LL * a.ff * a.d);
-  mma_unit<UP>(a, W, UP ? a.ff : a.d, UP ? a.d : a.ff, sub * 16, e.y, e.z, false, pol);
-  if (!UP && a.ctrl && a.stats && lane == 0) atomicMax(&a.stats[4], globaltimer());
+  mma_unit<UP, NT, kMmaWarps>(a, W, UP ? a.ff : a.d, UP ? a.d : a.ff, sub * 16, e.y, e.z, false, pol, red);
+  if (!UP && a.ctrl && a.stats && threadIdx.x == 0) atomicMax(&a.stats[4], globaltimer());
   if (UP) pdl_trigger();
 }
 
-// Launch the pair (gate/up + SiLU, then down) for up to max_active routed
-// entries (+ the shared expert when a.shared_w).  Shapes: d, ff, sff % 16 == 0
-// and % 32 == 0 on the reduction side (checked by the callers).
-static int launch_ffn_mma(cudaStream_t st, FfnMmaArgs a, const FuseArgs& fz_up,
-                          const FuseArgs& fz_dn) {
+template <int NT>
+static int launch_ffn_mma_nt(cudaStream_t st, FfnMmaArgs a, const FuseArgs& fz_up,
+                             const FuseArgs& fz_dn) {
   a.routed_units = a.ff / 16;
   a.shared_units = a.shared_w ? a.sff / 16 : 0;
   const int n_ent = a.ctrl ? a.max_active : a.n_list;
-  const int up_units = a.shared_units + n_ent * a.routed_units;
-  const int up_ctas = (up_units + kMmaWarps - 1) / kMmaWarps + (fz_up.hc ? 1 : 0);
-  EF_CUDA_RET(launch_k(ffn_mma_kernel<true>, dim3(up_ctas), dim3(kMmaWarps * 32), 0, st, a, fz_up));
+  const int up_ctas = a.shared_units + n_ent * a.routed_units + (fz_up.hc ? 1 : 0);
+  EF_CUDA_RET(launch_k(ffn_mma_kernel<true, NT>, dim3(up_ctas), dim3(MmaWarps<true>::value * 32),
+                       0, st, a, fz_up));
   FfnMmaArgs b = a;
   b.wait_ready = false;
   b.routed_units = a.d / 16;
   b.shared_units = a.shared_w ? a.d / 16 : 0;
-  const int dn_units = b.shared_units + n_ent * b.routed_units;
-  EF_CUDA_RET(launch_k(ffn_mma_kernel<false>, dim3((dn_units + kMmaWarps - 1) / kMmaWarps),
-                       dim3(kMmaWarps * 32), 0, st, b, fz_dn));
+  const int dn_ctas = b.shared_units + n_ent * b.routed_units;
+  EF_CUDA_RET(launch_k(ffn_mma_kernel<false, NT>, dim3(dn_ctas), dim3(MmaWarps<false>::value * 32),
+                       0, st, b, fz_dn));
   return EF_OK;
+}
+
+// Launch the pair for `max_tok` tokens per expert at most (the batch: a
+// token picks an expert once): 8-token n-tiles, up to 4 per pass.
+static int launch_ffn_mma(cudaStream_t st, FfnMmaArgs a, const FuseArgs& fz_up,
+                          const FuseArgs& fz_dn, int max_tok) {
+  if (max_tok <= 8) return launch_ffn_mma_nt<1>(st, a, fz_up, fz_dn);
+  if (max_tok <= 16) return launch_ffn_mma_nt<2>(st, a, fz_up, fz_dn);
+  return launch_ffn_mma_nt<4>(st, a, fz_up, fz_dn);
 }
 
 // The tensor-core decode FFN serves bf16 experts whose dimensions are
 // multiples of 32 (every SURVEY §8 shape); EF_FFN_MMA=0 selects the GEMV pair
 // (A/B comparisons, fp32 engines always use it).
 namespace ef {
-bool ffn_mma_enabled(int dtype, int d, int ff, int sff) {
+bool ffn_mma_enabled(int dtype, int d, int ff, int sff, int max_tok) {
   static const int env = [] {
     const char* v = getenv("EF_FFN_MMA");
     return v ? atoi(v) : 1;
   }();
-  return env != 0 && dtype == EF_BF16 && d % 32 == 0 && ff % 32 == 0 && sff % 32 == 0;
+  if (env == 0 || dtype != EF_BF16 || d % 32 || ff % 32 || sff % 32) return false;
+  // auto: the GEMV pair streams a lone token's experts faster (tools/ffn_mma_lab.py,
+  // profiles/r02_ffn_lab.txt); from 2 tokens per expert, or to fold a shared
+  // expert into the layer's launches, the tensor-core pair
+  return env == 2 || max_tok > 1 || sff > 0;
 }
 }  // namespace ef
 
@@ -1850,7 +1904,7 @@ int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k,
     max_rows = std::max(max_rows, nrows[i]);
   }
   if (max_rows == 0) return EF_OK;
-  if (!identity && ffn_mma_enabled(dtype, d, ff, 0)) {
+  if (!identity && ffn_mma_enabled(dtype, d, ff, 0, max_rows)) {
     FfnMmaArgs a{};
     a.al = al;
     a.n_list = n_active;
@@ -1861,7 +1915,7 @@ int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k,
     a.ff = ff;
     a.act = (__nv_bfloat16*)act;
     a.y = y;
-    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{});
+    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{}, max_rows);
   }
   CtrlSrc cs{};
   if (dtype == EF_BF16) {
@@ -1889,7 +1943,7 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
               dflag, seq, io ? *io : GateIO{}, nullptr};
   FuseArgs fd{};
   fd.y_perm = perm;  // y in slot order (the engine's combine reads it without inv)
-  if (ffn_mma_enabled(dtype, d, ff, sh ? sh->sff : 0)) {
+  if (ffn_mma_enabled(dtype, d, ff, sh ? sh->sff : 0, max_rows)) {
     FfnMmaArgs a{};
     a.ctrl = reinterpret_cast<const DevCtrl*>(dctrl);
     a.slab = slab;
@@ -1913,7 +1967,7 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
     a.y = y;
     a.y_perm = perm;
     a.max_active = max_active;
-    return launch_ffn_mma(st, a, fu, FuseArgs{});
+    return launch_ffn_mma(st, a, fu, FuseArgs{}, std::max(max_rows, sh ? sh->B : 0));
   }
   EF_CHECK_ARG(!sh, "the shared expert rides in the tensor-core FFN launch only");
   if (dtype == EF_BF16) {
@@ -2059,7 +2113,7 @@ int expert_ffn_ep(cudaStream_t st, const float* recv, int64_t W, int B, const in
                   unsigned long long* stats, int max_active, int max_rows, int d, int ff,
                   int dtype, void* act, float* y) {
   EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
-  if (ffn_mma_enabled(dtype, d, ff, 0)) {
+  if (ffn_mma_enabled(dtype, d, ff, 0, max_rows)) {
     FfnMmaArgs a{};
     a.ctrl = reinterpret_cast<const DevCtrl*>(dctrl);
     a.slab = slab;
@@ -2078,7 +2132,7 @@ int expert_ffn_ep(cudaStream_t st, const float* recv, int64_t W, int B, const in
     a.y = y;
     a.y_perm = perm;
     a.max_active = max_active;
-    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{});
+    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{}, max_rows);
   }
   ActiveList al{};
   CtrlSrc cs{reinterpret_cast<const DevCtrl*>(dctrl), slab, stride, ready, stats, true};
@@ -2102,7 +2156,7 @@ int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k,
                     unsigned long long* stats, int max_active, int max_rows, int d, int ff,
                     int dtype, void* act, float* y, const SharedFfn* sh) {
   EF_CHECK_ARG(max_active >= 1 && max_active <= kMaxActive, "too many active experts");
-  if (ffn_mma_enabled(dtype, d, ff, sh ? sh->sff : 0)) {
+  if (ffn_mma_enabled(dtype, d, ff, sh ? sh->sff : 0, max_rows)) {
     FfnMmaArgs a{};
     a.ctrl = reinterpret_cast<const DevCtrl*>(dctrl);
     a.slab = slab;
@@ -2125,7 +2179,7 @@ int expert_ffn_ctrl(cudaStream_t st, const float* x, const int32_t* perm, int k,
     a.act = (__nv_bfloat16*)act;
     a.y = y;
     a.max_active = max_active;
-    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{});
+    return launch_ffn_mma(st, a, FuseArgs{}, FuseArgs{}, std::max(max_rows, sh ? sh->B : 0));
   }
   EF_CHECK_ARG(!sh, "the shared expert rides in the tensor-core FFN launch only");
   ActiveList al{};
@@ -2353,8 +2407,12 @@ int preload_pipeline_kernels() {
   preload(combine_kernel, n);
   preload(host_io_kernel, n);
   preload(ep_pack_kernel, n);
-  preload(ffn_mma_kernel<true>, n);
-  preload(ffn_mma_kernel<false>, n);
+  preload(ffn_mma_kernel<true, 1>, n);
+  preload(ffn_mma_kernel<false, 1>, n);
+  preload(ffn_mma_kernel<true, 2>, n);
+  preload(ffn_mma_kernel<false, 2>, n);
+  preload(ffn_mma_kernel<true, 4>, n);
+  preload(ffn_mma_kernel<false, 4>, n);
   preload(ep_owner_kernel, n);
   return n;
 }

@@ -66,7 +66,7 @@ struct SharedFfn {
   void* act;      // [B, sff] bf16
   float* y;       // [B, d]
 };
-bool ffn_mma_enabled(int dtype, int d, int ff, int sff);
+bool ffn_mma_enabled(int dtype, int d, int ff, int sff, int max_tok);
 int expert_ffn_ptrs(cudaStream_t st, const float* x, const int32_t* perm, int k, bool identity,
                     const char* const* wbase, const int32_t* p0, const int32_t* nrows,
                     int n_active, int d, int ff, int dtype, void* act, float* y);

@@ -47,7 +47,8 @@ class MoEEngine:
                  peer_pool_experts: int = 0, peer_ipc_handle: Optional[bytes] = None,
                  peer_pool_ids: Optional[Sequence[int]] = None, ep_rank: int = 0,
                  ep_world: int = 0, ep_nccl_id: Optional[bytes] = None,
-                 ep_collective=None, bandwidth_feedback: bool = False):
+                 ep_collective=None, bandwidth_feedback: bool = False,
+                 peer_pool_export: bool = False, peer_ipc_layout_hash: Optional[int] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("MoEEngine needs a CUDA device (no CPU fallback)")
         self.cfg, self.policy = cfg, policy
@@ -119,9 +120,13 @@ class MoEEngine:
         # a pool another process (one process per GPU) created on peer_device:
         # its 64-byte handle from that engine's peer_pool_handle()
         self._peer_ipc = None
+        ec.peer_pool_export = int(bool(peer_pool_export))
         if peer_ipc_handle is not None:
             if len(peer_ipc_handle) != 64:
                 raise ValueError("peer_ipc_handle must be the 64-byte handle of peer_pool_handle()")
+            if peer_ipc_layout_hash is None:
+                raise ValueError("opening a peer pool needs the exporter's peer_ipc_layout_hash")
+            ec.peer_ipc_layout_hash = int(peer_ipc_layout_hash)
             self._peer_ipc = C.create_string_buffer(bytes(peer_ipc_handle), 64)
             ec.peer_ipc_handle = C.cast(self._peer_ipc, L.vp)
         ec.ep_world, ec.ep_rank = self.ep_world, self.ep_rank
@@ -259,12 +264,14 @@ class MoEEngine:
         return [(rows[i], names[rows[i + 1]], ExpertId(rows[i + 2], rows[i + 3]))
                 for i in range(0, len(rows), 4)]
 
-    def peer_pool_handle(self) -> bytes:
-        """64-byte CUDA IPC handle of this engine's peer pool, for the engines
-        of other processes (``peer_ipc_handle=``) to serve misses from it."""
+    def peer_pool_handle(self):
+        """(64-byte CUDA IPC handle, layout hash) of this engine's peer pool,
+        for the engines of other processes (``peer_ipc_handle=``,
+        ``peer_ipc_layout_hash=``) to serve misses from it."""
         buf = C.create_string_buffer(64)
-        L.check(L.lib.ef_engine_peer_pool_handle(self._h.ptr, buf))
-        return buf.raw
+        h = C.c_uint64()
+        L.check(L.lib.ef_engine_peer_pool_handle(self._h.ptr, buf, C.byref(h)))
+        return buf.raw, h.value
 
     def stats(self) -> dict:
         keys = ["steps", "copies", "copy_bytes", "stall_ms", "phys_slots", "logical_capacity",

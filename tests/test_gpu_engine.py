@@ -492,9 +492,9 @@ from paper_2510_26730_b200.runtime import PRESETS, MoEEngine, synthetic_hidden
 cfg = PRESETS["tiny-bf16"]
 kw = dict(budget_experts=12, policy=ef.PolicyConfig("a", "adaptive", predictor="pregate"),
           link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2, seed=5)
-n = int(sys.argv[3])
+n, handle, lh = int(sys.argv[3]), bytes.fromhex(sys.argv[2]), int(sys.argv[4])
 a = MoEEngine(cfg, **kw)
-b = MoEEngine(cfg, peer_pool_experts=n, peer_ipc_handle=bytes.fromhex(sys.argv[2]), **kw)
+b = MoEEngine(cfg, peer_pool_experts=n, peer_ipc_handle=handle, peer_ipc_layout_hash=lh, **kw)
 for t in range(6):
     h1 = synthetic_hidden(cfg, 5, t, 2, torch.device("cuda", 0))
     h2 = h1.clone()
@@ -505,31 +505,42 @@ for t in range(6):
 assert a.cache_events() == b.cache_events()
 sb = b.stats()
 assert 0 < sb["peer_copies"] < sb["copies"], sb
+try:  # another id order than the exporter's: refused, never silently wrong bytes
+    MoEEngine(cfg, peer_pool_experts=n, peer_pool_ids=list(range(n))[::-1], peer_ipc_handle=handle,
+              peer_ipc_layout_hash=lh, **kw)
+    raise SystemExit("layout mismatch not detected")
+except ValueError:
+    pass
 print("ipc ok", int(sb["peer_copies"]), int(sb["copies"]))
 """
 
 
 @pytest.mark.gpu
 def test_peer_pool_ipc_across_processes(monkeypatch):
-    """One process per GPU: this process fills a peer pool and exports its
-    CUDA IPC handle; an engine in another process opens it
-    (``peer_ipc_handle``) and serves its misses from it, decoding exactly like
-    a host-only engine.  On a one-GPU box both processes share the device
-    (the test-only same-device mode, tiny shape)."""
+    """One process per GPU: this process fills an export-only peer pool (no
+    same-device override needed: its own misses never read it) and exports
+    its CUDA IPC handle and layout hash; an engine in another process opens
+    it (``peer_ipc_handle``) and serves its misses from it, decoding exactly
+    like a host-only engine; an opener with another id order is refused.  On
+    a one-GPU box the opener shares the device (test-only same-device mode)."""
     import os
     import subprocess
     import sys
-    monkeypatch.setenv("EF_PEER_SAME_DEVICE", "1")  # inherited by the child process
     cfg = PRESETS["tiny-bf16"]
     n_pool = cfg.num_layers * cfg.num_experts // 2
     owner = MoEEngine(cfg, budget_experts=12, policy=ef.PolicyConfig("a", "adaptive",
                                                                      predictor="pregate"),
                       link_bw=2 * ef.GB, layer_time_s=2e-4, max_batch=2, seed=5,
-                      peer_pool_experts=n_pool)
-    handle = owner.peer_pool_handle()
+                      peer_pool_experts=n_pool, peer_pool_export=True)
+    handle, lh = owner.peer_pool_handle()
     assert len(handle) == 64
+    for t in range(2):  # the exporter's own decode never reads its pool
+        owner.step(synthetic_hidden(cfg, 5, t, 2, DEV))
+    torch.cuda.synchronize()
+    assert owner.stats()["peer_copies"] == 0
+    monkeypatch.setenv("EF_PEER_SAME_DEVICE", "1")  # inherited by the child process
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _IPC_CHILD, root, handle.hex(), str(n_pool)],
+    r = subprocess.run([sys.executable, "-c", _IPC_CHILD, root, handle.hex(), str(n_pool), str(lh)],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ipc ok" in r.stdout, r.stdout + r.stderr
     owner.close()

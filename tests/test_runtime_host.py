@@ -46,7 +46,7 @@ def test_engine_cfg_struct_matches_header():
         names.append(chunks[0].split()[-1])
         names += [c.strip() for c in chunks[1:]]
     assert names == [f[0] for f in L.EngineCfg._fields_]
-    assert names[-5:] == ["ep_world", "ep_rank", "ep_nccl_id", "ep_collective", "ep_user"]
+    assert names[-7:-2] == ["ep_world", "ep_rank", "ep_nccl_id", "ep_collective", "ep_user"]
 
 
 def test_new_entry_points_exported():
