@@ -442,6 +442,7 @@ struct ef_engine {
     *src_seq = seq;
     CK(cudaMemcpyAsync(ready + s, src_seq, sizeof(uint32_t), cudaMemcpyHostToDevice,
                        copy_stream));
+    if (track_fills) track_fill(seq);
     slot_seq[s] = seq;
     ++copies;
     copy_bytes += stride;
@@ -546,6 +547,20 @@ struct ef_engine {
     return (fuse & 8) && (fuse & 1) && l > 0 && l < cfg.L && cfg.M <= 128 && B <= 8 &&
            (int64_t)B * cfg.d * 4 <= 128 * 1024;
   }
+  // ---- persistent decode layer (decode_layer.cuh): one launch per layer on
+  // the fast path for B <= 8 bf16 steps; per-layer outputs the next layer's
+  // prologue reads are double-buffered by layer parity
+  bool mega_ok = false;   // buffers allocated (shape supported at max_batch or below)
+  bool mega = false;      // this step runs the persistent layer kernel
+  LayerSync* sync_d = nullptr;  // [L]
+  float *mk_h[2] = {}, *mk_y[2] = {}, *mk_wts[2] = {}, *mk_ys[2] = {};
+  void enqueue_mega(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask);
+  void enqueue_any(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask) {
+    if (mega)
+      enqueue_mega(stream, l, B, h, R, mask);
+    else
+      enqueue_layer(stream, l, B, h, R, mask);
+  }
   void abort_pipeline(cudaStream_t stream, int from, int enq);
   void init_weights();
   void step(cudaStream_t stream, float* h, int B, const std::vector<int64_t>& tokens);
@@ -565,6 +580,38 @@ struct ef_engine {
   int4 *ptiles_h = nullptr, *ptiles_hdev = nullptr, *ptiles_d = nullptr;
   int64_t ptiles_cap = 0;  // int4 entries per region (4 regions)
   cudaEvent_t copy_mark = nullptr;
+  // prefill: one event per outstanding expert fill, so a layer's GEMMs wait
+  // for the copies of their own slots only, not for prefetches of later
+  // layers still on the link (fills complete in order on the one copy stream)
+  bool track_fills = false;
+  std::deque<std::pair<uint32_t, cudaEvent_t>> fills;  // outstanding, by fill sequence
+  std::vector<cudaEvent_t> fill_pool;
+  uint32_t fills_done = 0;  // every fill up to this sequence has landed
+  void reap_fills() {
+    while (!fills.empty() && cudaEventQuery(fills.front().second) == cudaSuccess) {
+      fills_done = fills.front().first;
+      fill_pool.push_back(fills.front().second);
+      fills.pop_front();
+    }
+  }
+  void track_fill(uint32_t seq) {
+    if (fills.size() > 256) reap_fills();
+    cudaEvent_t ev;
+    if (fill_pool.empty()) {
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    } else {
+      ev = fill_pool.back();
+      fill_pool.pop_back();
+    }
+    CK(cudaEventRecord(ev, copy_stream));
+    fills.emplace_back(seq, ev);
+  }
+  // make `stream` wait until fill `need` has landed
+  void wait_fill(cudaStream_t stream, uint32_t need) {
+    reap_fills();
+    if (need <= fills_done || fills.empty()) return;
+    CK(cudaStreamWaitEvent(stream, fills[need - fills.front().first].second, 0));
+  }
   int64_t prefills = 0, prefill_tokens = 0;
   double prefill_gemm_flop = 0;
   void prefill(cudaStream_t stream, float* h, int T, const std::vector<int64_t>& tokens);
@@ -775,9 +822,13 @@ ef_engine::~ef_engine() {
                   (void*)fast_words, (void*)fmask_d, (void*)px_d, (void*)plogits_d, (void*)pwts_d, (void*)py_d,
                   (void*)pys_d, (void*)psgl_d, (void*)psel_d, (void*)pcounts_d, (void*)poffsets_d,
                   (void*)pperm_d, (void*)pinv_d, (void*)piota_d, pA_d, pact_d, pacts_d,
-                  (void*)ptiles_d})
+                  (void*)ptiles_d, (void*)sync_d, (void*)mk_h[0], (void*)mk_h[1], (void*)mk_y[0],
+                  (void*)mk_y[1], (void*)mk_wts[0], (void*)mk_wts[1], (void*)mk_ys[0],
+                  (void*)mk_ys[1]})
     if (p) cudaFree(p);
   if (copy_mark) cudaEventDestroy(copy_mark);
+  for (auto& f : fills) cudaEventDestroy(f.second);
+  for (auto ev : fill_pool) cudaEventDestroy(ev);
   for (void* p : {(void*)hctrl, (void*)hout, (void*)seq_ring, (void*)host_tab,
                   (void*)plogits_h, (void*)psel_h, (void*)ptiles_h})
     if (p) cudaFreeHost(p);
@@ -907,6 +958,79 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   ++launches;
 }
 
+// One launch for the whole layer (decode_layer.cuh): the previous layer's
+// combine + rmsnorm, router + pre-gate rows, route with device-side slot
+// resolution and host publishing (fused gate), shared and routed expert FFN.
+void ef_engine::enqueue_mega(cudaStream_t stream, int l, int B, float* h, int R,
+                             const uint64_t* mask) {
+  const int M = cfg.M, k = cfg.top_k, d = cfg.d, L = cfg.L;
+  R = std::max(1, std::min(R, L - l));
+  layer_R[l] = R;
+  layer_seq[l] = ++gate_seq;
+  const bool sgate = cfg.shared_ff && cfg.shared_gate;
+  const int cur = l & 1, prev = (l + 1) & 1;
+  DecodeLayerIn in{};
+  in.B = B;
+  in.d = d;
+  in.ff = cfg.ff;
+  in.sff = cfg.shared_ff;
+  in.M = M;
+  in.k = k;
+  in.mode = cfg.route_mode;
+  in.R = R;
+  in.sgate = sgate;
+  in.eps = 1e-6f;
+  in.h_src = l == 0 ? h : mk_h[prev];
+  in.h_dst = mk_h[cur];
+  in.x_out = x_d;
+  in.has_prev = l > 0;
+  in.y_prev = mk_y[prev];
+  in.wts_prev = mk_wts[prev];
+  in.ys_prev = cfg.shared_ff ? mk_ys[prev] : nullptr;
+  in.sgl_prev = sgate ? sgl_of(l - 1) : nullptr;
+  in.comb_stamp = l > 0 ? stats_d + kStats * (l - 1) + 5 : nullptr;
+  in.w_router = (char*)router_w + (int64_t)l * M * d * esz;
+  in.w_sgate = sgate ? (char*)sgate_w + (int64_t)l * d * esz : nullptr;
+  in.logits = logits_d;
+  in.sgl_out = sgate ? sgl_of(l) : nullptr;
+  in.bias = cfg.routing_bias;
+  in.mlo = mask[0];
+  in.mhi = mask[1];
+  in.topup_U = cur_topup;
+  in.mask_out = fmask_d + 2 * l;
+  in.sel = sel_d;
+  in.counts = counts_d;
+  in.offsets = offsets_d;
+  in.perm = perm_d;
+  in.inv = inv_d;
+  in.wts_out = mk_wts[cur];
+  in.rf = RouteFast{&dctrl[l], fast_words + l, layer_seq[l], {}};
+  for (int e = 0; e < M; ++e) in.rf.tab[e] = host_tab[(int64_t)l * M + e];
+  in.hc_dev = &hctrl_dev[l];
+  in.io = GateIO{fast_words + l, sel_d, logits_d, B * k, R * B * M, dev_of(out_sel(l)),
+                 dev_of(out_logits(l)), const_cast<uint32_t*>(&dev_of(out(l))->done), M,
+                 fmask_d + 2 * l, dev_of(&out(l)->mask[0])};
+  in.slab = slab;
+  in.stride = stride;
+  in.ready = ready;
+  in.shared_w = cfg.shared_ff ? shared_w + (int64_t)l * sstride : nullptr;
+  in.act = act_d;
+  in.act_s = acts_d;
+  in.y_out = mk_y[cur];
+  in.ys_out = cfg.shared_ff ? mk_ys[cur] : nullptr;
+  in.max_active = std::min(B * k, M);
+  in.sync = sync_d + l;
+  in.stats = stats_d + kStats * l;
+  CKS(launch_decode_layer(stream, in));
+  ++launches;
+  if (l + 1 == L) {  // the last layer's combine: no next rmsnorm
+    CKS(launch_final_combine(stream, mk_h[cur], h, mk_y[cur], mk_wts[cur],
+                             cfg.shared_ff ? mk_ys[cur] : nullptr, sgate ? sgl_of(l) : nullptr, B,
+                             d, k));
+    ++launches;
+  }
+}
+
 void ef_engine::abort_pipeline(cudaStream_t stream, int from, int enq) {
   // Release every enqueued gate with an empty decision so the GPU drains,
   // then reset the flags for the next step.
@@ -983,7 +1107,13 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
   timing_begin(stream);
   cur_h = h;
   CKS(launch_init_stats(stream, stats_d, L));
-  CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
+  mega = mega_ok && fast_path() &&
+         decode_layer_supported(cfg.dtype, cfg.d, cfg.ff, cfg.shared_ff, M, k, B);
+  if (mega) {  // layer 0's prologue normalises h itself
+    CKS(launch_zero_sync(stream, sync_d, L));
+  } else {
+    CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
+  }
   launches += 2;
   mask_tokens = B;
   cur_topup = residency_mask(0, cur_mask);
@@ -1008,7 +1138,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       enqueue_front(stream, 0, B, Rmax, cur_mask);
       dbg_sync("router/route/shared", 0);
     } else {
-      enqueue_layer(stream, 0, B, h, Rmax, cur_mask);
+      enqueue_any(stream, 0, B, h, Rmax, cur_mask);
     }
     enq = 1;
     // the previous step's stats, now that this step's first layer is queued
@@ -1106,7 +1236,8 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
         run += cnt[e];
       }
       hc.n_active = n;
-      ffn_bytes += (int64_t)n * stride;
+      // the persistent layer's FFN window (stats 3..4) also streams the shared expert(s)
+      ffn_bytes += (int64_t)n * stride + (mega ? sstride : 0);
       ffn_launches += 2;
       std::atomic_thread_fence(std::memory_order_seq_cst);
       _mm_sfence();
@@ -1123,7 +1254,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
           enqueue_front(stream, l + 1, B, R1, cur_mask);
           dbg_sync("router/route/shared", l + 1);
         } else {
-          enqueue_layer(stream, l + 1, B, h, R1, cur_mask);
+          enqueue_any(stream, l + 1, B, h, R1, cur_mask);
         }
         enq = l + 2;
       } else if (debug) {
@@ -1358,7 +1489,21 @@ void ef_engine::fold_stats(int i) {
     if (sj[1] >= sj[0]) bubble_ms += (sj[1] - sj[0]) * 1e-6;
     if (sj[3] != ~0ull && sj[4] > sj[3]) ffn_ms += (sj[4] - sj[3]) * 1e-6;
     fast_layers += sj[11] ? 1 : 0;
-    if (dump) {  // per-layer device timeline (us)
+    if (dump && mega) {  // persistent layer: phases relative to CTA 0's start (us)
+      auto rel = [&](unsigned long long v) {
+        return (v == 0 || v == ~0ull) ? -1.0 : ((double)v - (double)sj[7]) * 1e-3;
+      };
+      char line[320];
+      snprintf(line, sizeof line,
+               "layer %2d prologue %5.1f route %5.1f released %5.1f ffn-start %5.1f routed-start "
+               "%5.1f shared-up-end %5.1f routed-up-end %5.1f ffn-end %5.1f published %5.1f "
+               "next %6.1f stall %5.1f%s\n",
+               j, rel(sj[12]), rel(sj[6]), rel(sj[13]), rel(sj[3]), rel(sj[10]), rel(sj[15]),
+               rel(sj[14]), rel(sj[4]), rel(sj[9]),
+               j + 1 < L ? rel(stats_h[kStats * (j + 1) + 7]) : 0.0, sj[2] * 1e-3,
+               sj[11] ? " fast" : "");
+      dump_text += line;
+    } else if (dump) {  // per-layer device timeline (us)
       auto us = [](unsigned long long a, unsigned long long b) {
         return ((double)b - (double)a) * 1e-3;
       };
@@ -1472,10 +1617,13 @@ void ef_engine::prefill_on(cudaStream_t stream, float* h, int T,
     std::fill(layer_use.begin(), layer_use.end(), -1);
     st->begin_layer(l);
     st->run_layer(l, r);
-    // every copy issued so far has to land (the link is serial: the layer's
-    // demand transfers are the last ones the decision waited for)
-    CK(cudaEventRecord(copy_mark, copy_stream));
-    CK(cudaStreamWaitEvent(stream, copy_mark, 0));
+    // the layer's GEMMs wait for the fills of their own slots only: the
+    // latest of them (fills land in order), so prefetches for later layers
+    // keep the link busy while this layer computes
+    uint32_t need = 0;
+    for (int e = 0; e < M; ++e)
+      if (cnt[e] && layer_use[e] >= 0) need = std::max(need, slot_seq[layer_use[e]]);
+    if (need > 0) wait_fill(stream, need);
     // ---- tiles {a_row0, b_row0, m_valid, n0}: 128-row m-tiles x 128-column n-tiles
     int4* tu = ptiles_h;
     int4* td = ptiles_h + ptiles_cap;
@@ -1688,6 +1836,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       CK(cudaHostGetDevicePointer((void**)&e->ptiles_hdev, e->ptiles_h, 0));
       CK(cudaMalloc(&e->ptiles_d, sizeof(int4) * 4 * e->ptiles_cap));
       CK(cudaEventCreateWithFlags(&e->copy_mark, cudaEventDisableTiming));
+      e->track_fills = true;
     }
     CK(cudaMalloc(&e->logits_d, (size_t)L * B * M * 4));
     CK(cudaMalloc(&e->sgl_d, (size_t)2 * B * 4));
@@ -1784,6 +1933,19 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
     e->layer_use.assign(M, -1);
     for (int s = 0; s < e->P; ++s) e->free_slots.push_back(s);
     e->ffn_mma = ffn_mma_enabled(c.dtype, c.d, c.ff, c.shared_ff, c.max_batch);
+    e->mega_ok = !e->ep && decode_layer_supported(c.dtype, c.d, c.ff, c.shared_ff, M, k, 1);
+    if (e->mega_ok) {
+      const int Bm = std::min(B, 8);
+      CK(cudaMalloc(&e->sync_d, sizeof(LayerSync) * L));
+      CK(cudaMemset(e->sync_d, 0, sizeof(LayerSync) * L));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaMalloc(&e->mk_h[i], (size_t)Bm * d * 4));
+        CK(cudaMalloc(&e->mk_y[i], (size_t)Bm * k * d * 4));
+        CK(cudaMalloc(&e->mk_wts[i], (size_t)Bm * k * 4));
+        if (c.shared_ff) CK(cudaMalloc(&e->mk_ys[i], (size_t)Bm * d * 4));
+      }
+      if (preload_decode_layer() < 3) throw CudaErr("could not load the persistent decode layer");
+    }
     e->init_weights();
     if (e->shm_base && !e->store_filled)  // the experts are in: attachers may map them
       __atomic_store_n(&reinterpret_cast<ef_engine::ShmHeader*>(e->shm_base)->complete, 1u, __ATOMIC_RELEASE);

@@ -486,14 +486,25 @@ __device__ __forceinline__ int float_order(float f) {
 __device__ __forceinline__ bool mask_has(uint64_t lo, uint64_t hi, int e) {
   return e < 64 ? ((lo >> e) & 1ull) : ((hi >> (e - 64)) & 1ull);
 }
+struct CtaBar {
+  __device__ void operator()() const { __syncthreads(); }
+};
+// tid / nthr: this thread's index in the participating group (the whole CTA,
+// or one 4-warp worker of the persistent decode kernel) and its size
+template <typename Bar = CtaBar>
 __device__ void topup_mask(TopupSmem& ts, const float* __restrict__ logits, int B, int M, int k,
-                           int U, uint64_t& mlo, uint64_t& mhi) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  for (int e = tid; e < kMaxExperts; e += blockDim.x) {
+                           int U, uint64_t& mlo, uint64_t& mhi, int tid = -1, int nthr = 0,
+                           Bar bar = Bar{}) {
+  if (tid < 0) {
+    tid = threadIdx.x;
+    nthr = blockDim.x;
+  }
+  const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
+  for (int e = tid; e < kMaxExperts; e += nthr) {
     ts.votes[e] = 0;
     ts.maxl[e] = INT_MIN;
   }
-  __syncthreads();
+  bar();
   for (int t = wid; t < B; t += nw) {
     const float* lg = logits + (int64_t)t * M;
     float v[4];
@@ -529,7 +540,7 @@ __device__ void topup_mask(TopupSmem& ts, const float* __restrict__ logits, int 
       if (lane == 0 && be != 0x7fffffff) atomicAdd(&ts.votes[be], 1);
     }
   }
-  __syncthreads();
+  bar();
   if (wid == 0) {
     uint64_t lo = mlo, hi = mhi;
     int n = __popcll(lo) + __popcll(hi);
@@ -570,7 +581,7 @@ __device__ void topup_mask(TopupSmem& ts, const float* __restrict__ logits, int 
       ts.m[1] = hi;
     }
   }
-  __syncthreads();
+  bar();
   mlo = ts.m[0];
   mhi = ts.m[1];
 }
@@ -2417,3 +2428,5 @@ int preload_pipeline_kernels() {
   return n;
 }
 }  // namespace ef
+
+#include "decode_layer.cuh"

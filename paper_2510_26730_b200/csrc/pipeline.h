@@ -117,6 +117,66 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
                      unsigned seq, const uint32_t* ready, unsigned long long* stats, int max_active,
                      int max_rows, int d, int ff, int dtype, void* act, float* y,
                      const GateIO* io = nullptr, const SharedFfn* sh = nullptr);
+// ---- persistent decode layer (decode_layer.cuh): one launch per layer runs the
+// previous layer's combine + rmsnorm, the router rows, the route, and the
+// shared + routed expert FFN (gate/up, then down) as a dataflow of work items
+// over a fixed grid (one 512-thread CTA per SM, four 4-warp workers each).
+struct LayerSync {  // per layer, zeroed at the start of every step
+  int q;            // next work item
+  int ticket;       // router rows finished
+  unsigned route;   // == launch seq: the decision block is final
+  int sh_up;        // shared-expert gate/up units finished
+  int up[kMaxActive];  // routed gate/up units finished, per decision entry
+  int pad[12];
+};
+struct DecodeLayerIn {
+  int B, d, ff, sff, M, k, mode, R;  // R router matrices (layer + pre-gate rows)
+  bool sgate;                        // one more router row: the shared expert's gate
+  float eps;
+  // hidden state: h_dst = h_src (+ previous layer's MoE output); x_out = rmsnorm(h_dst)
+  const float* h_src;
+  float* h_dst;
+  float* x_out;
+  bool has_prev;
+  const float* y_prev;    // [B*k, d] slot order
+  const float* wts_prev;  // [B*k]
+  const float* ys_prev;   // [B, d] shared-expert output (null: none)
+  const float* sgl_prev;  // [B] shared-gate logits (null: ungated)
+  unsigned long long* comb_stamp;
+  // router
+  const void* w_router;  // [R*M, d] (rows of layers l .. l+R-1)
+  const void* w_sgate;   // [d]
+  float* logits;         // [R][B][M]
+  float* sgl_out;        // [B]
+  // route
+  float bias;
+  uint64_t mlo, mhi;
+  int topup_U;
+  uint64_t* mask_out;
+  int32_t *sel, *counts, *offsets, *perm, *inv;
+  float* wts_out;
+  RouteFast rf;
+  void* hc_dev;  // HostCtrl of the layer (null: standalone, every expert must resolve)
+  GateIO io;     // host publishing (io.host_done null: none)
+  // FFN
+  const char* slab;
+  int64_t stride;
+  const uint32_t* ready;  // null: no copy waits
+  const void* shared_w;
+  void* act;
+  void* act_s;
+  float* y_out;
+  float* ys_out;
+  int max_active;
+  LayerSync* sync;
+  unsigned long long* stats;
+};
+bool decode_layer_supported(int dtype, int d, int ff, int sff, int M, int k, int B);
+int launch_decode_layer(cudaStream_t st, const DecodeLayerIn& in);
+int launch_final_combine(cudaStream_t st, const float* h_src, float* h_dst, const float* y,
+                         const float* wts, const float* ys, const float* sgl, int B, int d, int k);
+int launch_zero_sync(cudaStream_t st, LayerSync* sync, int L);
+int preload_decode_layer();
 // expert parallelism (kernels.cu "expert parallelism" section)
 int ep_pack(cudaStream_t st, const float* x, const float* logits, const int32_t* sel,
             const float* wts, int B, int d, int Rm, int M, int k, float* out);

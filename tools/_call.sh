@@ -1,8 +1,9 @@
 #!/bin/bash
-# C3/C4 decode: standalone FFN pair lab + serialised launch list of a Qwen / DeepSeek B=1 decode
+# persistent decode layer: phase timeline (Qwen / Mixtral B=1) + one ncu --set full capture
 cd "$GRAFT_REPO_ROOT"
-(EF_FFN_MMA=1 timeout 300 python tools/ffn_mma_lab.py; EF_FFN_MMA=0 timeout 300 python tools/ffn_mma_lab.py) > gpurun_out/r2c_ffnlab.txt 2>&1
-for c in qwen1.5-moe-a2.7b deepseek-v2-lite; do
-EF_PIPE_DEBUG=1 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 300 --csv \
-  --log-file gpurun_out/r2c_launch_$c.csv python tools/profile_decode.py --config $c --layers 4 --steps 3 --batch 1 > gpurun_out/r2c_ncu_$c.log 2>&1
+for c in qwen1.5-moe-a2.7b:1 mixtral-8x7b:1; do
+  cfg=${c%%:*}; b=${c##*:}
+  EF_STATS_DUMP=1 timeout 400 python bench.py --config $cfg --batch $b --steps 6 --warmup 4 --no-grid --no-cpu > gpurun_out/m2_${cfg}_b$b.log 2> gpurun_out/m2_${cfg}_b$b.err; echo "rc=$?" >> gpurun_out/m2_${cfg}_b$b.log
 done
+EF_PIPE_DEBUG=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_layer -s 6 -c 1 -o gpurun_out/m2_ncu_qwen \
+  python tools/profile_decode.py --config qwen1.5-moe-a2.7b --layers 4 --steps 3 --batch 1 > gpurun_out/m2_ncu.log 2>&1; echo "rc=$?" >> gpurun_out/m2_ncu.log
