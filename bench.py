@@ -554,7 +554,11 @@ def run_ours(args, cfg, bias):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak,
                          "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
-                         "kernel": "ef_expert_ffn_decode (gate/up+SiLU GEMV, down GEMV)",
+                         "kernel": ("decode_layer_kernel (persistent layer: routed + shared "
+                                    "expert gate/up and down units on mma.sync; window = first "
+                                    "FFN unit -> last down unit)"
+                                    if st1.get("layer_kernel_steps", 0) > st0.get("layer_kernel_steps", 0)
+                                    else "ef_expert_ffn_decode (gate/up+SiLU GEMV, down GEMV)"),
                          "bytes_per_launch": ffn_bytes / max(ffn_pairs, 1),
                          "timing": "on-device globaltimer stamps per layer (first FFN CTA past "
                                    "its ready check -> last down-projection CTA), summed over the "

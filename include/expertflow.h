@@ -399,7 +399,8 @@ int ef_engine_event_details(ef_engine* e, char* buf, int64_t max_len, int64_t* n
    peer-HBM tier), prefetch_admitted / prefetch_used / prefetch_wasted (experts admitted
    by a PREFETCH transfer; routed to by a later layer before eviction; evicted unused),
    bw_physical_Bps (EWMA, alpha 0.25, of the measured expert-copy rates; copy-stream
-   events), bw_physical_transfers (copies folded into it) */
+   events), bw_physical_transfers (copies folded into it), layer_kernel_steps (decode
+   steps run on the persistent one-launch-per-layer kernel) */
 int ef_engine_stats(ef_engine* e, double* out, int n);
 /* device pointers for tests: 0 slab, 1 router weights, 2 shared, 3 logits, 4 sel, 5 wts,
    6 perm, 7 inv, 8 y, 9 x */

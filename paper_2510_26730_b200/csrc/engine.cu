@@ -552,7 +552,50 @@ struct ef_engine {
   // prologue reads are double-buffered by layer parity
   bool mega_ok = false;   // buffers allocated (shape supported at max_batch or below)
   bool mega = false;      // this step runs the persistent layer kernel
+  int64_t mega_steps = 0;
+  double enqueue_ms = 0, publish_wait_ms = 0;  // host: launch calls / waiting for the publish
+  // EF_MEGA_TRACE=1: per work item start/end of every layer (the dump prints
+  // a summary of one layer); [L][kTraceItems][2]
+  static constexpr int kTraceItems = 8192;
+  unsigned long long* trace_d = nullptr;
+  std::vector<int> trace_rows, trace_cats;  // per layer: router rows, item range starts
   LayerSync* sync_d = nullptr;  // [L]
+  // tagged publish words {seq | value << 32} per layer: mask (4), sel (B*k),
+  // scored logits rows (R*B*M); mapped host memory
+  uint64_t* pub_h = nullptr;
+  uint64_t* pub_dev = nullptr;
+  int64_t pub_stride = 0;
+  // wait for layer l's tagged publish and unpack it where the classic
+  // pipeline's HostOut block puts it
+  void wait_publish(int l, int B, int R) {
+    const int k = cfg.top_k, M = cfg.M;
+    const volatile uint64_t* w = pub_h + (int64_t)l * pub_stride;
+    const uint32_t tag = layer_seq[l];
+    const int n = 4 + B * k + R * B * M;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = n - 1; i >= 0; --i) {  // the last word first: usually all have landed then
+      unsigned spins = 0;
+      while ((uint32_t)w[i] != tag) {
+        _mm_pause();
+        if ((++spins & 0xffff) == 0 &&
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 20.0)
+          throw RuntimeErr("decode layer kernel did not publish within 20 s");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    HostOut* ho = out(l);
+    uint32_t m[4];
+    for (int i = 0; i < 4; ++i) m[i] = (uint32_t)(w[i] >> 32);
+    ho->mask[0] = (uint64_t)m[0] | ((uint64_t)m[1] << 32);
+    ho->mask[1] = (uint64_t)m[2] | ((uint64_t)m[3] << 32);
+    int32_t* sel = out_sel(l);
+    for (int f = 0; f < B * k; ++f) sel[f] = (int32_t)(uint32_t)(w[4 + f] >> 32);
+    float* lg = out_logits(l);
+    for (int i = 0; i < R * B * M; ++i) {
+      const uint32_t v = (uint32_t)(w[4 + B * k + i] >> 32);
+      std::memcpy(&lg[i], &v, 4);
+    }
+  }
   float *mk_h[2] = {}, *mk_y[2] = {}, *mk_wts[2] = {}, *mk_ys[2] = {};
   void enqueue_mega(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask);
   void enqueue_any(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask) {
@@ -824,12 +867,12 @@ ef_engine::~ef_engine() {
                   (void*)pperm_d, (void*)pinv_d, (void*)piota_d, pA_d, pact_d, pacts_d,
                   (void*)ptiles_d, (void*)sync_d, (void*)mk_h[0], (void*)mk_h[1], (void*)mk_y[0],
                   (void*)mk_y[1], (void*)mk_wts[0], (void*)mk_wts[1], (void*)mk_ys[0],
-                  (void*)mk_ys[1]})
+                  (void*)mk_ys[1], (void*)trace_d})
     if (p) cudaFree(p);
   if (copy_mark) cudaEventDestroy(copy_mark);
   for (auto& f : fills) cudaEventDestroy(f.second);
   for (auto ev : fill_pool) cudaEventDestroy(ev);
-  for (void* p : {(void*)hctrl, (void*)hout, (void*)seq_ring, (void*)host_tab,
+  for (void* p : {(void*)hctrl, (void*)hout, (void*)seq_ring, (void*)host_tab, (void*)pub_h,
                   (void*)plogits_h, (void*)psel_h, (void*)ptiles_h})
     if (p) cudaFreeHost(p);
   if (shm_base) {
@@ -1021,6 +1064,21 @@ void ef_engine::enqueue_mega(cudaStream_t stream, int l, int B, float* h, int R,
   in.max_active = std::min(B * k, M);
   in.sync = sync_d + l;
   in.stats = stats_d + kStats * l;
+  in.pub = pub_dev + (int64_t)l * pub_stride;
+  in.parity = (int)(mega_steps & 1);
+  if (trace_d) {
+    in.trace = trace_d + (int64_t)l * kTraceItems * 2;
+    const int su = cfg.shared_ff / 16, ru = cfg.ff / 16, sd = cfg.shared_ff ? d / 16 : 0;
+    const int ma = std::min(B * k, M);
+    trace_rows[l] = R * M + (sgate ? 1 : 0);
+    trace_cats[5 * l + 0] = 0;
+    trace_cats[5 * l + 1] = su;
+    trace_cats[5 * l + 2] = su + ma * ru;
+    trace_cats[5 * l + 3] = su + ma * ru + sd;
+    trace_cats[5 * l + 4] = su + ma * ru + sd + ma * (d / 16);
+    if (trace_rows[l] + trace_cats[5 * l + 4] > kTraceItems) in.trace = nullptr;
+  }
+  in.io.host_done = nullptr;  // published as tagged words (wait_publish)
   CKS(launch_decode_layer(stream, in));
   ++launches;
   if (l + 1 == L) {  // the last layer's combine: no next rmsnorm
@@ -1110,7 +1168,8 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
   mega = mega_ok && fast_path() &&
          decode_layer_supported(cfg.dtype, cfg.d, cfg.ff, cfg.shared_ff, M, k, B);
   if (mega) {  // layer 0's prologue normalises h itself
-    CKS(launch_zero_sync(stream, sync_d, L));
+    ++mega_steps;
+    CKS(launch_zero_sync(stream, sync_d, L, (int)(mega_steps & 1)));
   } else {
     CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
   }
@@ -1152,6 +1211,11 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       HostOut* ho = out(l);
       auto w0 = clk::now();
       unsigned spins = 0;
+      if (mega) {
+        wait_publish(l, B, layer_R[l]);
+        ho->done = 1u;
+        publish_wait_ms += std::chrono::duration<double, std::milli>(clk::now() - w0).count();
+      }
       while (ho->done == 0u) {
         _mm_pause();
         if ((++spins & 0xffff) == 0 &&
@@ -1254,7 +1318,9 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
           enqueue_front(stream, l + 1, B, R1, cur_mask);
           dbg_sync("router/route/shared", l + 1);
         } else {
+          auto e0 = clk::now();
           enqueue_any(stream, l + 1, B, h, R1, cur_mask);
+          enqueue_ms += std::chrono::duration<double, std::milli>(clk::now() - e0).count();
         }
         enq = l + 2;
       } else if (debug) {
@@ -1522,6 +1588,42 @@ void ef_engine::fold_stats(int i) {
       dump_text += line;
     }
   }
+  if (dump && mega && trace_d) {  // work-item summary of the middle layer (us from CTA 0's start)
+    const int j = L / 2;
+    std::vector<unsigned long long> tr(2 * kTraceItems);
+    cudaMemcpy(tr.data(), trace_d + (int64_t)j * kTraceItems * 2, tr.size() * 8, cudaMemcpyDeviceToHost);
+    const double t0 = (double)stats_h[kStats * j + 7];
+    const char* names[5] = {"router", "shared-up", "routed-up", "shared-down", "routed-down"};
+    for (int c = 0; c < 5; ++c) {
+      int lo, hi;
+      if (c == 0) {
+        lo = 0;
+        hi = trace_rows[j];
+      } else {
+        lo = trace_rows[j] + trace_cats[5 * j + c - 1];
+        hi = trace_rows[j] + trace_cats[5 * j + c];
+      }
+      std::vector<double> s0, e0, du;
+      for (int i = lo; i < hi; ++i) {
+        if (!tr[2 * i] || !tr[2 * i + 1] || tr[2 * i + 1] < tr[2 * i]) continue;
+        s0.push_back(((double)tr[2 * i] - t0) * 1e-3);
+        e0.push_back(((double)tr[2 * i + 1] - t0) * 1e-3);
+        du.push_back(((double)tr[2 * i + 1] - (double)tr[2 * i]) * 1e-3);
+      }
+      if (s0.empty()) continue;
+      auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+      char line[256];
+      snprintf(line, sizeof line,
+               "  trace layer %d %-11s n %4zu start min %6.1f med %6.1f max %6.1f | end med %6.1f max "
+               "%6.1f | dur med %5.1f max %5.1f\n",
+               j, names[c], s0.size(), *std::min_element(s0.begin(), s0.end()), med(s0),
+               *std::max_element(s0.begin(), s0.end()), med(e0),
+               *std::max_element(e0.begin(), e0.end()), med(du),
+               *std::max_element(du.begin(), du.end()));
+      dump_text += line;
+    }
+    cudaMemset(trace_d, 0, sizeof(unsigned long long) * 2 * kTraceItems * L);
+  }
   if (dump) {
     double a = 0, b = 0, c = 0;
     for (int j = 1; j < L; ++j) {
@@ -1533,8 +1635,12 @@ void ef_engine::fold_stats(int i) {
     char line[320];
     snprintf(line, sizeof line,
              "router phases (SM cycles, mean over layers 1..): weights-ready %.0f combine %.0f "
-             "gemv %.0f\nstep device time %.3f ms copies %lld\n",
-             a / (L - 1), b / (L - 1), c / (L - 1), ms, (long long)stats_copies[i]);
+             "gemv %.0f\nstep device time %.3f ms copies %lld; host per layer so far: decision "
+             "%.1f us, enqueue %.1f us, publish wait %.1f us\n",
+             a / (L - 1), b / (L - 1), c / (L - 1), ms, (long long)stats_copies[i],
+             1e3 * host_ms / std::max<int64_t>(1, steps * L),
+             1e3 * enqueue_ms / std::max<int64_t>(1, steps * (L - 1)),
+             1e3 * publish_wait_ms / std::max<int64_t>(1, steps * L));
     dump_text += line;
   }
 }
@@ -1945,6 +2051,15 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
         if (c.shared_ff) CK(cudaMalloc(&e->mk_ys[i], (size_t)Bm * d * 4));
       }
       if (preload_decode_layer() < 3) throw CudaErr("could not load the persistent decode layer");
+      if (getenv("EF_MEGA_TRACE")) {
+        CK(cudaMalloc(&e->trace_d, sizeof(unsigned long long) * 2 * ef_engine::kTraceItems * L));
+        e->trace_rows.assign(L, 0);
+        e->trace_cats.assign(5 * L, 0);
+      }
+      e->pub_stride = 4 + (int64_t)Bm * k + (int64_t)L * Bm * M;
+      CK(cudaHostAlloc(&e->pub_h, sizeof(uint64_t) * e->pub_stride * L, cudaHostAllocMapped));
+      std::memset(e->pub_h, 0, sizeof(uint64_t) * e->pub_stride * L);
+      CK(cudaHostGetDevicePointer((void**)&e->pub_dev, e->pub_h, 0));
     }
     e->init_weights();
     if (e->shm_base && !e->store_filled)  // the experts are in: attachers may map them
@@ -2044,7 +2159,7 @@ extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
   EF_TRY({
     e->flush_stats();
     e->poll_copy_times();
-    double v[24] = {(double)e->steps,         (double)e->copies,
+    double v[25] = {(double)e->steps,         (double)e->copies,
                     (double)e->copy_bytes,    e->stall_ms,
                     (double)e->P,             (double)e->st->cache().capacity(),
                     (double)e->cfg.staging_slots, (double)e->launches,
@@ -2055,8 +2170,9 @@ extern "C" int ef_engine_stats(ef_engine* e, double* out, int n) {
                     (double)e->fast_layers,   (double)e->peer_copies,
                     (double)e->peer_bytes,    (double)e->pf_admitted,
                     (double)e->pf_used,       (double)e->pf_wasted,
-                    e->phys_bw->estimate(),   (double)e->phys_observed};
-    for (int i = 0; i < n && i < 24; ++i) out[i] = v[i];
+                    e->phys_bw->estimate(),   (double)e->phys_observed,
+                    (double)e->mega_steps};
+    for (int i = 0; i < n && i < 25; ++i) out[i] = v[i];
   });
 }
 

@@ -121,13 +121,14 @@ int expert_ffn_fused(cudaStream_t st, const float* x, const int32_t* perm, int k
 // previous layer's combine + rmsnorm, the router rows, the route, and the
 // shared + routed expert FFN (gate/up, then down) as a dataflow of work items
 // over a fixed grid (one 512-thread CTA per SM, four 4-warp workers each).
-struct LayerSync {  // per layer, zeroed at the start of every step
+struct LayerSync {  // per layer, zeroed at the start of every step (rq: see launch_zero_sync)
+  int rq[2];        // router row claims, by step parity
   int q;            // next work item
   int ticket;       // router rows finished
   unsigned route;   // == launch seq: the decision block is final
   int sh_up;        // shared-expert gate/up units finished
   int up[kMaxActive];  // routed gate/up units finished, per decision entry
-  int pad[12];
+  int pad[10];
 };
 struct DecodeLayerIn {
   int B, d, ff, sff, M, k, mode, R;  // R router matrices (layer + pre-gate rows)
@@ -170,12 +171,15 @@ struct DecodeLayerIn {
   int max_active;
   LayerSync* sync;
   unsigned long long* stats;
+  void* pub;  // mapped host words of the tagged publish (null: none)
+  int parity; // router-claim counter of this step (launch_zero_sync)
+  void* trace;  // EF_MEGA_TRACE: per work item {start, end} ns, [router rows | queue items]
 };
 bool decode_layer_supported(int dtype, int d, int ff, int sff, int M, int k, int B);
 int launch_decode_layer(cudaStream_t st, const DecodeLayerIn& in);
 int launch_final_combine(cudaStream_t st, const float* h_src, float* h_dst, const float* y,
                          const float* wts, const float* ys, const float* sgl, int B, int d, int k);
-int launch_zero_sync(cudaStream_t st, LayerSync* sync, int L);
+int launch_zero_sync(cudaStream_t st, LayerSync* sync, int L, int parity);
 int preload_decode_layer();
 // expert parallelism (kernels.cu "expert parallelism" section)
 int ep_pack(cudaStream_t st, const float* x, const float* logits, const int32_t* sel,

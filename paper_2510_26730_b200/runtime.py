@@ -278,7 +278,7 @@ class MoEEngine:
                 "staging_slots", "kernel_launches", "host_decision_ms", "ffn_ms", "step_ms",
                 "preload_copies", "d2h_bytes", "ffn_bytes", "ffn_launches", "gate_wait_ms",
                 "fast_layers", "peer_copies", "peer_bytes", "prefetch_admitted", "prefetch_used",
-                "prefetch_wasted", "bw_physical_Bps", "bw_physical_transfers"]
+                "prefetch_wasted", "bw_physical_Bps", "bw_physical_transfers", "layer_kernel_steps"]
         out = (C.c_double * len(keys))()
         L.check(L.lib.ef_engine_stats(self._h.ptr, out, len(keys)))
         return dict(zip(keys, list(out)))

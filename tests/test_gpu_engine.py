@@ -359,6 +359,36 @@ def test_b1_headline_path_numerics(shape):
     assert eng.stats()["fast_layers"] > 0  # the device-resolved (headline) path ran
 
 
+@pytest.mark.parametrize("shape,mega,B", [("qwen", "1", 1), ("qwen", "1", 8), ("qwen", "0", 1),
+                                          ("deepseek", "1", 4), ("mixtral", "2", 1),
+                                          ("tiny", "2", 8)])
+def test_layer_kernel_parity(monkeypatch, shape, mega, B):
+    """The persistent one-launch-per-layer decode kernel (decode_layer.cuh:
+    previous combine + rmsnorm, router rows, the route computed by every
+    worker from the logits, shared + routed expert units on mma.sync) against
+    the oracle: decisions bit-exact, router rows and layer inputs within fp32
+    rounding, outputs within the bf16 tolerance.  EF_MEGA=2 forces it on
+    shapes without a shared expert, EF_MEGA=0 runs the classic pipeline; the
+    engine reports which one ran."""
+    monkeypatch.setenv("EF_MEGA", mega)
+    if shape == "mixtral":
+        cfg, budget = MoEConfig("mixtral-2l", 2, 8, 2, 4096, 14336), 6
+    elif shape == "qwen":
+        cfg = MoEConfig("qwen-3l", 3, 60, 4, 2048, 1408, route_mode="softmax_topk",
+                        shared_ff=5632, shared_gate=True)
+        budget = 72
+    elif shape == "deepseek":
+        cfg = MoEConfig("ds-2l", 2, 64, 6, 2048, 1408, route_mode="softmax_topk", shared_ff=2816)
+        budget = 51
+    else:
+        cfg, budget = PRESETS["tiny-bf16"], 12
+    eng, _ = run_and_check(cfg, ef.PolicyConfig("a", "adaptive", predictor="pregate"), B=B,
+                           steps=3, budget=budget, link_bw=50 * ef.GB, layer_s=1e-4, seed=5,
+                           bias=1e4, timing=True)
+    ran = eng.stats()["layer_kernel_steps"]
+    assert (ran > 0) == (mega != "0"), ran
+
+
 @pytest.mark.parametrize("fuse,pdl", [("0", "1"), ("1", "1"), ("3", "1"), ("11", "0"), ("27", "0"),
                                       ("19", "1")])
 def test_pipeline_variants_parity(monkeypatch, fuse, pdl):

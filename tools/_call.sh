@@ -1,9 +1,10 @@
 #!/bin/bash
-# persistent decode layer: phase timeline (Qwen / Mixtral B=1) + one ncu --set full capture
+# v6: unit load depth A/B, C4 prefill (per-slot fill waits) + decode, layer-kernel parity test, full GPU tests
 cd "$GRAFT_REPO_ROOT"
-for c in qwen1.5-moe-a2.7b:1 mixtral-8x7b:1; do
+for u in 1 0; do
+for c in qwen1.5-moe-a2.7b:1 deepseek-v2-lite:1 qwen1.5-moe-a2.7b:8; do
   cfg=${c%%:*}; b=${c##*:}
-  EF_STATS_DUMP=1 timeout 400 python bench.py --config $cfg --batch $b --steps 6 --warmup 4 --no-grid --no-cpu > gpurun_out/m2_${cfg}_b$b.log 2> gpurun_out/m2_${cfg}_b$b.err; echo "rc=$?" >> gpurun_out/m2_${cfg}_b$b.log
-done
-EF_PIPE_DEBUG=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_layer -s 6 -c 1 -o gpurun_out/m2_ncu_qwen \
-  python tools/profile_decode.py --config qwen1.5-moe-a2.7b --layers 4 --steps 3 --batch 1 > gpurun_out/m2_ncu.log 2>&1; echo "rc=$?" >> gpurun_out/m2_ncu.log
+  EF_MEGA_UDEPTH=$u timeout 400 python bench.py --config $cfg --batch $b --steps 20 --warmup 4 --no-grid --no-cpu > gpurun_out/m7_u${u}_${cfg}_b$b.log 2>&1
+done; done
+timeout 900 python tools/bench_c4.py > gpurun_out/m7_c4.log 2>&1; echo "rc=$?" >> gpurun_out/m7_c4.log
+timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/m7_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/m7_pytest.log
