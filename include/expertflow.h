@@ -103,6 +103,30 @@ int ef_tqueue_next(ef_tqueue* q, int32_t* layer, int32_t* expert, int* priority,
                    int* found);
 int ef_tqueue_len(ef_tqueue* q, int64_t* n);
 
+/* Physical transfer engine (xfer.cu): expert copies pinned host -> HBM issued in
+   TransferQueue order (MISS 0 before PREFETCH 1, FIFO within a class; memory.py:184-202)
+   on a dedicated high-priority copy stream, at most max_inflight outstanding (1 = the
+   reference's serial link, engine.py:328-354), each bracketed by CUDA events; measured
+   rates feed a BandwidthEstimator (alpha 0.25, memory.py:205-236).  Replaces the
+   reference's logical _pump/_advance_to transfer start/finish for a caller running its
+   own scheduler. */
+typedef struct ef_xfer ef_xfer;
+int ef_xfer_create(int32_t device, int32_t max_inflight, ef_xfer** out);
+void ef_xfer_destroy(ef_xfer* x);
+/* queue one copy; *ticket identifies it (0, 1, 2, ... in submission order) */
+int ef_xfer_submit(ef_xfer* x, int32_t layer, int32_t expert, int32_t priority,
+                   const void* src_host, void* dst_dev, int64_t bytes, int64_t* ticket);
+/* issue queued copies while fewer than max_inflight are outstanding */
+int ef_xfer_pump(ef_xfer* x, int32_t* issued);
+/* tickets completed since the last poll, in completion order (pumps first) */
+int ef_xfer_poll(ef_xfer* x, int64_t* tickets, int32_t max, int32_t* n);
+/* block the host until `ticket` has landed (pumping as copies complete) */
+int ef_xfer_wait(ef_xfer* x, int64_t ticket);
+/* make `stream` wait on the device for an issued `ticket` (no host block) */
+int ef_xfer_stream_wait(ef_xfer* x, int64_t ticket, void* stream);
+/* measured bandwidth EWMA in bytes/s (0 before the first completion), copies completed */
+int ef_xfer_bandwidth(ef_xfer* x, double* bytes_per_s, int64_t* completed);
+
 typedef struct ef_bw ef_bw;
 int ef_bw_create(int has_initial, double initial, double alpha, ef_bw** out);
 void ef_bw_destroy(ef_bw* b);

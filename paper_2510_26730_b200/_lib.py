@@ -97,6 +97,14 @@ _SIGS = {
     "ef_tqueue_enqueue": (C.c_int, [vp, i32, i32, C.c_int, P(i64)]),
     "ef_tqueue_next": (C.c_int, [vp, P(i32), P(i32), P(C.c_int), P(i64), P(C.c_int)]),
     "ef_tqueue_len": (C.c_int, [vp, P(i64)]),
+    "ef_xfer_create": (C.c_int, [i32, i32, P(vp)]),
+    "ef_xfer_destroy": (None, [vp]),
+    "ef_xfer_submit": (C.c_int, [vp, i32, i32, i32, vp, vp, i64, P(i64)]),
+    "ef_xfer_pump": (C.c_int, [vp, P(i32)]),
+    "ef_xfer_poll": (C.c_int, [vp, P(i64), i32, P(i32)]),
+    "ef_xfer_wait": (C.c_int, [vp, i64]),
+    "ef_xfer_stream_wait": (C.c_int, [vp, i64, vp]),
+    "ef_xfer_bandwidth": (C.c_int, [vp, P(C.c_double), P(i64)]),
     "ef_bw_create": (C.c_int, [C.c_int, f64, f64, P(vp)]),
     "ef_bw_destroy": (None, [vp]),
     "ef_bw_observe": (C.c_int, [vp, i64, i64, P(f64)]),

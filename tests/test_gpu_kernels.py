@@ -175,3 +175,45 @@ def test_combine_and_rmsnorm():
     L.check(L.lib.ef_rmsnorm(stream(), ptr(th2), ptr(t2), B, d, 1e-6))
     torch.cuda.synchronize()
     assert np.abs(t2.cpu().numpy() - N.rmsnorm(h)).max() < 1e-5
+
+
+@pytest.mark.gpu
+def test_transfer_engine_priority_order_and_bandwidth():
+    """ef_xfer_*: copies land byte-exact, issue in TransferQueue order (every
+    MISS before any PREFETCH, FIFO within a class; memory.py:184-202) on the
+    one-copy link, device-side waits order a consumer stream after a copy,
+    and the measured rate reaches the bandwidth estimate."""
+    import torch
+    n, nbytes = 6, 8 << 20
+    src = [torch.randint(0, 255, (nbytes,), dtype=torch.uint8).pin_memory() for _ in range(n)]
+    dst = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(n)]
+    x = C.c_void_p()
+    L.check(L.lib.ef_xfer_create(0, 1, C.byref(x)))
+    try:
+        prios = [1, 1, 0, 1, 0, 0]  # PREFETCH, PREFETCH, MISS, PREFETCH, MISS, MISS
+        tick = []
+        for i, p in enumerate(prios):
+            t = C.c_int64()
+            L.check(L.lib.ef_xfer_submit(x, 0, i, p, C.c_void_p(src[i].data_ptr()),
+                                         C.c_void_p(dst[i].data_ptr()), nbytes, C.byref(t)))
+            tick.append(t.value)
+        assert tick == list(range(n))
+        st = torch.cuda.Stream()
+        L.check(L.lib.ef_xfer_pump(x, None))
+        L.check(L.lib.ef_xfer_stream_wait(x, 2, C.c_void_p(st.cuda_stream)))  # the first MISS
+        with torch.cuda.stream(st):
+            probe = dst[2].sum(dtype=torch.int64)
+        L.check(L.lib.ef_xfer_wait(x, 3))  # the last PREFETCH: everything has landed
+        buf = (C.c_int64 * n)()
+        got = C.c_int32()
+        L.check(L.lib.ef_xfer_poll(x, buf, n, C.byref(got)))
+        assert list(buf[:got.value]) == [2, 4, 5, 0, 1, 3], list(buf[:got.value])
+        st.synchronize()
+        assert int(probe) == int(src[2].sum(dtype=torch.int64))
+        for i in range(n):
+            assert torch.equal(dst[i].cpu(), src[i])
+        bw, done = C.c_double(), C.c_int64()
+        L.check(L.lib.ef_xfer_bandwidth(x, C.byref(bw), C.byref(done)))
+        assert done.value == n and 1e9 < bw.value < 1e12, bw.value
+    finally:
+        L.lib.ef_xfer_destroy(x)
