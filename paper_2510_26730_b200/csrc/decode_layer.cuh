@@ -253,11 +253,12 @@ __device__ __noinline__ void dl_unit_u(const DlArgs& a, DlSmem& sm, const __nv_b
 }
 
 // a.udepth selects the 32-wide k blocks in flight per warp and iteration:
-// 0 (default) U = 2 gate/up (8 x 16 B per lane), 3 down; 1: U = 4 / 6;
-// 2: U = 1 / 2.  With ~600 workers streaming, fewer loads in flight per
+// 2 (default) U = 1 gate/up (4 x 16 B per lane), 2 down; 0: U = 2 / 3;
+// 1: U = 4 / 6.  With ~600 workers streaming, fewer loads in flight per
 // warp keep the same HBM throughput at a lower queueing latency, which
-// shortens every dependent phase of the layer (B200: Qwen B=8 2321 vs 2204
-// tok/s, DeepSeek B=1 569 vs 552).
+// shortens every dependent phase of the layer (B200, tok/s for depth
+// 1 / 0 / 2: Qwen B=1 671 / 676 / 701, Qwen B=8 2204 / 2321 / 2313,
+// DeepSeek B=1 552 / 569 / 565).
 template <bool UP>
 __device__ __forceinline__ void dl_unit(const DlArgs& a, DlSmem& sm, const __nv_bfloat16* xb,
                                         const __nv_bfloat16* W, int rows_total, int K, int r0,
@@ -923,7 +924,7 @@ int launch_decode_layer(cudaStream_t st, const DecodeLayerIn& in) {
   a.kinter = kinter;
   static const int udepth = [] {
     const char* v = getenv("EF_MEGA_UDEPTH");
-    return v ? atoi(v) : 0;
+    return v ? atoi(v) : 2;
   }();
   a.udepth = udepth;
   a.trace = reinterpret_cast<unsigned long long*>(in.trace);
