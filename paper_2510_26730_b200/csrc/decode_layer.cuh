@@ -98,6 +98,7 @@ struct DlArgs {
   unsigned long long* pub;  // tagged publish words {seq | value << 32} (null: none)
   int hold;                 // shared-expert units wait for the router ticket
   int parity;               // router-claim counter of this step
+  int x_first;              // h / x written before the host publish
   int kinter;               // unit k blocks interleaved across the worker's warps
   int udepth;               // loads in flight per warp (dl_unit)
   unsigned long long* trace;  // EF_MEGA_TRACE: per work item {start, end} ns (null: off)
@@ -475,10 +476,11 @@ __device__ __noinline__ void dl_route(const DlArgs& a, DlSmem& sm, const float* 
         if (st) st[13] = gtimer();
       }
     }
+    // publish first unless the host records x_l (it copies x once it has the selection)
+    if (a.pub && !a.x_first) dl_publish(a, mlo, mhi);
   }
   wbar(1 + wk);
-  // this layer's h and x (every CTA computed the same rows), before the
-  // publish: the host may copy x once it has the selection (record_routing)
+  // this layer's h and x (every CTA computed the same rows)
   for (int i = tw * 4; i < B * a.d; i += 128 * 4) {
     const int t = i / a.d, c = i % a.d;
     const float4 v = *reinterpret_cast<const float4*>(hs + t * a.dp + c);
@@ -486,11 +488,11 @@ __device__ __noinline__ void dl_route(const DlArgs& a, DlSmem& sm, const float* 
     *reinterpret_cast<float4*>(a.h_dst + i) = v;
     *reinterpret_cast<float4*>(a.x_out + i) = make_float4(v.x * sc, v.y * sc, v.z * sc, v.w * sc);
   }
-  __threadfence();
+  if (a.x_first) __threadfence();
   if (a.comb_stamp && tw == 0) *a.comb_stamp = gtimer();
-  wbar(1 + wk);
+  if (a.x_first) wbar(1 + wk);
   if (wl == 0) {
-    if (a.pub) dl_publish(a, mlo, mhi);
+    if (a.pub && a.x_first) dl_publish(a, mlo, mhi);
     // on an unresolved layer: wait for the host's decision block (gate_duty
     // raises sync->route = seq once it is copied); io.host_done is null, so
     // gate_duty does not publish again
@@ -917,6 +919,7 @@ int launch_decode_layer(cudaStream_t st, const DecodeLayerIn& in) {
   }();
   a.hold = hold;
   a.parity = in.parity;
+  a.x_first = in.x_before_publish ? 1 : 0;
   static const int kinter = [] {
     const char* v = getenv("EF_MEGA_KINTER");
     return v ? atoi(v) : 0;

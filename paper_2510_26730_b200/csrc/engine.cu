@@ -404,45 +404,26 @@ struct ef_engine {
     }
   }
 
+  // Copies are booked immediately (slot, fill sequence: the decision block
+  // needs them) but their CUDA calls are deferred while the decode loop
+  // decides a layer (defer_copies) and issued by flush_copies() right after
+  // the next layer's launch: ~15 us of driver calls per expert copy move off
+  // the host's critical path (decision -> go -> next launch).  A demand miss
+  // is a multi-ms stall anyway; the copy starts a few us later.
+  struct PendingCopy {
+    int slot;
+    uint64_t key;
+    uint32_t seq;
+  };
+  bool defer_copies = false;
+  std::vector<PendingCopy> pending_copies;
   void issue_copy(uint64_t key, bool preload) {
     // A free slot's previous readers have all completed (see the header).
     if (free_slots.empty())
       throw RuntimeErr("no free physical expert slot (raise staging_slots)");
     int s = free_slots.front();
     free_slots.pop_front();
-    const int64_t flat = idx(key);
-    CopyTiming ct{nullptr, nullptr, stride};
-    if (ev_pending.size() < 4096) {
-      ct.a = take_event();
-      ct.b = take_event();
-      CK(cudaEventRecord(ct.a, copy_stream));
-    }
-    const int64_t ps = peer_n ? pool_slot_of[flat] : -1;
-    if (ps >= 0) {
-      // miss served from the peer's HBM over NVLink (copy engine, same stream,
-      // so the ready flag below still lands after the blob)
-      CK(cudaMemcpyPeerAsync(slab + (int64_t)s * stride, cfg.device, peer_pool + ps * stride,
-                             peer_dev, stride, copy_stream));
-      ++peer_copies;
-      peer_bytes += stride;
-    } else {
-      const char* src = store[eid_layer(key)] + (int64_t)eid_expert(key) * stride;
-      CK(cudaMemcpyAsync(slab + (int64_t)s * stride, src, stride, cudaMemcpyHostToDevice,
-                         copy_stream));
-    }
-    if (ct.a) {
-      CK(cudaEventRecord(ct.b, copy_stream));
-      ev_pending.push_back(ct);
-    }
     uint32_t seq = ++copy_seq;
-    // Publish the fill sequence with the copy engine (a 4-byte H2D copy from a
-    // pinned ring right behind the blob on the same stream).  A kernel would
-    // need an SM, and the routed FFN waiting on this flag may hold all of them.
-    uint32_t* src_seq = &seq_ring[seq % kSeqRing];
-    *src_seq = seq;
-    CK(cudaMemcpyAsync(ready + s, src_seq, sizeof(uint32_t), cudaMemcpyHostToDevice,
-                       copy_stream));
-    if (track_fills) track_fill(seq);
     slot_seq[s] = seq;
     ++copies;
     copy_bytes += stride;
@@ -452,6 +433,48 @@ struct ef_engine {
     } else {
       inflight_slot = s;
     }
+    pending_copies.push_back(PendingCopy{s, key, seq});
+    if (!defer_copies) flush_copies();
+  }
+  void flush_copies() {
+    const auto ic0 = std::chrono::steady_clock::now();
+    for (const PendingCopy& pc : pending_copies) {
+      const int s = pc.slot;
+      const int64_t flat = idx(pc.key);
+      CopyTiming ct{nullptr, nullptr, stride};
+      if (ev_pending.size() < 4096) {
+        ct.a = take_event();
+        ct.b = take_event();
+        CK(cudaEventRecord(ct.a, copy_stream));
+      }
+      const int64_t ps = peer_n ? pool_slot_of[flat] : -1;
+      if (ps >= 0) {
+        // miss served from the peer's HBM over NVLink (copy engine, same stream,
+        // so the ready flag below still lands after the blob)
+        CK(cudaMemcpyPeerAsync(slab + (int64_t)s * stride, cfg.device, peer_pool + ps * stride,
+                               peer_dev, stride, copy_stream));
+        ++peer_copies;
+        peer_bytes += stride;
+      } else {
+        const char* src = store[eid_layer(pc.key)] + (int64_t)eid_expert(pc.key) * stride;
+        CK(cudaMemcpyAsync(slab + (int64_t)s * stride, src, stride, cudaMemcpyHostToDevice,
+                           copy_stream));
+      }
+      if (ct.a) {
+        CK(cudaEventRecord(ct.b, copy_stream));
+        ev_pending.push_back(ct);
+      }
+      // Publish the fill sequence with the copy engine (a 4-byte H2D copy from a
+      // pinned ring right behind the blob on the same stream).  A kernel would
+      // need an SM, and the routed FFN waiting on this flag may hold all of them.
+      uint32_t* src_seq = &seq_ring[pc.seq % kSeqRing];
+      *src_seq = pc.seq;
+      CK(cudaMemcpyAsync(ready + s, src_seq, sizeof(uint32_t), cudaMemcpyHostToDevice,
+                         copy_stream));
+      if (track_fills) track_fill(pc.seq);
+    }
+    pending_copies.clear();
+    hd_copy_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ic0).count();
   }
 
   // Experts that get the cache-aware routing bias in `layer` (oracle/numerics.py
@@ -554,6 +577,9 @@ struct ef_engine {
   bool mega = false;      // this step runs the persistent layer kernel
   int64_t mega_steps = 0;
   double enqueue_ms = 0, publish_wait_ms = 0;  // host: launch calls / waiting for the publish
+  // host decision breakdown (EF_STATS_DUMP): batch gate of the layer's row,
+  // pre-gate queries, scheduler (run_layer minus the two others), copy issue
+  double hd_gate_ms = 0, hd_pregate_ms = 0, hd_sched_ms = 0, hd_copy_ms = 0, hd_poll_ms = 0;
   // EF_MEGA_TRACE=1: per work item start/end of every layer (the dump prints
   // a summary of one layer); [L][kTraceItems][2]
   static constexpr int kTraceItems = 8192;
@@ -1065,6 +1091,7 @@ void ef_engine::enqueue_mega(cudaStream_t stream, int l, int B, float* h, int R,
   in.sync = sync_d + l;
   in.stats = stats_d + kStats * l;
   in.pub = pub_dev + (int64_t)l * pub_stride;
+  in.x_before_publish = cfg.record_routing == 1;  // the host copies x_l once it has the selection
   in.parity = (int)(mega_steps & 1);
   if (trace_d) {
     in.trace = trace_d + (int64_t)l * kTraceItems * 2;
@@ -1090,8 +1117,15 @@ void ef_engine::enqueue_mega(cudaStream_t stream, int l, int B, float* h, int R,
 }
 
 void ef_engine::abort_pipeline(cudaStream_t stream, int from, int enq) {
-  // Release every enqueued gate with an empty decision so the GPU drains,
-  // then reset the flags for the next step.
+  // Issue the copies the scheduler has booked (its cache counts them in
+  // flight), release every enqueued gate with an empty decision so the GPU
+  // drains, then reset the flags for the next step.
+  defer_copies = false;
+  try {
+    flush_copies();
+  } catch (...) {
+    pending_copies.clear();
+  }
   for (int j = from; j < enq; ++j) {
     hctrl[j].n_active = 0;
     std::atomic_thread_fence(std::memory_order_seq_cst);
@@ -1235,7 +1269,9 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       // ---- scheduler view of this layer's routing (workload.py:161-179 contract)
       LayerRouting r;
       r.gate.resize(M);
+      auto g0 = clk::now();
       batch_gate(lg0, B, M, cfg.routing_bias, cur_mask, r.gate.data());
+      hd_gate_ms += std::chrono::duration<double, std::milli>(clk::now() - g0).count();
       std::vector<int> cnt(M, 0);
       r.group_actual.resize(B);
       for (int t = 0; t < B; ++t) {
@@ -1253,9 +1289,11 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
       d2h_bytes += (int64_t)(B * k + R * B * M) * 4;
       hooks->pregate_fn = [&, R, lg0](int layer, int hz, double* o) {
         if (hz >= R) throw RuntimeErr("pre-gate horizon beyond the scored router rows");
+        auto p0 = clk::now();
         uint64_t m[2];
         scored_mask(layer + hz, lg0 + (int64_t)hz * B * M, B, m);
         batch_gate(lg0 + (int64_t)hz * B * M, B, M, cfg.routing_bias, m, o);
+        hd_pregate_ms += std::chrono::duration<double, std::milli>(clk::now() - p0).count();
       };
       if (cfg.record_routing) {
         // route(l) has completed, so x_d holds x_l until layer l+1 is enqueued
@@ -1282,11 +1320,21 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
           pf_pending[(int64_t)l * M + e] = 0;
           ++pf_used;
         }
-      poll_copy_times();
+      auto q0 = clk::now();
+      // measured copy rates feed the decision only with bandwidth feedback;
+      // otherwise they are polled after the next layer's launch
+      if (simcfg.bw_feedback) poll_copy_times();
+      auto s0 = clk::now();
+      hd_poll_ms += std::chrono::duration<double, std::milli>(s0 - q0).count();
+      const double pg0 = hd_pregate_ms;
+      defer_copies = !debug;  // book now, issue after the next layer's launch
       if (l == 0) st->begin_token(tokens, gsizes, r);
       std::fill(layer_use.begin(), layer_use.end(), -1);
       st->begin_layer(l);
       st->run_layer(l, r);
+      defer_copies = false;
+      hd_sched_ms += std::chrono::duration<double, std::milli>(clk::now() - s0).count() -
+                     (hd_pregate_ms - pg0);
       // ---- publish the decision: slots, rows, copy sequence numbers
       HostCtrl& hc = hctrl[l];
       int n = 0, run = 0;
@@ -1323,7 +1371,15 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
           enqueue_ms += std::chrono::duration<double, std::milli>(clk::now() - e0).count();
         }
         enq = l + 2;
-      } else if (debug) {
+      }
+      // the decision's copies (booked above), then the copy-rate poll
+      flush_copies();
+      if (!simcfg.bw_feedback) {
+        auto q1 = clk::now();
+        poll_copy_times();
+        hd_poll_ms += std::chrono::duration<double, std::milli>(clk::now() - q1).count();
+      }
+      if (l + 1 == L && debug) {
         dbg_sync("copies", l);
         enqueue_back(stream, l, B, h);
         dbg_sync("gate/ffn/combine", l);
@@ -1636,9 +1692,15 @@ void ef_engine::fold_stats(int i) {
     snprintf(line, sizeof line,
              "router phases (SM cycles, mean over layers 1..): weights-ready %.0f combine %.0f "
              "gemv %.0f\nstep device time %.3f ms copies %lld; host per layer so far: decision "
-             "%.1f us, enqueue %.1f us, publish wait %.1f us\n",
+             "%.1f us (gate %.2f, pre-gate %.2f, scheduler %.2f, copy issue %.2f, copy polls %.2f), "
+             "enqueue %.1f us, publish wait %.1f us\n",
              a / (L - 1), b / (L - 1), c / (L - 1), ms, (long long)stats_copies[i],
              1e3 * host_ms / std::max<int64_t>(1, steps * L),
+             1e3 * hd_gate_ms / std::max<int64_t>(1, steps * L),
+             1e3 * hd_pregate_ms / std::max<int64_t>(1, steps * L),
+             1e3 * hd_sched_ms / std::max<int64_t>(1, steps * L),
+             1e3 * hd_copy_ms / std::max<int64_t>(1, steps * L),
+             1e3 * hd_poll_ms / std::max<int64_t>(1, steps * L),
              1e3 * enqueue_ms / std::max<int64_t>(1, steps * (L - 1)),
              1e3 * publish_wait_ms / std::max<int64_t>(1, steps * L));
     dump_text += line;

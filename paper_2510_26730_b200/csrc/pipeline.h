@@ -173,6 +173,7 @@ struct DecodeLayerIn {
   unsigned long long* stats;
   void* pub;  // mapped host words of the tagged publish (null: none)
   int parity; // router-claim counter of this step (launch_zero_sync)
+  bool x_before_publish;  // write h / x before the host publish (the host records x)
   void* trace;  // EF_MEGA_TRACE: per work item {start, end} ns, [router rows | queue items]
 };
 bool decode_layer_supported(int dtype, int d, int ff, int sff, int M, int k, int B);
