@@ -135,6 +135,18 @@ ExpertCache::ExpertCache(int64_t capacity_bytes, int64_t expert_size, bool recor
   if (capacity_ < 1) throw ValueError("capacity cannot hold one expert");
 }
 
+ExpertCache::Node* ExpertCache::alloc_node() {
+  if (free_.empty()) {
+    chunks_.emplace_back(new Node[kChunk]);
+    Node* c = chunks_.back().get();
+    for (int i = kChunk - 1; i >= 0; --i) free_.push_back(c + i);
+  }
+  Node* n = free_.back();
+  free_.pop_back();
+  *n = Node{};
+  return n;
+}
+
 void ExpertCache::unlink(Node* n) {
   List& l = lists_[n->tier];
   (n->prev ? n->prev->next : l.head) = n->next;
@@ -159,7 +171,7 @@ bool ExpertCache::access(uint64_t k, int64_t now) {
     log(now, kEvMiss, k);
     return false;
   }
-  Node* n = it->second.get();
+  Node* n = it->second;
   unlink(n);
   append(n, kHigh);
   n->touch = seq_++;
@@ -174,7 +186,7 @@ std::vector<uint64_t> ExpertCache::admit(uint64_t k, int tier, int64_t now) {
   if (tier != kLow && tier != kHigh) throw ValueError("unknown tier");
   auto it = nodes_.find(k);
   if (it != nodes_.end()) {  // re-admission only re-places
-    Node* n = it->second.get();
+    Node* n = it->second;
     unlink(n);
     append(n, tier);
     n->touch = seq_++;
@@ -187,16 +199,17 @@ std::vector<uint64_t> ExpertCache::admit(uint64_t k, int tier, int64_t now) {
     uint64_t vk = v->key;
     unlink(v);
     nodes_.erase(vk);
+    free_.push_back(v);
     ++evictions;
     log(now, kEvEvict, vk);
     victims.push_back(vk);
   }
-  auto node = std::make_unique<Node>();
+  Node* node = alloc_node();
   node->key = k;
   node->touch = seq_++;
   node->last = now;
-  append(node.get(), tier);
-  nodes_.emplace(k, std::move(node));
+  append(node, tier);
+  nodes_.emplace(k, node);
   ++admissions;
   log(now, kEvAdmit, k);
   return victims;
@@ -207,7 +220,8 @@ void ExpertCache::reassign_tiers(const std::vector<uint64_t>& predicted, int64_t
   // predicted: sorted, unique keys
   // memory.py:137-156: global touch order, then split by the new tier.
   if (window < 0) throw ValueError("recent_window must be >= 0");
-  std::vector<Node*> order;
+  std::vector<Node*>& order = order_;
+  order.clear();
   order.reserve(nodes_.size());
   Node* a = lists_[kLow].head;
   Node* b = lists_[kHigh].head;

@@ -110,7 +110,14 @@ class ExpertCache {
   int64_t seq_ = 0;
   bool record_;
   List lists_[2];
-  std::unordered_map<uint64_t, std::unique_ptr<Node>> nodes_;
+  // nodes live in pooled chunks (locality for the tier walks of
+  // reassign_tiers), recycled through a free list
+  static constexpr int kChunk = 1024;
+  std::vector<std::unique_ptr<Node[]>> chunks_;
+  std::vector<Node*> free_;
+  std::vector<Node*> order_;  // reassign_tiers scratch
+  Node* alloc_node();
+  std::unordered_map<uint64_t, Node*> nodes_;
   std::vector<CacheEvent> events_;
 };
 
