@@ -535,6 +535,10 @@ struct ef_engine {
   // shared-gate logits, double-buffered by layer parity: router(l) writes
   // layer l's while its CTAs still combine layer l-1 with the other buffer
   float* sgl_of(int l) { return sgl_d + (l & 1) * cfg.max_batch; }
+  // the router input x_l, double-buffered by layer parity: with the combine in
+  // its own kernel (EF_FUSE without bit 8), combine(l) writes x_{l+1} while the
+  // host may still be copying x_l for the routing record
+  float* x_of(int l) { return x_d + (int64_t)(l & 1) * cfg.max_batch * cfg.d; }
   uint64_t* fmask_d = nullptr;  // [L][2] final bias mask of each layer (route kernel)
   void enqueue_layer(cudaStream_t stream, int l, int B, float* h, int R, const uint64_t* mask);
   void enqueue_front(cudaStream_t stream, int l, int B, int R, const uint64_t* mask);
@@ -947,7 +951,7 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
     RouteFast rf{&dctrl[l], fast_words + l, layer_seq[l], {}};
     if (fp)
       for (int e = 0; e < M; ++e) rf.tab[e] = host_tab[(int64_t)l * M + e];
-    CKS(router_route_fused(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
+    CKS(router_route_fused(stream, x_of(l), (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype, R,
                            B, d, M, logits_d, stats_d + kStats * l + 7, k, cfg.route_mode,
                            cfg.routing_bias, mask[0], mask[1], cur_topup, fmask_d + 2 * l,
                            fp ? nullptr : dev_of(&out(l)->mask[0]), sel_d, wts_d, counts_d,
@@ -960,11 +964,11 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
                            sgate ? sgl_of(l) : nullptr));  // shared gate = one more router row
     ++launches;
   } else {
-    CKS(router_logits_stamped(stream, x_d, (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype,
+    CKS(router_logits_stamped(stream, x_of(l), (char*)router_w + (int64_t)l * M * d * esz, cfg.dtype,
                               R, B, d, M, logits_d, stats_d + kStats * l + 7));
     ++launches;
     if (sgate) {
-      CKS(ef_router_logits(stream, x_d, (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
+      CKS(ef_router_logits(stream, x_of(l), (char*)sgate_w + (int64_t)l * d * esz, cfg.dtype, 1, B, d,
                            1, sgl_of(l)));
       ++launches;
     }
@@ -978,7 +982,7 @@ void ef_engine::enqueue_front(cudaStream_t stream, int l, int B, int R, const ui
   if (cfg.shared_ff && !ffn_mma) {  // always resident: runs while the host decides the layer
     const char* sw = shared_w + (int64_t)l * sstride;
     int32_t z = 0, nb = B;
-    CKS(expert_ffn_ptrs(stream, x_d, perm_d, k, true, &sw, &z, &nb, 1, d, cfg.shared_ff,
+    CKS(expert_ffn_ptrs(stream, x_of(l), perm_d, k, true, &sw, &z, &nb, 1, d, cfg.shared_ff,
                         cfg.dtype, acts_d, ys_d));
     launches += 2;
   }
@@ -999,15 +1003,15 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
     // the tensor-core FFN carries the layer's shared expert(s) in the same launches
     SharedFfn sh{shared_w + (int64_t)l * sstride, cfg.shared_ff, B, acts_d, ys_d};
     const SharedFfn* shp = ffn_mma && cfg.shared_ff ? &sh : nullptr;
-    CKS(expert_ffn_fused(stream, x_d, perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
+    CKS(expert_ffn_fused(stream, x_of(l), perm_d, k, slab, stride, &hctrl_dev[l], &dctrl[l],
                          reinterpret_cast<volatile unsigned*>(fuse_d + 2), layer_seq[l], ready,
                          stats_d + kStats * l, std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d,
                          y_d, &io, shp));
     launches += 2;
     if (!comb_next) {  // y is in slot order after the fused FFN: no inv
-      // after the last layer there is no next rmsnorm: x_d keeps x_{L-1},
+      // after the last layer there is no next rmsnorm: x_of(L-1) keeps x_{L-1},
       // which the host may still be reading (record_routing) on the fast path
-      CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_d : nullptr, y_d, nullptr, wts_d,
+      CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_of(l + 1) : nullptr, y_d, nullptr, wts_d,
                           cfg.shared_ff ? ys_d : nullptr,
                           sgate ? sgl_of(l) : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
       ++launches;
@@ -1017,12 +1021,12 @@ void ef_engine::enqueue_back(cudaStream_t stream, int l, int B, float* h) {
   CKS(launch_gate(stream, &hctrl_dev[l], &dctrl[l], stats_d + kStats * l));
   ++launches;
   SharedFfn sh{shared_w + (int64_t)l * sstride, cfg.shared_ff, B, acts_d, ys_d};
-  CKS(expert_ffn_ctrl(stream, x_d, perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
+  CKS(expert_ffn_ctrl(stream, x_of(l), perm_d, k, slab, stride, &dctrl[l], ready, stats_d + kStats * l,
                       std::min(B * k, M), B, d, cfg.ff, cfg.dtype, act_d, y_d,
                       ffn_mma && cfg.shared_ff ? &sh : nullptr));
   launches += 2;
   if (comb_next) return;
-  CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_d : nullptr, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
+  CKS(combine_stamped(stream, h, l + 1 < cfg.L ? x_of(l + 1) : nullptr, y_d, inv_d, wts_d, cfg.shared_ff ? ys_d : nullptr,
                       sgate ? sgl_of(l) : nullptr, B, d, k, 1e-6f, stats_d + kStats * l + 5));
   ++launches;
 }
@@ -1051,7 +1055,7 @@ void ef_engine::enqueue_mega(cudaStream_t stream, int l, int B, float* h, int R,
   in.eps = 1e-6f;
   in.h_src = l == 0 ? h : mk_h[prev];
   in.h_dst = mk_h[cur];
-  in.x_out = x_d;
+  in.x_out = x_of(l);
   in.has_prev = l > 0;
   in.y_prev = mk_y[prev];
   in.wts_prev = mk_wts[prev];
@@ -1205,7 +1209,7 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
     ++mega_steps;
     CKS(launch_zero_sync(stream, sync_d, L, (int)(mega_steps & 1)));
   } else {
-    CKS(ef_rmsnorm(stream, h, x_d, B, cfg.d, 1e-6f));
+    CKS(ef_rmsnorm(stream, h, x_of(0), B, cfg.d, 1e-6f));
   }
   launches += 2;
   mask_tokens = B;
@@ -1296,12 +1300,12 @@ void ef_engine::step_on(cudaStream_t stream, float* h, int B,
         hd_pregate_ms += std::chrono::duration<double, std::milli>(clk::now() - p0).count();
       };
       if (cfg.record_routing) {
-        // route(l) has completed, so x_d holds x_l until layer l+1 is enqueued
+        // route(l) has completed, so x_of(l) holds x_l until layer l+2 is enqueued
         std::vector<float> lg(lg0, lg0 + (int64_t)R * B * M);
         rlog.push_back(RoutingRec{std::move(lg), std::vector<int32_t>(sel, sel + B * k), R, B,
                                   cur_mask[0], cur_mask[1],
                                   cfg.record_routing == 2 ? std::vector<float>()
-                                                          : record_x(x_d, (int64_t)B * cfg.d),
+                                                          : record_x(x_of(l), (int64_t)B * cfg.d),
                                   mask_tokens});
       }
       // the route kernel may have started FFN(l) on the slots of its table
@@ -1968,7 +1972,7 @@ extern "C" int ef_engine_create(const ef_engine_cfg* cfg, const ef_sim_cfg* sim,
       CK(cudaMalloc(&e->acts_d, (size_t)B * c.shared_ff * e->esz));
       CK(cudaMalloc(&e->ys_d, (size_t)B * d * 4));
     }
-    CK(cudaMalloc(&e->x_d, (size_t)B * d * 4));
+    CK(cudaMalloc(&e->x_d, (size_t)2 * B * d * 4));  // x_of(l): by layer parity
     CK(cudaMalloc(&e->h_io_d, (size_t)B * d * 4));
     e->max_prefill = c.max_prefill;
     if (c.max_prefill > 0) {
