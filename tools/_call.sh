@@ -1,6 +1,5 @@
 #!/bin/bash
-# Mixtral B=1: persistent layer kernel forced (EF_MEGA=2) vs the classic pipeline, 2 reps each
+# refresh the classic pipeline's router capture (headline path, Mixtral B=1): router_route_row_kernel --set full
 cd "$GRAFT_REPO_ROOT"
-for rep in 1 2; do for m in 2 1; do
-  EF_MEGA=$m timeout 400 python bench.py --config mixtral-8x7b --batch 1 --steps 20 --warmup 4 --no-grid --no-cpu > gpurun_out/x_m${m}_$rep.log 2>&1
-done; done
+EF_PIPE_DEBUG=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:router_route -s 8 -c 1 -o gpurun_out/r2_ncu_router \
+  python tools/profile_decode.py --config mixtral-8x7b --layers 4 --steps 3 --batch 1 > gpurun_out/r2_ncu_router.log 2>&1; echo "rc=$?" >> gpurun_out/r2_ncu_router.log
